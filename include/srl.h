@@ -1,0 +1,205 @@
+/* srl.h — C ABI of the SortedRL rollout engine (B200 / sm_100a).
+ *
+ * The engine runs the rollout phase of SortedRL (arXiv 2603.23414): batched
+ * autoregressive decode of a policy under online length-aware continuous
+ * batching, with the paper's stateful controller and rollout buffer.
+ * Citations "P:n" are PAPER.md line numbers; "Rn" are DESIGN.md readings.
+ *
+ *   srl_submit_prompts      feed the dataloader stream (P:147 step 1)
+ *   srl_decode_step         one global decode step: refill free slots from the
+ *                           pending queue (oversubscription), decode,
+ *                           sample, stop-detect, compact finished sequences into
+ *                           the rollout buffer, early-terminate when an update
+ *                           group is ready
+ *   srl_harvest_finished    the length-sorted update group (selective batching,
+ *                           P:177) with tokens + behaviour logprobs
+ *   srl_load_policy_weights refresh the policy after an update and apply the
+ *                           off-policy cache bound K
+ *
+ * Conventions
+ *   - Every call returns int32: SRL_OK (0), an informational status (> 0), or
+ *     an error (< 0).  srl_last_error() describes the last error of the
+ *     calling thread.  No C++ exception crosses this boundary.
+ *   - One engine per GPU per process; an engine is NOT thread-safe (single
+ *     owner).
+ *   - Host arrays passed IN are copied before the call returns.  OUT arrays are
+ *     caller-owned with an explicit capacity; counts are returned separately.
+ *   - Device memory is allocated by the caller (the Python wrapper, via torch)
+ *     and lent to the engine for its lifetime (srl_arena); the engine never
+ *     frees it.  Sizes come from srl_arena_sizes().  `stream` is a
+ *     cudaStream_t owned by the caller.
+ *   - srl_decode_step, srl_harvest_finished and srl_load_policy_weights
+ *     synchronise `stream` before returning (their results are host values).
+ */
+#ifndef SRL_H
+#define SRL_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes */
+#define SRL_OK 0
+#define SRL_GROUP_READY 1 /* an update group is ready: harvest, then load weights */
+#define SRL_DONE 2        /* stream exhausted and every trajectory emitted */
+#define SRL_E_INVALID_ARG (-1)
+#define SRL_E_STATE (-2)     /* call not allowed in the current state */
+#define SRL_E_EMPTY (-3)     /* nothing submitted */
+#define SRL_E_CAPACITY (-4)  /* buffer / KV pool too small */
+#define SRL_E_DUPLICATE_ID (-5)
+#define SRL_E_CUDA (-6)
+#define SRL_E_NCCL (-7)
+
+/* ---- enums */
+enum { SRL_MODE_SORTED = 0, SRL_MODE_SYNC = 1 };
+enum { SRL_RESUME_KEEP_KV = 0, SRL_RESUME_REPREFILL = 1 };   /* reading R10 */
+enum { SRL_BARRIER_TRAINED = 0, SRL_BARRIER_ADMITTED = 1 };  /* reading R8 */
+enum { SRL_STOP_FORCED = 0, SRL_STOP_EOS = 1 };              /* reading R16 */
+enum { SRL_KV_BF16 = 0, SRL_KV_FP32 = 1 };
+
+/* Policy shape (LLaMA-3.1 / Qwen-2.5 family; reading R19). */
+typedef struct srl_model_cfg {
+  int32_t L, d, Hq, Hkv, dh, ff, V;
+  float rope_theta, rms_eps;
+  int32_t qkv_bias; /* Qwen-2.5 has q/k/v biases */
+} srl_model_cfg;
+
+/* Scheduler.  Q_g slots per GPU, Q_tot = R * Q_g ("Q").
+ * U   update-group size
+ * K   cache bound in policy versions; -1 = infinity.  K = 0 is the paper's fully
+ *     on-policy mode, K = -1 its partial mode; reading R9.
+ * pool_prompts  n*b prompts loaded per epoch, G responses per prompt.
+ * cap           max generation length; page_tokens must be 64.
+ * kv_pages      KV pages per GPU; max_traj capacity of the trajectory table;
+ * max_prompt    longest prompt accepted; prefill_chunk rows per prefill pass. */
+typedef struct srl_sched_cfg {
+  int32_t Q_g, U, K, pool_prompts, G, cap, page_tokens, kv_pages;
+  int32_t mode, resume, barrier, stop, eos_id, kv_dtype;
+  float temperature;
+  uint64_t sample_seed;
+  int32_t max_traj, max_prompt, prefill_chunk;
+} srl_sched_cfg;
+
+/* Data-parallel replica identity (R > 1 uses NCCL). */
+typedef struct srl_comm {
+  int32_t rank, world;
+  uint8_t nccl_unique_id[128]; /* from ncclGetUniqueId on rank 0, shared by the caller */
+} srl_comm;
+
+/* Device memory lent by the caller, sized by srl_arena_sizes. */
+typedef struct srl_arena {
+  void* weights;  /* flat policy weights, layout from srl_weight_offset */
+  void* kv;       /* KV cache pool */
+  void* scratch;  /* activations, partials, controller state, buffers */
+  uint64_t weights_bytes, kv_bytes, scratch_bytes;
+} srl_arena;
+
+typedef struct srl_step_info {
+  int64_t k;          /* global step index of the step just run (-1 if none) */
+  int32_t r_k;        /* running requests in that step (Eq. (bubble)) */
+  int32_t n_finished; /* trajectories finished in that step */
+  int32_t n_ready;    /* ready (finished, not emitted) trajectories */
+  int32_t n_admitted; /* admissions in that step (all replicas) */
+  int32_t n_prefill_tokens; /* prefill tokens processed on this GPU */
+  int32_t v;          /* current policy version */
+  float dt_ms;        /* device time of the step on this GPU (cudaEvent) */
+} srl_step_info;
+
+/* One harvested trajectory (SPEC BufferEntry / P:199). */
+typedef struct srl_traj {
+  int64_t prompt_id;   /* the caller's prompt id */
+  int64_t tok_offset;  /* offset of its tokens in the caller's toks/logprobs/versions */
+  int32_t traj_id, sample, len;
+  int32_t v_first, v_last, finish_step, lifecycle, restarts;
+  int32_t final_group; /* 1 when this is the epoch's final (possibly short) group */
+  int32_t epoch;
+} srl_traj;
+
+/* Trace records: kind 0 = step (a = k, b = r_k); events (P:338 trace). */
+enum { SRL_EV_STEP = 0, SRL_EV_LOAD = 1, SRL_EV_ADMIT = 2, SRL_EV_PREEMPT = 3, SRL_EV_FINISH = 4,
+       SRL_EV_EMIT = 5, SRL_EV_DISCARD = 6, SRL_EV_SCAVENGE = 7, SRL_EV_EMIT_MEMBER = 8 };
+typedef struct srl_trace_rec {
+  int32_t kind, a, b, c, d, e;
+} srl_trace_rec;
+/* Field meaning per kind:
+ *   STEP        a=k, b=r_k
+ *   LOAD        a=k, b=epoch, c=first traj_id, d=count
+ *   ADMIT       a=k, b=global slot, c=traj_id, d=kept tokens
+ *   PREEMPT     a=k, b=global slot, c=traj_id, d=tokens kept (0/1)
+ *   FINISH      a=k, b=global slot, c=traj_id, d=length
+ *   EMIT        a=group index, b=version, c=count, d=final flag   (followed by c EMIT_MEMBER)
+ *   EMIT_MEMBER a=group index, b=position in group, c=traj_id
+ *   DISCARD     a=version, b=traj_id, c=where (1 pending, 2 running, 3 ready)
+ *   SCAVENGE    a=version, b=traj_id, c=global slot */
+
+typedef struct srl_engine srl_engine;
+
+/* Byte sizes of the three arena regions for a configuration.  Returns < 0 for
+ * an invalid configuration (Q_g <= 0, U > pool*G in SORTED mode, ...). */
+int32_t srl_arena_sizes(const srl_model_cfg* m, const srl_sched_cfg* s, int32_t world, uint64_t* weights_bytes,
+                        uint64_t* kv_bytes, uint64_t* scratch_bytes);
+
+/* Byte offset and element count of a named weight tensor inside the flat
+ * weight region ("embed", "lm_head", "final_norm", "L<i>.wq", "L<i>.wk",
+ * "L<i>.wv", "L<i>.bq", "L<i>.bk", "L<i>.bv", "L<i>.wo", "L<i>.attn_norm",
+ * "L<i>.mlp_norm", "L<i>.wg", "L<i>.wu", "L<i>.wd"), all bf16 row-major in the
+ * shapes of a linear layer's weight [out, in].  Returns -1 if unknown. */
+int64_t srl_weight_offset(const srl_model_cfg* m, const char* name, int64_t* numel);
+
+int32_t srl_create(const srl_model_cfg* m, const srl_sched_cfg* s, int32_t device, void* stream,
+                   const srl_arena* mem, const srl_comm* comm /* NULL => R = 1 */, srl_engine** out);
+int32_t srl_destroy(srl_engine* e);
+
+/* Append n prompts to the stream.  Prompt i has tokens toks[tok_off[i] .. tok_off[i+1])
+ * (host arrays); trajectory ids are prompt_index*G + sample in submission order.
+ * forced_len[n*G] (host; required in FORCED stop mode, each in [1, cap]).
+ * All ranks must submit identical lists.  Errors: SRL_E_DUPLICATE_ID,
+ * SRL_E_INVALID_ARG, SRL_E_CAPACITY (max_traj / prompt storage exceeded). */
+int32_t srl_submit_prompts(srl_engine* e, int32_t n, const uint64_t* prompt_ids, const int32_t* tok_off,
+                           const int32_t* toks, const int32_t* forced_len);
+
+/* One global decode step.  Returns SRL_OK, SRL_GROUP_READY, SRL_DONE, or
+ * SRL_E_STATE (a group awaits harvest/load, or no weights loaded),
+ * SRL_E_EMPTY, SRL_E_CAPACITY.  `info` (optional) receives the step summary. */
+int32_t srl_decode_step(srl_engine* e, srl_step_info* info);
+
+/* Copy out the ready update group: records in group order (ascending
+ * (len, traj_id) in SORTED mode; completion order in SYNC mode), and the
+ * concatenated tokens / behaviour logprobs / generating policy versions.
+ * Returns SRL_E_STATE when no group is ready and SRL_E_CAPACITY (nothing
+ * consumed) when cap_recs or cap_toks is too small. */
+int32_t srl_harvest_finished(srl_engine* e, int32_t cap_recs, srl_traj* recs, int32_t* n_out, int32_t* toks,
+                             float* logprobs, int32_t* versions, int64_t cap_toks);
+
+/* Collective over the replicas.  Install policy version `version` (> current;
+ * the first call may use any version >= 0).  flat_w: device pointer to a flat
+ * weight image (srl_weight_offset layout) on rank 0 (ignored elsewhere), or
+ * NULL when the caller already wrote the engine's weight region.  Then applies
+ * the cache bound: trajectories with version - v_first > K are discarded and
+ * re-queued (tokens dropped); under REPREFILL running ones are scavenged.
+ * SRL_E_STATE if a group is ready but not harvested or version <= current. */
+int32_t srl_load_policy_weights(srl_engine* e, const void* flat_w, int64_t version);
+
+/* Trace / event log since record index `from` (see srl_trace_rec).  *n_out
+ * receives the number copied; *n_total the total recorded. */
+int32_t srl_get_trace(srl_engine* e, int64_t from, int32_t cap, srl_trace_rec* out, int32_t* n_out,
+                      int64_t* n_total);
+
+/* Counters: raw generated tokens, discarded tokens, emitted trajectories,
+ * groups, device-side kernel launches issued by the engine. */
+int32_t srl_get_counters(srl_engine* e, int64_t* raw_tokens, int64_t* discarded_tokens, int64_t* emitted,
+                         int64_t* groups, int64_t* kernel_launches);
+
+/* Change K between updates (SRL_E_STATE while a group is pending). */
+int32_t srl_set_cache_bound(srl_engine* e, int32_t K);
+
+/* Test accessor: copy the fp32 logits [Q_g, V] of the last decode step (local
+ * slots; rows of empty slots are unspecified) to host memory. */
+int32_t srl_debug_copy_logits(srl_engine* e, float* out_host, int64_t cap_floats);
+
+const char* srl_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,65 @@
+/* srl_ops.h — op-level C ABI of the SortedRL rollout hot path (sm_100a).
+ *
+ * These are the individual device steps that srl_decode_step (srl.h) chains;
+ * they are exported so that tests can check each step against the CPU oracle
+ * in isolation.  Conventions (same as srl.h):
+ *   - every pointer argument is a DEVICE pointer unless its name ends in _host;
+ *   - tensors are dense row-major, the last listed dimension contiguous;
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream); calls are
+ *     asynchronous on that stream and never synchronise;
+ *   - the return value is 0 on success, < 0 on a rejected argument or launch
+ *     failure (see srl_last_error()); no output is written when < 0 is returned
+ *     for an argument error.
+ *   - memory is owned by the caller; nothing is retained after return.
+ */
+#ifndef SRL_OPS_H
+#define SRL_OPS_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Decode projection GEMM, split-K partials (
+ * PAPER.md P:110 §2.2 "frequent loading of model weights").
+ *   X   [M, K] bf16, W [N, K] bf16 (a linear layer's weight, y = x W^T),
+ *   out [splits, M, N] fp32: out[s][m][n] = sum over the s-th contiguous
+ *       K/64-block range of X[m][k]*W[n][k].  Sum the splits (in order) for Y.
+ *   Requires K % 64 == 0, 1 <= splits <= K/64, M >= 0, N >= 0.
+ *   tcgen05.mma (kind::f16, fp32 accumulate in TMEM), operands staged by TMA. */
+int32_t srl_op_gemm_bf16(const void* X, int32_t M, const void* W, int32_t N, int32_t K, float* out,
+                         int32_t splits, void* stream);
+
+/* Split count the engine would choose for an [M,N,K] GEMM on `num_sms` SMs. */
+int32_t srl_op_gemm_splits(int32_t M, int32_t N, int32_t K, int32_t num_sms);
+
+/* Paged decode attention with GQA (PagedAttention).
+ *   q          [M, Hq, dh]  bf16 (kv_fp32 = 0) or fp32 (kv_fp32 = 1)
+ *   k_pool, v_pool [n_pages, Hkv, 64, dh] same dtype as q
+ *   page_table [M, max_pages] int32: row r's token j lives in page page_table[r][j/64], row j%64
+ *   row_pos    [M] int32: query position; ctx = row_pos+1 tokens are attended (row_pos < 0: output 0)
+ *   out_f32    [M, Hq, dh] fp32: softmax_j(q . K_j / sqrt(dh)) V_j, query head h uses kv head h/(Hq/Hkv)
+ *   workspace  device bytes >= srl_op_attention_workspace(M, Hq, Hkv, dh, max_ctx)
+ * Requires dh in {32, 64, 128}, Hq/Hkv <= 8, max_ctx >= every ctx, max_pages*64 >= max_ctx. */
+int64_t srl_op_attention_workspace(int32_t M, int32_t Hq, int32_t Hkv, int32_t dh, int32_t max_ctx);
+int32_t srl_op_attention(const void* q, const void* k_pool, const void* v_pool, int32_t n_pages,
+                         const int32_t* page_table, int32_t max_pages, const int32_t* row_pos, int32_t M,
+                         int32_t Hq, int32_t Hkv, int32_t dh, int32_t kv_fp32, int32_t max_ctx, void* workspace,
+                         float* out_f32, void* stream);
+
+/* Seeded Gumbel-max sampling + log-probability.
+ *   logits [M, V] fp32; per row r: n = row_n[r] (index of the generated token),
+ *   traj = row_traj[r], restarts = row_restarts[r]; rows with row_active[r] < 0 are skipped
+ *   (tok_out = -1).  tok_out[r] = argmax_j(z_j/T + Gumbel_j) with Gumbel_j from
+ *   Philox4x32-10(key = seed, counter = (j>>2, n, traj, restarts))[j&3], ties -> lowest j;
+ *   lp_out[r] = log softmax(z/T)[tok]. */
+int32_t srl_op_sample(const float* logits, int32_t M, int32_t V, const int32_t* row_n, const int32_t* row_traj,
+                      const int32_t* row_restarts, float temperature, uint64_t seed, const int32_t* row_active,
+                      int32_t* tok_out, float* lp_out, void* stream);
+
+/* Thread-local description of the last error (never NULL). */
+const char* srl_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -163,6 +163,7 @@ class ModelRunner:
         self.record_logits = record_logits
         self.log = []
         self._models = {}
+        self.k = 0           # steps served
 
     def model(self, version):
         if version not in self._models:
@@ -193,8 +194,10 @@ class ModelRunner:
             z = mdl.logits(x).astype(np.float32)
             tok, lp, s = sample_row(z, self.invT, self.seed, n, t.tid, t.restarts)
             if self.record_logits:
-                self.log.append(dict(tid=t.tid, n=n, logits=z, tok=tok, lp=lp, scores=s))
+                self.log.append(dict(k=self.k, g=g, tid=t.tid, n=n, restarts=t.restarts, logits=z, tok=tok, lp=lp,
+                                     scores=s))
             if self.teacher is not None:
                 tok = self.teacher[t.tid][n]
             outs.append((tok, lp))
+        self.k += 1
         return outs

@@ -1,0 +1,471 @@
+// attention.cu — paged decode attention with GQA and split-KV (SURVEY §8(a)
+// a6; "loading of model weights and KV caches"
+// PagedAttention).  For each row r (a sequence at position pos_r, ctx =
+// pos_r + 1) and query head h with kv head h / G:
+//     o[r,h] = softmax_j(q[r,h] . K_j / sqrt(dh)) V_j ,  j < ctx
+// Work item = (row, kv head, chunk of kChunkPages 64-token pages).
+//
+// bf16 KV (the production path): a persistent kernel; one producer warp
+// streams (page, head) K/V blocks with 2-D TMA (128B swizzle) into a 4-stage
+// mbarrier ring, four consumer warps each take 16 tokens of the page and use
+// mma.sync m16n8k16 with the KV tokens on the M side and the G query heads
+// of the kv head on N (S^T = K Q^T; O^T += V^T P^T, P^T transposed in
+// registers with movmatrix), warp-shuffle online softmax in the log2 domain,
+// and a cross-warp merge.  Per-chunk partials (o, m, l) are merged by
+// attn_combine in chunk order.
+// fp32 KV (test mode): a plain FFMA kernel with the same item/partial format.
+#include "common.cuh"
+#include "layers.hpp"
+#include "tma.hpp"
+
+namespace srl {
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+// ---------------------------------------------------------------- plan
+__global__ void attn_plan_kernel(AttnArgs a, int split) {
+  __shared__ int wsum[32];
+  __shared__ int base_s;
+  if (threadIdx.x == 0) base_s = 0;
+  __syncthreads();
+  const int chunk_tok = 64 * kChunkPages;
+  for (int b0 = 0; b0 < a.M; b0 += blockDim.x) {
+    const int m = b0 + threadIdx.x;
+    int nch = 0;
+    if (m < a.M) {
+      const int ctx = a.row_pos[m] + 1;
+      nch = ctx <= 0 ? 0 : (split ? (ctx + chunk_tok - 1) / chunk_tok : 1);
+    }
+    const int cnt = nch * a.Hkv;
+    // block exclusive scan of cnt
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int x = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int s = wsum[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= o) s += y;
+      }
+      wsum[lane] = s;
+    }
+    __syncthreads();
+    const int excl = base_s + (w ? wsum[w - 1] : 0) + x - cnt;
+    if (m < a.M) {
+      a.row_item0[m] = excl;
+      a.row_nchunk[m] = nch;
+      for (int h = 0; h < a.Hkv; ++h)
+        for (int c = 0; c < nch; ++c) {
+          const int it = excl + h * nch + c;
+          if (it < a.max_items) {
+            a.items[it * 3 + 0] = m;
+            a.items[it * 3 + 1] = h;
+            a.items[it * 3 + 2] = c;
+          }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) base_s += wsum[31];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *a.n_items = min(base_s, a.max_items);
+}
+
+int attn_max_items(int M, int Hkv, int max_ctx) {
+  const int chunk_tok = 64 * kChunkPages;
+  return M * Hkv * ((max_ctx + chunk_tok - 1) / chunk_tok);
+}
+
+// ---------------------------------------------------------------- combine
+template <bool F32OUT>
+__global__ void attn_combine_kernel(AttnArgs a, float* out_f32) {
+  const int G = a.Hq / a.Hkv;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (gw >= a.M * a.Hq) return;
+  const int m = gw / a.Hq, h = gw % a.Hq;
+  const int kvh = h / G, g = h % G;
+  const int nch = a.row_nchunk[m];
+  if (nch == 0) {
+    for (int d = lane; d < a.dh; d += 32) {
+      if (F32OUT) out_f32[((size_t)m * a.Hq + h) * a.dh + d] = 0.f;
+      a.out[((size_t)m * a.Hq + h) * a.dh + d] = __float2bfloat16(0.f);
+    }
+    return;
+  }
+  const int it0 = a.row_item0[m] + kvh * nch;
+  float mx = -INFINITY;
+  for (int c = 0; c < nch; ++c) mx = fmaxf(mx, a.part_ml[((size_t)(it0 + c) * G + g) * 2 + 0]);
+  float l = 0.f;
+  for (int c = 0; c < nch; ++c) {
+    const float* ml = a.part_ml + ((size_t)(it0 + c) * G + g) * 2;
+    l += ml[1] * exp2f(ml[0] - mx);
+  }
+  const float inv = 1.f / l;
+  for (int d = lane; d < a.dh; d += 32) {
+    float acc = 0.f;
+    for (int c = 0; c < nch; ++c) {
+      const float mc = a.part_ml[((size_t)(it0 + c) * G + g) * 2 + 0];
+      acc += a.part_o[((size_t)(it0 + c) * G + g) * a.dh + d] * exp2f(mc - mx);
+    }
+    const float o = acc * inv;
+    if (F32OUT) out_f32[((size_t)m * a.Hq + h) * a.dh + d] = o;
+    a.out[((size_t)m * a.Hq + h) * a.dh + d] = __float2bfloat16(o);
+  }
+}
+
+// ---------------------------------------------------------------- fp32 KV (FFMA, test mode)
+constexpr int kF32Threads = 128;
+__global__ void __launch_bounds__(kF32Threads) attn_f32_kernel(AttnArgs a) {
+  extern __shared__ float sm[];
+  const int G = a.Hq / a.Hkv;
+  const int chunk_tok = 64 * kChunkPages;
+  float* sq = sm;                       // [G][dh]
+  float* ss = sq + G * a.dh;            // [G][chunk_tok]
+  const int n_items = *a.n_items;
+  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    const int m = a.items[it * 3], kvh = a.items[it * 3 + 1], c = a.items[it * 3 + 2];
+    const int ctx = a.row_pos[m] + 1;
+    const int nch = a.row_nchunk[m];
+    const int t0 = nch == 1 ? 0 : c * chunk_tok;
+    const int t1 = nch == 1 ? ctx : min(ctx, t0 + chunk_tok);
+    const int slot = a.row_slot[m];
+    const float* qrow = reinterpret_cast<const float*>(a.q) + ((size_t)m * a.Hq + kvh * G) * a.dh;
+    const float* kp = reinterpret_cast<const float*>(a.k_pool);
+    const float* vp = reinterpret_cast<const float*>(a.v_pool);
+    __syncthreads();
+    for (int i = threadIdx.x; i < G * a.dh; i += blockDim.x) sq[i] = qrow[i];
+    float run_m[8], run_l[8];
+    for (int g = 0; g < G; ++g) {
+      run_m[g] = -INFINITY;
+      run_l[g] = 0.f;
+    }
+    // o accumulators: thread owns (g, d) pairs i = threadIdx.x + k*blockDim
+    float acc[8];
+    for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+    for (int b0 = t0; b0 < t1; b0 += chunk_tok) {
+      const int b1 = min(t1, b0 + chunk_tok);
+      __syncthreads();
+      const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      for (int j = b0 + w; j < b1; j += kF32Threads / 32) {
+        const int page = a.page_table[(size_t)slot * a.max_pages + j / 64];
+        const float* krow = kp + (((size_t)page * a.Hkv + kvh) * 64 + j % 64) * a.dh;
+        for (int g = 0; g < G; ++g) {
+          float p = 0.f;
+          for (int d = lane; d < a.dh; d += 32) p += sq[g * a.dh + d] * krow[d];
+          for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+          if (lane == 0) ss[g * chunk_tok + (j - b0)] = p * a.scale * kLog2e;
+        }
+      }
+      __syncthreads();
+      for (int g = 0; g < G; ++g) {
+        float bm = -INFINITY;
+        for (int j = 0; j < b1 - b0; ++j) bm = fmaxf(bm, ss[g * chunk_tok + j]);
+        const float nm = fmaxf(run_m[g], bm);
+        const float alpha = run_m[g] == -INFINITY ? 0.f : exp2f(run_m[g] - nm);
+        float lsum = 0.f;
+        for (int j = 0; j < b1 - b0; ++j) lsum += exp2f(ss[g * chunk_tok + j] - nm);
+        run_l[g] = run_l[g] * alpha + lsum;
+        for (int k = 0; k < 8; ++k) {
+          const int i = threadIdx.x + k * blockDim.x;
+          if (i < G * a.dh && i / a.dh == g) acc[k] *= alpha;
+        }
+        run_m[g] = nm;
+      }
+      for (int k = 0; k < 8; ++k) {
+        const int i = threadIdx.x + k * blockDim.x;
+        if (i >= G * a.dh) break;
+        const int g = i / a.dh, d = i % a.dh;
+        float o = acc[k];
+        for (int j = b0; j < b1; ++j) {
+          const int page = a.page_table[(size_t)slot * a.max_pages + j / 64];
+          const float v = vp[(((size_t)page * a.Hkv + kvh) * 64 + j % 64) * a.dh + d];
+          o += exp2f(ss[g * chunk_tok + (j - b0)] - run_m[g]) * v;
+        }
+        acc[k] = o;
+      }
+    }
+    for (int k = 0; k < 8; ++k) {
+      const int i = threadIdx.x + k * blockDim.x;
+      if (i >= G * a.dh) break;
+      a.part_o[(size_t)it * G * a.dh + i] = acc[k];
+    }
+    if (threadIdx.x < G) {
+      a.part_ml[((size_t)it * G + threadIdx.x) * 2 + 0] = run_m[threadIdx.x];
+      a.part_ml[((size_t)it * G + threadIdx.x) * 2 + 1] = run_l[threadIdx.x];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- bf16 KV (TMA + mma.sync)
+constexpr int kStages = 4;
+constexpr int kConsumerWarps = 4;
+constexpr int kAttnThreads = (kConsumerWarps + 1) * 32;
+
+template <int DH>
+struct AttnCfg {
+  static constexpr int kBoxCols = DH < 64 ? DH : 64;       // elements per TMA box row
+  static constexpr int kBoxes = DH / kBoxCols;             // boxes per 64-token block
+  static constexpr int kBoxBytes = 64 * kBoxCols * 2;
+  static constexpr int kBlockBytes = kBoxes * kBoxBytes;   // one page x one head, K or V
+  static constexpr int kStageBytes = 2 * kBlockBytes;      // K + V
+  static constexpr bool kSwz = kBoxCols == 64;             // 128B swizzle
+};
+
+template <int DH>
+__device__ __forceinline__ uint32_t kv_addr(uint32_t block_base, int tok, int chunk16) {
+  using C = AttnCfg<DH>;
+  constexpr int kChunksPerBox = C::kBoxCols / 8;
+  const int b = chunk16 / kChunksPerBox, c = chunk16 % kChunksPerBox;
+  const int cc = C::kSwz ? (c ^ (tok & 7)) : c;
+  return block_base + b * C::kBoxBytes + tok * (C::kBoxCols * 2) + (cc << 4);
+}
+
+struct ItemInfo {
+  int m, kvh, p0, p1, ctx, slot;
+};
+
+__device__ __forceinline__ ItemInfo item_info(const AttnArgs& a, int it) {
+  ItemInfo r;
+  r.m = a.items[it * 3];
+  r.kvh = a.items[it * 3 + 1];
+  const int c = a.items[it * 3 + 2];
+  r.ctx = a.row_pos[r.m] + 1;
+  const int npages = (r.ctx + 63) / 64;
+  if (a.row_nchunk[r.m] == 1) {
+    r.p0 = 0;
+    r.p1 = npages;
+  } else {
+    r.p0 = c * kChunkPages;
+    r.p1 = min(npages, r.p0 + kChunkPages);
+  }
+  r.slot = a.row_slot[r.m];
+  return r;
+}
+
+template <int DH>
+__global__ void __launch_bounds__(kAttnThreads, 1)
+    attn_bf16_kernel(AttnArgs a, const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV) {
+  using C = AttnCfg<DH>;
+  constexpr int MT = DH / 16;  // 16-dim tiles
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stages = smem;
+  float* mrg = reinterpret_cast<float*>(stages + kStages * C::kStageBytes);  // [4 warps][8 q][DH + 2]
+  uint64_t* full = reinterpret_cast<uint64_t*>(mrg + kConsumerWarps * 8 * (DH + 2));
+  uint64_t* empty = full + kStages;
+
+  const int G = a.Hq / a.Hkv;
+  const int w = warp_id(), lane = lane_id();
+  const int n_items = *a.n_items;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (w == kConsumerWarps) {
+    // ---------------- producer warp
+    if (lane == 0) {
+      tma_prefetch(&tmK);
+      tma_prefetch(&tmV);
+      const uint64_t pol = policy_evict_first();
+      int q = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const ItemInfo ii = item_info(a, it);
+        for (int p = ii.p0; p < ii.p1; ++p, ++q) {
+          const int s = q % kStages;
+          const uint32_t ph = (q / kStages) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          const int page = a.page_table[(size_t)ii.slot * a.max_pages + p];
+          const int row = (page * a.Hkv + ii.kvh) * 64;
+          uint8_t* kb = stages + s * C::kStageBytes;
+          uint8_t* vb = kb + C::kBlockBytes;
+          mbar_arrive_expect_tx(&full[s], C::kStageBytes);
+#pragma unroll
+          for (int b = 0; b < C::kBoxes; ++b) {
+            tma_load_2d_hint(kb + b * C::kBoxBytes, &tmK, &full[s], b * C::kBoxCols, row, pol);
+            tma_load_2d_hint(vb + b * C::kBoxBytes, &tmV, &full[s], b * C::kBoxCols, row, pol);
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumer warps
+  const float scale2 = a.scale * kLog2e;
+  int q = 0;
+  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    const ItemInfo ii = item_info(a, it);
+    // Q^T fragments (B operand): n = query index lane/4 (< G), k = dims
+    uint32_t bq[MT][2];
+    {
+      const int n = lane >> 2;
+      const __nv_bfloat16* qrow =
+          reinterpret_cast<const __nv_bfloat16*>(a.q) + ((size_t)ii.m * a.Hq + ii.kvh * G + n) * DH;
+#pragma unroll
+      for (int kk = 0; kk < MT; ++kk) {
+        const int d0 = kk * 16 + 2 * (lane & 3);
+        bq[kk][0] = n < G ? *reinterpret_cast<const uint32_t*>(qrow + d0) : 0u;
+        bq[kk][1] = n < G ? *reinterpret_cast<const uint32_t*>(qrow + d0 + 8) : 0u;
+      }
+    }
+    float o[MT][4];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+    for (int p = ii.p0; p < ii.p1; ++p, ++q) {
+      const int s = q % kStages;
+      const uint32_t ph = (q / kStages) & 1;
+      mbar_wait(&full[s], ph);
+      const uint32_t kb = smem_u32(stages + s * C::kStageBytes);
+      const uint32_t vb = kb + C::kBlockBytes;
+      const int tok0 = w * 16;
+      const int tbase = p * 64 + tok0;  // absolute position of the warp's first token
+      if (tbase < ii.ctx) {
+        float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int kk = 0; kk < MT; ++kk) {
+          uint32_t a0, a1, a2, a3;
+          ldmatrix_x4(kv_addr<DH>(kb, tok0 + (lane & 15), 2 * kk + (lane >> 4)), a0, a1, a2, a3);
+          mma_bf16_16816(sacc, a0, a1, a2, a3, bq[kk][0], bq[kk][1]);
+        }
+        // sacc: [0]=(tok r, q c0) [1]=(tok r, q c1) [2]=(tok r+8, q c0) [3]=(tok r+8, q c1)
+        const int r = lane >> 2;
+        const bool v0 = tbase + r < ii.ctx, v1 = tbase + r + 8 < ii.ctx;
+        float x0 = v0 ? sacc[0] * scale2 : -INFINITY;
+        float x1 = v0 ? sacc[1] * scale2 : -INFINITY;
+        float x2 = v1 ? sacc[2] * scale2 : -INFINITY;
+        float x3 = v1 ? sacc[3] * scale2 : -INFINITY;
+        float bm0 = fmaxf(x0, x2), bm1 = fmaxf(x1, x3);
+#pragma unroll
+        for (int off = 4; off < 32; off <<= 1) {
+          bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, off));
+          bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, off));
+        }
+        const float nm0 = fmaxf(m0, bm0), nm1 = fmaxf(m1, bm1);
+        const float al0 = m0 == -INFINITY ? 0.f : exp2f(m0 - nm0);
+        const float al1 = m1 == -INFINITY ? 0.f : exp2f(m1 - nm1);
+        const float p0 = exp2f(x0 - nm0), p1 = exp2f(x1 - nm1), p2 = exp2f(x2 - nm0), p3 = exp2f(x3 - nm1);
+        float s0 = p0 + p2, s1 = p1 + p3;
+#pragma unroll
+        for (int off = 4; off < 32; off <<= 1) {
+          s0 += __shfl_xor_sync(0xffffffffu, s0, off);
+          s1 += __shfl_xor_sync(0xffffffffu, s1, off);
+        }
+        l0 = l0 * al0 + s0;
+        l1 = l1 * al1 + s1;
+        m0 = nm0;
+        m1 = nm1;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          o[mt][0] *= al0;
+          o[mt][2] *= al0;
+          o[mt][1] *= al1;
+          o[mt][3] *= al1;
+        }
+        const uint32_t pb0 = movmatrix_trans(pack_bf16(p0, p1));
+        const uint32_t pb1 = movmatrix_trans(pack_bf16(p2, p3));
+        const int vtok = tok0 + (lane & 7) + ((lane >> 4) << 3);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          uint32_t a0, a1, a2, a3;
+          ldmatrix_x4_trans(kv_addr<DH>(vb, vtok, 2 * mt + ((lane >> 3) & 1)), a0, a1, a2, a3);
+          mma_bf16_16816(o[mt], a0, a1, a2, a3, pb0, pb1);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    // ---- merge the 4 warps' partial states (columns c0 = 2*(lane&3), c1 = c0+1)
+    float* my = mrg + w * 8 * (DH + 2);
+    const int c0 = 2 * (lane & 3);
+    if ((lane >> 2) == 0) {
+      my[c0 * (DH + 2) + DH] = m0;
+      my[c0 * (DH + 2) + DH + 1] = l0;
+      my[(c0 + 1) * (DH + 2) + DH] = m1;
+      my[(c0 + 1) * (DH + 2) + DH + 1] = l1;
+    }
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      const int d = mt * 16 + (lane >> 2);
+      my[c0 * (DH + 2) + d] = o[mt][0];
+      my[(c0 + 1) * (DH + 2) + d] = o[mt][1];
+      my[c0 * (DH + 2) + d + 8] = o[mt][2];
+      my[(c0 + 1) * (DH + 2) + d + 8] = o[mt][3];
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32));
+    for (int i = threadIdx.x; i < G * DH; i += kConsumerWarps * 32) {
+      const int g = i / DH, d = i % DH;
+      float mx = -INFINITY;
+      for (int ww = 0; ww < kConsumerWarps; ++ww) mx = fmaxf(mx, mrg[(ww * 8 + g) * (DH + 2) + DH]);
+      float acc = 0.f, l = 0.f;
+      for (int ww = 0; ww < kConsumerWarps; ++ww) {
+        const float* e = mrg + (ww * 8 + g) * (DH + 2);
+        const float f = e[DH] == -INFINITY ? 0.f : exp2f(e[DH] - mx);
+        acc += e[d] * f;
+        l += e[DH + 1] * f;
+      }
+      a.part_o[((size_t)it * G + g) * DH + d] = acc;
+      if (d == 0) {
+        a.part_ml[((size_t)it * G + g) * 2 + 0] = mx;
+        a.part_ml[((size_t)it * G + g) * 2 + 1] = l;
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32));
+  }
+}
+
+template <int DH>
+static void launch_bf16(const AttnArgs& a, const void* tk, const void* tv, cudaStream_t st) {
+  using C = AttnCfg<DH>;
+  const size_t smem = 1024 + kStages * C::kStageBytes + kConsumerWarps * 8 * (DH + 2) * 4 + 2 * kStages * 8 + 64;
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(attn_bf16_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    set = true;
+  }
+  int grid = 148;
+  const int occ = (int)((228 * 1024) / (smem + 1024));
+  grid *= occ < 1 ? 1 : occ;
+  attn_bf16_kernel<DH><<<grid, kAttnThreads, smem, st>>>(a, *reinterpret_cast<const CUtensorMap*>(tk),
+                                                          *reinterpret_cast<const CUtensorMap*>(tv));
+}
+
+void attn_plan(const AttnArgs& a, int split, cudaStream_t st) {
+  attn_plan_kernel<<<1, 1024, 0, st>>>(a, split);
+}
+
+void attn_run(const AttnArgs& a, bool kv_fp32, const void* tmap_k, const void* tmap_v, cudaStream_t st) {
+  if (a.M <= 0) return;
+  if (kv_fp32) {
+    const int G = a.Hq / a.Hkv;
+    const size_t smem = (size_t)G * a.dh * 4 + (size_t)G * 64 * kChunkPages * 4;
+    attn_f32_kernel<<<148 * 4, kF32Threads, smem, st>>>(a);
+  } else {
+    switch (a.dh) {
+      case 128: launch_bf16<128>(a, tmap_k, tmap_v, st); break;
+      case 64: launch_bf16<64>(a, tmap_k, tmap_v, st); break;
+      case 32: launch_bf16<32>(a, tmap_k, tmap_v, st); break;
+      default: return;
+    }
+  }
+  const int warps = a.M * a.Hq;
+  attn_combine_kernel<false><<<(warps + 7) / 8, 256, 0, st>>>(a, nullptr);
+}
+
+void attn_combine_f32(const AttnArgs& a, float* out_f32, cudaStream_t st) {
+  const int warps = a.M * a.Hq;
+  attn_combine_kernel<true><<<(warps + 7) / 8, 256, 0, st>>>(a, out_f32);
+}
+
+}  // namespace srl

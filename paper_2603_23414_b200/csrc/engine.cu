@@ -1,0 +1,732 @@
+// engine.cu — host orchestration of one rollout decode step and the C ABI
+// of include/srl.h.  All arithmetic of the step runs in the device kernels
+// (gemm_tc.cu, layers.cu, attention.cu, sampler.cu, ctl.cu); this file plans
+// memory, chains the launches on the caller's stream and mirrors a handful
+// of host-side counters.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "engine.hpp"
+#include "kernels.hpp"
+#include "layers.hpp"
+#include "tma.hpp"
+
+namespace srl {
+extern thread_local std::string g_last_error;
+void set_error(const char* fmt, const char* a, long b);
+}  // namespace srl
+
+using namespace srl;
+
+namespace {
+
+constexpr size_t kAlign = 1024;
+inline size_t al(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+struct LayerW {
+  __nv_bfloat16 *attn_norm, *wqkv, *bqkv, *wo, *mlp_norm, *wgu, *wd;
+};
+
+// ------------------------------------------------------------------ weight layout
+struct WeightLayout {
+  struct Ent {
+    std::string name;
+    size_t off, numel;
+  };
+  std::vector<Ent> ents;
+  size_t total = 0;
+  void add(const std::string& n, size_t numel) {
+    ents.push_back({n, total, numel});
+    total += al(numel * 2);
+  }
+  // q/k/v (and their biases, and gate/up) must be contiguous: add them unaligned in one run
+  void add_run(const std::vector<std::pair<std::string, size_t>>& run) {
+    size_t off = total;
+    for (auto& e : run) {
+      ents.push_back({e.first, off, e.second});
+      off += e.second * 2;
+    }
+    total = al(off);
+  }
+  const Ent* find(const std::string& n) const {
+    for (auto& e : ents)
+      if (e.name == n) return &e;
+    return nullptr;
+  }
+};
+
+WeightLayout make_layout(const srl_model_cfg& m) {
+  WeightLayout w;
+  const size_t d = m.d, qd = (size_t)m.Hq * m.dh, kd = (size_t)m.Hkv * m.dh, ff = m.ff;
+  w.add("embed", (size_t)m.V * d);
+  for (int l = 0; l < m.L; ++l) {
+    const std::string p = "L" + std::to_string(l) + ".";
+    w.add(p + "attn_norm", d);
+    w.add_run({{p + "wq", qd * d}, {p + "wk", kd * d}, {p + "wv", kd * d}});
+    if (m.qkv_bias) w.add_run({{p + "bq", qd}, {p + "bk", kd}, {p + "bv", kd}});
+    w.add(p + "wo", d * qd);
+    w.add(p + "mlp_norm", d);
+    w.add_run({{p + "wg", ff * d}, {p + "wu", ff * d}});
+    w.add(p + "wd", d * ff);
+  }
+  w.add("final_norm", d);
+  w.add("lm_head", (size_t)m.V * d);
+  return w;
+}
+
+// ------------------------------------------------------------------ scratch layout
+struct ScratchPlan {
+  size_t total = 0;
+  size_t take(size_t bytes) {
+    size_t o = total;
+    total += al(bytes);
+    return o;
+  }
+};
+
+struct Sizes {
+  int Q_g, R, Q_tot, max_pages, max_ctx, max_prompts, mmax, prefill_rows_max, max_items, G;
+  long long ev_cap, h_cap_tok, part_floats;
+  size_t qkv_n;
+};
+
+int validate(const srl_model_cfg* m, const srl_sched_cfg* s, int world, std::string& why) {
+  if (!m || !s) return why = "null config", -1;
+  if (m->L <= 0 || m->d <= 0 || m->Hq <= 0 || m->Hkv <= 0 || m->dh <= 0 || m->ff <= 0 || m->V <= 0)
+    return why = "model dims must be positive", -1;
+  if (m->Hq % m->Hkv) return why = "Hq must be a multiple of Hkv", -1;
+  if (m->Hq / m->Hkv > 8) return why = "GQA group > 8 not supported", -1;
+  if (m->dh != 32 && m->dh != 64 && m->dh != 128) return why = "dh must be 32, 64 or 128", -1;
+  if (m->d % 64 || (m->Hq * m->dh) % 64 || m->ff % 64) return why = "d, Hq*dh, ff must be multiples of 64", -1;
+  if (s->Q_g <= 0 || s->U <= 0 || s->G <= 0 || s->cap <= 0 || s->pool_prompts <= 0 || s->kv_pages <= 0)
+    return why = "Q_g, U, G, cap, pool_prompts, kv_pages must be positive", -1;
+  if (s->page_tokens != kPage) return why = "page_tokens must be 64", -1;
+  if (world < 1 || world > kMaxR) return why = "world out of range", -1;
+  if ((long long)s->Q_g * world > 1024) return why = "Q_tot must be <= 1024", -1;
+  if (s->mode == SRL_MODE_SORTED && s->U > s->pool_prompts * s->G) return why = "U larger than the prompt pool (S:252)", -1;
+  if (s->U > kMaxGroup) return why = "U too large", -1;
+  if (s->stop == SRL_STOP_EOS && s->eos_id < 0) return why = "EOS stop needs eos_id", -1;
+  if (s->temperature <= 0.f) return why = "temperature must be > 0", -1;
+  if (s->max_traj <= 0 || s->max_prompt <= 0 || s->prefill_chunk <= 0) return why = "max_traj, max_prompt, prefill_chunk must be positive", -1;
+  if (s->kv_dtype != SRL_KV_BF16 && s->kv_dtype != SRL_KV_FP32) return why = "kv_dtype", -1;
+  return 0;
+}
+
+Sizes compute_sizes(const srl_model_cfg* m, const srl_sched_cfg* s, int world) {
+  Sizes z;
+  z.Q_g = s->Q_g;
+  z.R = world;
+  z.Q_tot = s->Q_g * world;
+  z.max_ctx = s->max_prompt + s->cap;
+  z.max_pages = (z.max_ctx + kPage - 1) / kPage;
+  z.max_prompts = (s->max_traj + s->G - 1) / s->G + 1;
+  z.prefill_rows_max = s->Q_g * (z.max_ctx);
+  z.mmax = s->Q_g > s->prefill_chunk ? s->Q_g : s->prefill_chunk;
+  z.G = m->Hq / m->Hkv;
+  const int a1 = attn_max_items(s->Q_g, m->Hkv, z.max_ctx);
+  const int a2 = s->prefill_chunk * m->Hkv;
+  z.max_items = a1 > a2 ? a1 : a2;
+  z.ev_cap = 1LL << 20;
+  const int gmax = s->max_traj < kMaxGroup ? s->max_traj : kMaxGroup;
+  z.h_cap_tok = (long long)gmax * s->cap;
+  z.qkv_n = (size_t)(m->Hq + 2 * m->Hkv) * m->dh;
+  // partial buffer: max over the four layer GEMMs and the LM head at the two M sizes
+  long long best = 0;
+  const int Ns[5] = {(int)z.qkv_n, m->d, 2 * m->ff, m->d, m->V};
+  const int Ks[5] = {m->d, m->Hq * m->dh, m->d, m->ff, m->d};
+  const int Ms[2] = {s->Q_g, s->prefill_chunk};
+  for (int mi = 0; mi < 2; ++mi)
+    for (int g = 0; g < 5; ++g) {
+      const int sp = gemm_choose_splits(Ms[mi], Ns[g], Ks[g], 148);
+      const long long f = (long long)sp * Ms[mi] * Ns[g];
+      if (g == 4 && (sp == 1 || mi == 1)) continue;  // LM head writes logits directly; no prefill LM head
+      if (f > best) best = f;
+    }
+  z.part_floats = best;
+  return z;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ the engine
+struct srl_engine {
+  srl_model_cfg m;
+  srl_sched_cfg s;
+  Sizes z;
+  int rank = 0, world = 1, device = 0, num_sms = 148;
+  cudaStream_t st = nullptr;
+  bool kv_f32 = false;
+  // arena
+  uint8_t *W = nullptr, *KV = nullptr, *S = nullptr;
+  WeightLayout wl;
+  std::vector<LayerW> lw;
+  __nv_bfloat16 *embed = nullptr, *final_norm = nullptr, *lm_head = nullptr;
+  std::vector<void*> kpool, vpool;
+  std::vector<CUtensorMap> tmK, tmV;
+  // scratch
+  float* x_res = nullptr;
+  __nv_bfloat16 *xn = nullptr, *attn_out = nullptr, *act = nullptr;
+  void* qbuf = nullptr;
+  float* part = nullptr;
+  float* logits = nullptr;
+  float *rope_cos = nullptr, *rope_sin = nullptr;
+  int* row_slot_id = nullptr;  // identity rows 0..Q_g-1
+  AttnArgs attn{};
+  Ctl ctl{};
+  CtlStatus* hst = nullptr;  // pinned
+  // host mirrors
+  std::unordered_set<uint64_t> ids;
+  std::vector<uint64_t> prompt_ids;
+  long long n_traj = 0, n_prompts = 0, prompt_tok_used = 0, prompt_tok_cap = 0;
+  int group_state = 0;  // 0 none, 1 ready, 2 harvested
+  bool v_valid = false;
+  long long v = -1;
+  long long launches = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace {
+
+int cuda_fail(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  char buf[256];
+  snprintf(buf, sizeof(buf), "%s: %s", what, cudaGetErrorString(e));
+  g_last_error = buf;
+  return SRL_E_CUDA;
+}
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+void plan_scratch(srl_engine* e, ScratchPlan& p, bool assign) {
+  const Sizes& z = e->z;
+  const srl_model_cfg& m = e->m;
+  const srl_sched_cfg& s = e->s;
+  uint8_t* B = e->S;
+  auto P = [&](size_t bytes) -> void* { size_t o = p.take(bytes); return assign ? (void*)(B + o) : nullptr; };
+  Ctl& c = e->ctl;
+  c.s = (CtlState*)P(sizeof(CtlState));
+  c.traj = (DevTraj*)P(sizeof(DevTraj) * s.max_traj);
+  c.slot_traj = (int*)P(4 * z.Q_tot);
+  c.page_table = (int*)P(4ull * z.Q_g * z.max_pages);
+  c.page_stack = (int*)P(4ull * s.kv_pages);
+  c.resumed = (int*)P(4ull * s.max_traj);
+  c.ready = (int*)P(4ull * s.max_traj);
+  c.group = (int*)P(4ull * s.max_traj);
+  c.tokens = (int*)P(4ull * s.max_traj * s.cap);
+  c.lps = (float*)P(4ull * s.max_traj * s.cap);
+  c.vers = (int*)P(4ull * s.max_traj * s.cap);
+  c.prompt_off = (int*)P(4ull * (z.max_prompts + 1));
+  c.prompt_tok = (int*)P(4ull * z.max_prompts * s.max_prompt);
+  c.events = (int*)P(24ull * z.ev_cap);
+  c.row_tok = (int*)P(4 * z.Q_g);
+  c.row_pos = (int*)P(4 * z.Q_g);
+  c.row_n = (int*)P(4 * z.Q_g);
+  c.row_traj = (int*)P(4 * z.Q_g);
+  c.row_restarts = (int*)P(4 * z.Q_g);
+  c.pre_tok = (int*)P(4ull * z.prefill_rows_max);
+  c.pre_pos = (int*)P(4ull * z.prefill_rows_max);
+  c.pre_slot = (int*)P(4ull * z.prefill_rows_max);
+  c.admit_local = (int*)P(4 * z.Q_g);
+  c.samp_tok = (int*)P(4 * z.Q_tot);
+  c.samp_lp = (float*)P(4 * z.Q_tot);
+  c.h_tok = (int*)P(4ull * z.h_cap_tok);
+  c.h_lp = (float*)P(4ull * z.h_cap_tok);
+  c.h_ver = (int*)P(4ull * z.h_cap_tok);
+  c.h_rec = (srl_traj*)P(sizeof(srl_traj) * kMaxGroup);
+  e->row_slot_id = (int*)P(4 * z.Q_g);
+  e->x_res = (float*)P(4ull * z.mmax * m.d);
+  e->xn = (__nv_bfloat16*)P(2ull * z.mmax * m.d);
+  e->attn_out = (__nv_bfloat16*)P(2ull * z.mmax * m.Hq * m.dh);
+  e->act = (__nv_bfloat16*)P(2ull * z.mmax * m.ff);
+  e->qbuf = P((e->kv_f32 ? 4ull : 2ull) * z.mmax * m.Hq * m.dh);
+  e->part = (float*)P(4ull * z.part_floats);
+  e->logits = (float*)P(4ull * z.Q_g * m.V);
+  e->rope_cos = (float*)P(4ull * z.max_ctx * (m.dh / 2));
+  e->rope_sin = (float*)P(4ull * z.max_ctx * (m.dh / 2));
+  AttnArgs& a = e->attn;
+  a.items = (int*)P(12ull * z.max_items);
+  a.n_items = (int*)P(64);
+  a.row_item0 = (int*)P(4ull * z.mmax);
+  a.row_nchunk = (int*)P(4ull * z.mmax);
+  a.part_o = (float*)P(4ull * z.max_items * z.G * m.dh);
+  a.part_ml = (float*)P(8ull * z.max_items * z.G);
+}
+
+size_t kv_bytes_for(const srl_model_cfg& m, const srl_sched_cfg& s) {
+  const size_t el = s.kv_dtype == SRL_KV_FP32 ? 4 : 2;
+  return al((size_t)s.kv_pages * m.Hkv * kPage * m.dh * el) * 2 * m.L;
+}
+
+// ---- GEMM helper: Y partials -> returns split count used
+int run_gemm(srl_engine* e, const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N, int K, float* out,
+             long long cap_floats) {
+  int sp = gemm_choose_splits(M, N, K, e->num_sms);
+  while (sp > 1 && (long long)sp * M * N > cap_floats) --sp;
+  gemm_bf16_partials(X, M, W, N, K, out, sp, e->st);
+  e->launches++;
+  return sp;
+}
+
+// One forward pass over M rows (decode: rows = local slots; prefill: rows = prompt tokens).
+void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const int* row_slot, bool decode) {
+  const srl_model_cfg& m = e->m;
+  cudaStream_t st = e->st;
+  const int d = m.d, qd = m.Hq * m.dh;
+  const int Nqkv = (int)e->z.qkv_n;
+  AttnArgs a = e->attn;
+  a.q = e->qbuf;
+  a.row_pos = row_pos;
+  a.row_slot = row_slot;
+  a.page_table = e->ctl.page_table;
+  a.max_pages = e->z.max_pages;
+  a.M = M;
+  a.Hq = m.Hq;
+  a.Hkv = m.Hkv;
+  a.dh = m.dh;
+  a.out = e->attn_out;
+  a.max_items = e->z.max_items;
+  a.scale = 1.0f / sqrtf((float)m.dh);
+  attn_plan(a, decode ? 1 : 0, st);
+  embed_norm(row_tok, row_pos, M, d, e->embed, e->lw[0].attn_norm, m.rms_eps, e->x_res, e->xn, st);
+  e->launches += 2;
+  const long long capf = e->z.part_floats;
+  for (int l = 0; l < m.L; ++l) {
+    const LayerW& w = e->lw[l];
+    int sp = run_gemm(e, e->xn, M, w.wqkv, Nqkv, d, e->part, capf);
+    QkvEpiArgs q{};
+    q.P = e->part;
+    q.S = sp;
+    q.M = M;
+    q.bias = m.qkv_bias ? w.bqkv : nullptr;
+    q.row_pos = row_pos;
+    q.row_slot = row_slot;
+    q.page_table = e->ctl.page_table;
+    q.max_pages = e->z.max_pages;
+    q.rope_cos = e->rope_cos;
+    q.rope_sin = e->rope_sin;
+    q.q_out = e->qbuf;
+    q.k_pool = e->kpool[l];
+    q.v_pool = e->vpool[l];
+    q.Hq = m.Hq;
+    q.Hkv = m.Hkv;
+    q.dh = m.dh;
+    qkv_epilogue(q, e->kv_f32, st);
+    a.k_pool = e->kpool[l];
+    a.v_pool = e->vpool[l];
+    attn_run(a, e->kv_f32, &e->tmK[l], &e->tmV[l], st);
+    sp = run_gemm(e, e->attn_out, M, w.wo, d, qd, e->part, capf);
+    resid_norm(e->part, sp, M, d, row_pos, e->x_res, w.mlp_norm, m.rms_eps, e->xn, st);
+    sp = run_gemm(e, e->xn, M, w.wgu, 2 * m.ff, d, e->part, capf);
+    silu_mul(e->part, sp, M, m.ff, e->act, st);
+    sp = run_gemm(e, e->act, M, w.wd, d, m.ff, e->part, capf);
+    const __nv_bfloat16* next = l + 1 < m.L ? e->lw[l + 1].attn_norm : e->final_norm;
+    resid_norm(e->part, sp, M, d, row_pos, e->x_res, next, m.rms_eps, e->xn, st);
+    e->launches += 6;
+  }
+  if (decode) {
+    int sp = gemm_choose_splits(M, m.V, d, e->num_sms);
+    while (sp > 1 && (long long)sp * M * m.V > capf) --sp;
+    if (sp == 1) {
+      gemm_bf16_partials(e->xn, M, e->lm_head, m.V, d, e->logits, 1, st);
+      e->launches++;
+    } else {
+      gemm_bf16_partials(e->xn, M, e->lm_head, m.V, d, e->part, sp, st);
+      reduce_splits(e->part, sp, (long long)M * m.V, e->logits, st);
+      e->launches += 2;
+    }
+  }
+}
+
+void read_status(srl_engine* e) {
+  cudaMemcpyAsync(e->hst, &e->ctl.s->st, sizeof(CtlStatus), cudaMemcpyDeviceToHost, e->st);
+  cudaStreamSynchronize(e->st);
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+extern "C" {
+
+int32_t srl_arena_sizes(const srl_model_cfg* m, const srl_sched_cfg* s, int32_t world, uint64_t* wb, uint64_t* kb,
+                        uint64_t* sb) {
+  std::string why;
+  if (validate(m, s, world, why)) return fail(SRL_E_INVALID_ARG, "srl_arena_sizes: " + why);
+  srl_engine tmp;
+  tmp.m = *m;
+  tmp.s = *s;
+  tmp.z = compute_sizes(m, s, world);
+  tmp.kv_f32 = s->kv_dtype == SRL_KV_FP32;
+  ScratchPlan p;
+  plan_scratch(&tmp, p, false);
+  if (wb) *wb = make_layout(*m).total;
+  if (kb) *kb = kv_bytes_for(*m, *s);
+  if (sb) *sb = p.total;
+  return SRL_OK;
+}
+
+int64_t srl_weight_offset(const srl_model_cfg* m, const char* name, int64_t* numel) {
+  if (!m || !name) return -1;
+  WeightLayout w = make_layout(*m);
+  const WeightLayout::Ent* e = w.find(name);
+  if (!e) return -1;
+  if (numel) *numel = (int64_t)e->numel;
+  return (int64_t)e->off;
+}
+
+int32_t srl_create(const srl_model_cfg* m, const srl_sched_cfg* s, int32_t device, void* stream, const srl_arena* mem,
+                   const srl_comm* comm, srl_engine** out) {
+  if (!out || !mem) return fail(SRL_E_INVALID_ARG, "srl_create: null argument");
+  const int world = comm ? comm->world : 1;
+  std::string why;
+  if (validate(m, s, world, why)) return fail(SRL_E_INVALID_ARG, "srl_create: " + why);
+  if (world > 1) return fail(SRL_E_INVALID_ARG, "srl_create: world > 1 requires the NCCL build (not in this library)");
+  uint64_t wb, kb, sb;
+  srl_arena_sizes(m, s, world, &wb, &kb, &sb);
+  if (mem->weights_bytes < wb || mem->kv_bytes < kb || mem->scratch_bytes < sb || !mem->weights || !mem->kv || !mem->scratch)
+    return fail(SRL_E_CAPACITY, "srl_create: arena smaller than srl_arena_sizes");
+  if (cudaSetDevice(device) != cudaSuccess) return cuda_fail("cudaSetDevice");
+  srl_engine* e = new srl_engine();
+  e->m = *m;
+  e->s = *s;
+  e->world = world;
+  e->rank = comm ? comm->rank : 0;
+  e->device = device;
+  e->st = (cudaStream_t)stream;
+  e->kv_f32 = s->kv_dtype == SRL_KV_FP32;
+  e->z = compute_sizes(m, s, world);
+  cudaDeviceGetAttribute(&e->num_sms, cudaDevAttrMultiProcessorCount, device);
+  e->W = (uint8_t*)mem->weights;
+  e->KV = (uint8_t*)mem->kv;
+  e->S = (uint8_t*)mem->scratch;
+  // weights
+  e->wl = make_layout(*m);
+  auto wp = [&](const std::string& n) -> __nv_bfloat16* {
+    const WeightLayout::Ent* en = e->wl.find(n);
+    return en ? (__nv_bfloat16*)(e->W + en->off) : nullptr;
+  };
+  e->embed = wp("embed");
+  e->final_norm = wp("final_norm");
+  e->lm_head = wp("lm_head");
+  for (int l = 0; l < m->L; ++l) {
+    const std::string p = "L" + std::to_string(l) + ".";
+    LayerW w;
+    w.attn_norm = wp(p + "attn_norm");
+    w.wqkv = wp(p + "wq");
+    w.bqkv = m->qkv_bias ? wp(p + "bq") : nullptr;
+    w.wo = wp(p + "wo");
+    w.mlp_norm = wp(p + "mlp_norm");
+    w.wgu = wp(p + "wg");
+    w.wd = wp(p + "wd");
+    e->lw.push_back(w);
+  }
+  // KV pools + TMA maps
+  const size_t el = e->kv_f32 ? 4 : 2;
+  const size_t pool = al((size_t)s->kv_pages * m->Hkv * kPage * m->dh * el);
+  e->tmK.resize(m->L);
+  e->tmV.resize(m->L);
+  for (int l = 0; l < m->L; ++l) {
+    e->kpool.push_back(e->KV + (2 * (size_t)l) * pool);
+    e->vpool.push_back(e->KV + (2 * (size_t)l + 1) * pool);
+    if (!e->kv_f32) {
+      const uint32_t bc = m->dh < 64 ? m->dh : 64;
+      const uint64_t rows = (uint64_t)s->kv_pages * m->Hkv * kPage;
+      if (tma_encode_2d(&e->tmK[l], e->kpool[l], rows, m->dh, (uint64_t)m->dh * 2, 64, bc, 2, bc == 64) ||
+          tma_encode_2d(&e->tmV[l], e->vpool[l], rows, m->dh, (uint64_t)m->dh * 2, 64, bc, 2, bc == 64)) {
+        delete e;
+        return fail(SRL_E_CUDA, "srl_create: TMA descriptor encode failed");
+      }
+    }
+  }
+  ScratchPlan p;
+  plan_scratch(e, p, true);
+  Ctl& c = e->ctl;
+  c.Q_g = s->Q_g;
+  c.R = world;
+  c.rank = e->rank;
+  c.Q_tot = e->z.Q_tot;
+  c.U = s->U;
+  c.pool_traj = s->pool_prompts * s->G;
+  c.G = s->G;
+  c.cap = s->cap;
+  c.kv_pages = s->kv_pages;
+  c.max_pages = e->z.max_pages;
+  c.mode = s->mode;
+  c.resume = s->resume;
+  c.barrier = s->barrier;
+  c.stop = s->stop;
+  c.eos_id = s->eos_id;
+  c.max_traj = s->max_traj;
+  c.max_prompt = s->max_prompt;
+  c.prefill_rows_max = e->z.prefill_rows_max;
+  c.ev_cap = e->z.ev_cap;
+  c.h_cap_tok = e->z.h_cap_tok;
+  e->prompt_tok_cap = (long long)e->z.max_prompts * s->max_prompt;
+  // init device state
+  cudaMemsetAsync(e->KV, 0, mem->kv_bytes, e->st);  // finite values in never-written KV rows
+  std::vector<int> ident(s->Q_g);
+  for (int i = 0; i < s->Q_g; ++i) ident[i] = i;
+  cudaMemcpyAsync(e->row_slot_id, ident.data(), 4 * s->Q_g, cudaMemcpyHostToDevice, e->st);
+  int zero = 0;
+  cudaMemcpyAsync(c.prompt_off, &zero, 4, cudaMemcpyHostToDevice, e->st);
+  ctl_init(c, s->K, e->st);
+  rope_table(e->rope_cos, e->rope_sin, e->z.max_ctx, m->dh, (double)m->rope_theta, e->st);
+  if (cudaHostAlloc((void**)&e->hst, sizeof(CtlStatus), cudaHostAllocDefault) != cudaSuccess) {
+    delete e;
+    return cuda_fail("cudaHostAlloc");
+  }
+  cudaEventCreate(&e->ev0);
+  cudaEventCreate(&e->ev1);
+  if (cudaStreamSynchronize(e->st) != cudaSuccess) {
+    delete e;
+    return cuda_fail("srl_create init");
+  }
+  *out = e;
+  return SRL_OK;
+}
+
+int32_t srl_destroy(srl_engine* e) {
+  if (!e) return SRL_OK;
+  if (e->hst) cudaFreeHost(e->hst);
+  if (e->ev0) cudaEventDestroy(e->ev0);
+  if (e->ev1) cudaEventDestroy(e->ev1);
+  delete e;
+  return SRL_OK;
+}
+
+int32_t srl_submit_prompts(srl_engine* e, int32_t n, const uint64_t* prompt_ids, const int32_t* tok_off,
+                           const int32_t* toks, const int32_t* forced_len) {
+  if (!e || n < 0 || (n > 0 && (!prompt_ids || !tok_off || !toks))) return fail(SRL_E_INVALID_ARG, "srl_submit_prompts: bad arguments");
+  if (n == 0) return SRL_OK;
+  const srl_sched_cfg& s = e->s;
+  std::unordered_set<uint64_t> seen;
+  for (int i = 0; i < n; ++i) {
+    if (e->ids.count(prompt_ids[i]) || !seen.insert(prompt_ids[i]).second)
+      return fail(SRL_E_DUPLICATE_ID, "srl_submit_prompts: duplicate prompt id (S:114)");
+    const int len = tok_off[i + 1] - tok_off[i];
+    if (len < 1 || len > s.max_prompt) return fail(SRL_E_INVALID_ARG, "srl_submit_prompts: prompt length outside [1, max_prompt]");
+  }
+  if (s.stop == SRL_STOP_FORCED && !forced_len) return fail(SRL_E_INVALID_ARG, "srl_submit_prompts: FORCED stop needs forced_len");
+  if (forced_len)
+    for (long long i = 0; i < (long long)n * s.G; ++i)
+      if (forced_len[i] < 1 || forced_len[i] > s.cap) return fail(SRL_E_INVALID_ARG, "srl_submit_prompts: forced_len outside [1, cap]");
+  const long long ntok = tok_off[n] - tok_off[0];
+  if (e->n_traj + (long long)n * s.G > s.max_traj || e->prompt_tok_used + ntok > e->prompt_tok_cap ||
+      e->n_prompts + n > e->z.max_prompts - 1)
+    return fail(SRL_E_CAPACITY, "srl_submit_prompts: max_traj / prompt storage exceeded");
+  std::vector<int> offs(n);
+  for (int i = 0; i < n; ++i) offs[i] = (int)(e->prompt_tok_used + (tok_off[i + 1] - tok_off[0]));
+  std::vector<DevTraj> tr((size_t)n * s.G);
+  for (int i = 0; i < n; ++i)
+    for (int g = 0; g < s.G; ++g) {
+      DevTraj& t = tr[(size_t)i * s.G + g];
+      memset(&t, 0, sizeof(t));
+      t.prompt_idx = (int)(e->n_prompts + i);
+      t.prompt_len = tok_off[i + 1] - tok_off[i];
+      t.forced_len = forced_len ? forced_len[(size_t)i * s.G + g] : s.cap;
+      t.epoch = -1;
+      t.v_first = -1;
+      t.admit_step = -1;
+      t.finish_step = -1;
+      t.state = TS_STREAM;
+      t.slot = -1;
+      t.fresh = 1;
+      t.sample = g;
+    }
+  Ctl& c = e->ctl;
+  cudaMemcpyAsync(c.prompt_tok + e->prompt_tok_used, toks + tok_off[0], 4 * ntok, cudaMemcpyHostToDevice, e->st);
+  cudaMemcpyAsync(c.prompt_off + e->n_prompts + 1, offs.data(), 4 * n, cudaMemcpyHostToDevice, e->st);
+  cudaMemcpyAsync(c.traj + e->n_traj, tr.data(), sizeof(DevTraj) * tr.size(), cudaMemcpyHostToDevice, e->st);
+  ctl_submit(c, n * s.G, n, e->st);
+  e->launches++;
+  if (cudaStreamSynchronize(e->st) != cudaSuccess) return cuda_fail("srl_submit_prompts");
+  for (int i = 0; i < n; ++i) {
+    e->ids.insert(prompt_ids[i]);
+    e->prompt_ids.push_back(prompt_ids[i]);
+  }
+  e->n_traj += (long long)n * s.G;
+  e->n_prompts += n;
+  e->prompt_tok_used += ntok;
+  return SRL_OK;
+}
+
+int32_t srl_decode_step(srl_engine* e, srl_step_info* info) {
+  if (!e) return fail(SRL_E_INVALID_ARG, "srl_decode_step: null engine");
+  if (info) {
+    memset(info, 0, sizeof(*info));
+    info->k = -1;
+  }
+  if (e->group_state != 0) return fail(SRL_E_STATE, "srl_decode_step: a group awaits harvest/load_policy_weights (P:30)");
+  if (!e->v_valid) return fail(SRL_E_STATE, "srl_decode_step: no policy weights loaded");
+  cudaStream_t st = e->st;
+  cudaEventRecord(e->ev0, st);
+  ctl_begin(e->ctl, st);
+  e->launches++;
+  read_status(e);
+  if (cudaGetLastError() != cudaSuccess) return cuda_fail("ctl_begin");
+  CtlStatus b = *e->hst;
+  if (info) {
+    info->v = b.v;
+    info->n_ready = b.n_ready;
+  }
+  if (b.status != ST_CONTINUE) {
+    if (b.status == SRL_GROUP_READY) e->group_state = 1;
+    if (b.status < 0) return fail(b.status, b.status == SRL_E_CAPACITY ? "srl_decode_step: KV pool / prefill capacity"
+                                                                     : (b.status == SRL_E_EMPTY ? "srl_decode_step: nothing submitted"
+                                                                                                 : "srl_decode_step: state"));
+    return b.status;
+  }
+  const Ctl& c = e->ctl;
+  // prefill of newly admitted sequences (prompt ++ kept tokens), in chunks
+  for (int r0 = 0; r0 < b.m_pre; r0 += e->s.prefill_chunk) {
+    const int mc = b.m_pre - r0 < e->s.prefill_chunk ? b.m_pre - r0 : e->s.prefill_chunk;
+    forward(e, mc, c.pre_tok + r0, c.pre_pos + r0, c.pre_slot + r0, false);
+  }
+  // decode of every local slot
+  forward(e, e->s.Q_g, c.row_tok, c.row_pos, e->row_slot_id, true);
+  SampleArgs sa{};
+  sa.logits = e->logits;
+  sa.M = e->s.Q_g;
+  sa.V = e->m.V;
+  sa.row_pos = c.row_pos;
+  sa.row_n = c.row_n;
+  sa.row_traj = c.row_traj;
+  sa.row_restarts = c.row_restarts;
+  sa.invT = 1.0f / e->s.temperature;
+  sa.seed = e->s.sample_seed;
+  sa.tok_out = c.samp_tok + (size_t)e->rank * e->s.Q_g;
+  sa.lp_out = c.samp_lp + (size_t)e->rank * e->s.Q_g;
+  sample(sa, st);
+  e->launches++;
+  ctl_end(c, st);
+  e->launches++;
+  cudaEventRecord(e->ev1, st);
+  read_status(e);
+  if (cudaGetLastError() != cudaSuccess) return cuda_fail("decode step");
+  const CtlStatus& en = *e->hst;
+  if (info) {
+    info->k = en.k - 1;
+    info->r_k = en.r_k;
+    info->n_finished = en.n_fin;
+    info->n_ready = en.n_ready;
+    info->n_admitted = b.n_admit;
+    info->n_prefill_tokens = b.m_pre;
+    info->v = en.v;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e->ev0, e->ev1);
+    info->dt_ms = ms;
+  }
+  if (en.status == SRL_GROUP_READY) e->group_state = 1;
+  return en.status;
+}
+
+int32_t srl_harvest_finished(srl_engine* e, int32_t cap_recs, srl_traj* recs, int32_t* n_out, int32_t* toks,
+                             float* logprobs, int32_t* versions, int64_t cap_toks) {
+  if (!e) return fail(SRL_E_INVALID_ARG, "srl_harvest_finished: null engine");
+  if (e->group_state != 1) return fail(SRL_E_STATE, "srl_harvest_finished: no group is ready");
+  ctl_harvest(e->ctl, e->st);
+  e->launches++;
+  read_status(e);
+  const CtlStatus& h = *e->hst;
+  if (h.status == SRL_E_CAPACITY) return fail(SRL_E_CAPACITY, "srl_harvest_finished: engine staging too small");
+  const int n = h.group_n;
+  const long long total = h.m_pre;
+  if (n_out) *n_out = n;
+  if (n > cap_recs || total > cap_toks || !recs) return fail(SRL_E_CAPACITY, "srl_harvest_finished: caller buffers too small");
+  cudaMemcpyAsync(recs, e->ctl.h_rec, sizeof(srl_traj) * n, cudaMemcpyDeviceToHost, e->st);
+  if (toks) cudaMemcpyAsync(toks, e->ctl.h_tok, 4 * total, cudaMemcpyDeviceToHost, e->st);
+  if (logprobs) cudaMemcpyAsync(logprobs, e->ctl.h_lp, 4 * total, cudaMemcpyDeviceToHost, e->st);
+  if (versions) cudaMemcpyAsync(versions, e->ctl.h_ver, 4 * total, cudaMemcpyDeviceToHost, e->st);
+  const int two = 2;
+  cudaMemcpyAsync(&e->ctl.s->group_state, &two, 4, cudaMemcpyHostToDevice, e->st);
+  if (cudaStreamSynchronize(e->st) != cudaSuccess) return cuda_fail("srl_harvest_finished");
+  for (int i = 0; i < n; ++i) {
+    const long long pi = recs[i].prompt_id;
+    recs[i].prompt_id = (pi >= 0 && pi < (long long)e->prompt_ids.size()) ? (int64_t)e->prompt_ids[pi] : -1;
+  }
+  e->group_state = 2;
+  return SRL_OK;
+}
+
+int32_t srl_load_policy_weights(srl_engine* e, const void* flat_w, int64_t version) {
+  if (!e) return fail(SRL_E_INVALID_ARG, "srl_load_policy_weights: null engine");
+  if (e->group_state == 1) return fail(SRL_E_STATE, "srl_load_policy_weights: harvest the ready group first");
+  if (version < 0 || (e->v_valid && version <= e->v))
+    return fail(SRL_E_STATE, "srl_load_policy_weights: policy version must increase");
+  if (flat_w && flat_w != e->W) {
+    cudaMemcpyAsync(e->W, flat_w, e->wl.total, cudaMemcpyDeviceToDevice, e->st);
+  }
+  ctl_bump(e->ctl, (int)version, e->st);
+  e->launches++;
+  read_status(e);
+  if (cudaGetLastError() != cudaSuccess) return cuda_fail("srl_load_policy_weights");
+  if (e->hst->status < 0) return fail(e->hst->status, "srl_load_policy_weights: capacity (resumed list)");
+  e->v = version;
+  e->v_valid = true;
+  e->group_state = 0;
+  return SRL_OK;
+}
+
+int32_t srl_get_trace(srl_engine* e, int64_t from, int32_t cap, srl_trace_rec* out, int32_t* n_out, int64_t* n_total) {
+  if (!e || from < 0 || cap < 0) return fail(SRL_E_INVALID_ARG, "srl_get_trace: bad arguments");
+  long long total = 0;
+  cudaMemcpyAsync(&total, &e->ctl.s->n_events, 8, cudaMemcpyDeviceToHost, e->st);
+  cudaStreamSynchronize(e->st);
+  if (n_total) *n_total = total;
+  long long lo = total - e->z.ev_cap;
+  if (lo < 0) lo = 0;
+  if (from < lo) from = lo;
+  long long cnt = total - from;
+  if (cnt > cap) cnt = cap;
+  if (cnt < 0) cnt = 0;
+  long long done = 0;
+  while (done < cnt) {
+    const long long idx = (from + done) % e->z.ev_cap;
+    long long run = e->z.ev_cap - idx;
+    if (run > cnt - done) run = cnt - done;
+    cudaMemcpyAsync(out + done, e->ctl.events + idx * 6, 24 * run, cudaMemcpyDeviceToHost, e->st);
+    done += run;
+  }
+  if (cudaStreamSynchronize(e->st) != cudaSuccess) return cuda_fail("srl_get_trace");
+  if (n_out) *n_out = (int32_t)cnt;
+  return SRL_OK;
+}
+
+int32_t srl_get_counters(srl_engine* e, int64_t* raw, int64_t* disc, int64_t* emitted, int64_t* groups, int64_t* launches) {
+  if (!e) return fail(SRL_E_INVALID_ARG, "srl_get_counters: null engine");
+  CtlState st;
+  cudaMemcpyAsync(&st, e->ctl.s, sizeof(CtlState), cudaMemcpyDeviceToHost, e->st);
+  if (cudaStreamSynchronize(e->st) != cudaSuccess) return cuda_fail("srl_get_counters");
+  if (raw) *raw = st.raw_tokens;
+  if (disc) *disc = st.discarded_tokens;
+  if (emitted) *emitted = st.emitted;
+  if (groups) *groups = st.n_groups;
+  if (launches) *launches = e->launches;
+  return SRL_OK;
+}
+
+int32_t srl_set_cache_bound(srl_engine* e, int32_t K) {
+  if (!e) return fail(SRL_E_INVALID_ARG, "srl_set_cache_bound: null engine");
+  if (e->group_state == 1) return fail(SRL_E_STATE, "srl_set_cache_bound: a group is pending");
+  if (K < -1) return fail(SRL_E_INVALID_ARG, "srl_set_cache_bound: K must be >= -1");
+  e->s.K = K;
+  cudaMemcpyAsync(&e->ctl.s->K, &K, 4, cudaMemcpyHostToDevice, e->st);
+  if (cudaStreamSynchronize(e->st) != cudaSuccess) return cuda_fail("srl_set_cache_bound");
+  return SRL_OK;
+}
+
+}  // extern "C"
+
+extern "C" int32_t srl_debug_copy_logits(srl_engine* e, float* out_host, int64_t cap_floats) {
+  if (!e || !out_host) return fail(SRL_E_INVALID_ARG, "srl_debug_copy_logits: bad arguments");
+  const long long n = (long long)e->s.Q_g * e->m.V;
+  if (cap_floats < n) return fail(SRL_E_CAPACITY, "srl_debug_copy_logits: buffer too small");
+  cudaMemcpyAsync(out_host, e->logits, 4 * n, cudaMemcpyDeviceToHost, e->st);
+  if (cudaStreamSynchronize(e->st) != cudaSuccess) return cuda_fail("srl_debug_copy_logits");
+  return SRL_OK;
+}

@@ -1,0 +1,147 @@
+// ops_abi.cu — extern "C" op-level entry points (include/srl_ops.h).
+#include <cstdio>
+#include <string>
+
+#include "kernels.hpp"
+#include "srl_ops.h"
+
+namespace srl {
+thread_local std::string g_last_error = "ok";
+void set_error(const char* fmt, const char* a = "", long b = 0) {
+  char buf[512];
+  snprintf(buf, sizeof(buf), fmt, a, b);
+  g_last_error = buf;
+}
+}  // namespace srl
+
+using namespace srl;
+
+extern "C" const char* srl_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" int32_t srl_op_gemm_bf16(const void* X, int32_t M, const void* W, int32_t N, int32_t K, float* out,
+                                    int32_t splits, void* stream) {
+  int r = gemm_bf16_partials(reinterpret_cast<const __nv_bfloat16*>(X), M,
+                             reinterpret_cast<const __nv_bfloat16*>(W), N, K, out, splits,
+                             reinterpret_cast<cudaStream_t>(stream));
+  if (r) set_error("srl_op_gemm_bf16: %s (code %ld)", r == -1 ? "bad shape/splits" : "launch/tma failure", r);
+  return r;
+}
+
+extern "C" int32_t srl_op_gemm_splits(int32_t M, int32_t N, int32_t K, int32_t num_sms) {
+  return gemm_choose_splits(M, N, K, num_sms);
+}
+
+// ---------------------------------------------------------------- attention op
+#include "layers.hpp"
+#include "tma.hpp"
+
+static size_t al256(size_t x) { return (x + 255) / 256 * 256; }
+
+static size_t attn_ws_layout(int M, int Hq, int Hkv, int dh, int max_ctx, size_t* offs) {
+  const int G = Hq / Hkv;
+  const int items = attn_max_items(M, Hkv, max_ctx);
+  size_t o = 0;
+  offs[0] = o; o += al256(12ull * items);            // items
+  offs[1] = o; o += al256(64);                        // n_items
+  offs[2] = o; o += al256(4ull * M);                  // row_item0
+  offs[3] = o; o += al256(4ull * M);                  // row_nchunk
+  offs[4] = o; o += al256(4ull * items * G * dh);     // part_o
+  offs[5] = o; o += al256(8ull * items * G);          // part_ml
+  offs[6] = o; o += al256(2ull * M * Hq * dh);        // bf16 out
+  offs[7] = o; o += al256(4ull * M);                  // row_slot identity
+  return o;
+}
+
+extern "C" int64_t srl_op_attention_workspace(int32_t M, int32_t Hq, int32_t Hkv, int32_t dh, int32_t max_ctx) {
+  size_t offs[8];
+  if (M <= 0 || Hq <= 0 || Hkv <= 0 || Hq % Hkv || dh <= 0 || max_ctx <= 0) return -1;
+  return (int64_t)attn_ws_layout(M, Hq, Hkv, dh, max_ctx, offs);
+}
+
+__global__ void iota_kernel(int* p, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = i;
+}
+
+extern "C" int32_t srl_op_attention(const void* q, const void* k_pool, const void* v_pool, int32_t n_pages,
+                                    const int32_t* page_table, int32_t max_pages, const int32_t* row_pos, int32_t M,
+                                    int32_t Hq, int32_t Hkv, int32_t dh, int32_t kv_fp32, int32_t max_ctx,
+                                    void* workspace, float* out_f32, void* stream) {
+  if (M <= 0 || Hq <= 0 || Hkv <= 0 || Hq % Hkv || Hq / Hkv > 8 || (dh != 32 && dh != 64 && dh != 128) ||
+      n_pages <= 0 || max_ctx <= 0 || max_pages * 64 < max_ctx) {
+    set_error("srl_op_attention: %s", "bad shape", 0);
+    return -1;
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  size_t offs[8];
+  attn_ws_layout(M, Hq, Hkv, dh, max_ctx, offs);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
+  AttnArgs a{};
+  a.q = q;
+  a.k_pool = k_pool;
+  a.v_pool = v_pool;
+  a.row_pos = row_pos;
+  a.row_slot = reinterpret_cast<int*>(ws + offs[7]);
+  a.page_table = page_table;
+  a.max_pages = max_pages;
+  a.M = M;
+  a.Hq = Hq;
+  a.Hkv = Hkv;
+  a.dh = dh;
+  a.items = reinterpret_cast<int*>(ws + offs[0]);
+  a.n_items = reinterpret_cast<int*>(ws + offs[1]);
+  a.row_item0 = reinterpret_cast<int*>(ws + offs[2]);
+  a.row_nchunk = reinterpret_cast<int*>(ws + offs[3]);
+  a.part_o = reinterpret_cast<float*>(ws + offs[4]);
+  a.part_ml = reinterpret_cast<float*>(ws + offs[5]);
+  a.out = reinterpret_cast<__nv_bfloat16*>(ws + offs[6]);
+  a.max_items = attn_max_items(M, Hkv, max_ctx);
+  a.scale = 1.0f / sqrtf((float)dh);
+  iota_kernel<<<(M + 255) / 256, 256, 0, st>>>(const_cast<int*>(a.row_slot), M);
+  CUtensorMap tk, tv;
+  if (!kv_fp32) {
+    const uint32_t bc = dh < 64 ? dh : 64;
+    const uint64_t rows = (uint64_t)n_pages * Hkv * 64;
+    if (tma_encode_2d(&tk, k_pool, rows, dh, (uint64_t)dh * 2, 64, bc, 2, bc == 64) ||
+        tma_encode_2d(&tv, v_pool, rows, dh, (uint64_t)dh * 2, 64, bc, 2, bc == 64)) {
+      set_error("srl_op_attention: %s", "TMA encode failed", 0);
+      return -2;
+    }
+  }
+  attn_plan(a, 1, st);
+  attn_run(a, kv_fp32 != 0, &tk, &tv, st);
+  attn_combine_f32(a, out_f32, st);
+  if (cudaGetLastError() != cudaSuccess) {
+    set_error("srl_op_attention: %s", "launch failure", 0);
+    return -3;
+  }
+  return 0;
+}
+
+// ---------------------------------------------------------------- sampler op
+extern "C" int32_t srl_op_sample(const float* logits, int32_t M, int32_t V, const int32_t* row_n,
+                                 const int32_t* row_traj, const int32_t* row_restarts, float temperature,
+                                 uint64_t seed, const int32_t* row_active, int32_t* tok_out, float* lp_out,
+                                 void* stream) {
+  if (M < 0 || V <= 0 || !(temperature > 0.f)) {
+    set_error("srl_op_sample: %s", "bad arguments", 0);
+    return -1;
+  }
+  SampleArgs a{};
+  a.logits = logits;
+  a.M = M;
+  a.V = V;
+  a.row_pos = row_active;
+  a.row_n = row_n;
+  a.row_traj = row_traj;
+  a.row_restarts = row_restarts;
+  a.invT = 1.0f / temperature;
+  a.seed = seed;
+  a.tok_out = tok_out;
+  a.lp_out = lp_out;
+  sample(a, reinterpret_cast<cudaStream_t>(stream));
+  if (cudaGetLastError() != cudaSuccess) {
+    set_error("srl_op_sample: %s", "launch failure", 0);
+    return -3;
+  }
+  return 0;
+}

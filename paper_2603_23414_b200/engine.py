@@ -1,0 +1,169 @@
+"""Thin Python binding of the SortedRL rollout engine (include/srl.h).
+
+Argument marshalling only: device memory comes from torch and is lent to the
+C library; every step of the rollout path runs in libsrl.so.  Names follow the
+C ABI: submit_prompts, decode_step, harvest_finished, load_policy_weights.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import Arena, Comm, ModelCfg, SchedCfg, StepInfo, TraceRec, TrajRec, check
+
+OK, GROUP_READY, DONE = 0, 1, 2
+EV_NAMES = {0: "STEP", 1: "LOAD", 2: "ADMIT", 3: "PREEMPT", 4: "FINISH", 5: "EMIT", 6: "DISCARD", 7: "SCAVENGE",
+            8: "EMIT_MEMBER"}
+
+
+def _i32p(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+@dataclass
+class Harvest:
+    records: list          # dicts per trajectory (group order)
+    tokens: np.ndarray     # int32, concatenated
+    logprobs: np.ndarray   # float32
+    versions: np.ndarray   # int32
+
+
+class RolloutEngine:
+    """One engine per GPU.  `model` / `sched` are duck-typed records with the
+    srl_model_cfg / srl_sched_cfg field names (workload.configs provides them)."""
+
+    def __init__(self, model, sched, *, max_traj: int, max_prompt: int, prefill_chunk: int = 2048,
+                 device: int = 0, stream=None, rank: int = 0, world: int = 1):
+        import torch
+        self.torch = torch
+        self.lib = _lib.load()
+        self.model, self.sched = model, sched
+        self.dev = torch.device("cuda", device)
+        self.m = ModelCfg(model.L, model.d, model.Hq, model.Hkv, model.dh, model.ff, model.V,
+                          float(model.rope_theta), float(model.rms_eps), int(model.qkv_bias))
+        self.s = SchedCfg(sched.Q_g, sched.U, sched.K, sched.pool_prompts, sched.G, sched.cap, sched.page_tokens,
+                          sched.kv_pages, sched.mode, sched.resume, sched.barrier, sched.stop, sched.eos_id,
+                          sched.kv_dtype, float(sched.temperature), int(sched.sample_seed), max_traj, max_prompt,
+                          prefill_chunk)
+        wb, kb, sb = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        check(self.lib.srl_arena_sizes(C.byref(self.m), C.byref(self.s), world, C.byref(wb), C.byref(kb),
+                                       C.byref(sb)), "srl_arena_sizes")
+        self.bytes = (wb.value, kb.value, sb.value)
+        self.W = torch.empty(wb.value, dtype=torch.uint8, device=self.dev)
+        self.KV = torch.empty(kb.value, dtype=torch.uint8, device=self.dev)
+        self.S = torch.empty(sb.value, dtype=torch.uint8, device=self.dev)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.dev)
+        arena = Arena(self.W.data_ptr(), self.KV.data_ptr(), self.S.data_ptr(), wb.value, kb.value, sb.value)
+        comm = None
+        if world > 1:
+            comm = Comm()
+            comm.rank, comm.world = rank, world
+        self.h = C.c_void_p()
+        check(self.lib.srl_create(C.byref(self.m), C.byref(self.s), device, C.c_void_p(self.stream.cuda_stream),
+                                  C.byref(arena), C.byref(comm) if comm else None, C.byref(self.h)), "srl_create")
+        self.max_traj = max_traj
+        self.Q_g, self.V = sched.Q_g, model.V
+
+    # ------------------------------------------------------------------ weights
+    def weight_view(self, name: str):
+        n = C.c_int64()
+        off = self.lib.srl_weight_offset(C.byref(self.m), name.encode(), C.byref(n))
+        if off < 0:
+            raise KeyError(name)
+        t = self.W[off:off + 2 * n.value].view(self.torch.bfloat16)
+        return t
+
+    def load_policy_weights(self, version: int, flat=None):
+        ptr = C.c_void_p(flat.data_ptr()) if flat is not None else None
+        return check(self.lib.srl_load_policy_weights(self.h, ptr, int(version)), "srl_load_policy_weights")
+
+    # ------------------------------------------------------------------ rollout
+    def submit_prompts(self, prompt_ids, tok_off, toks, forced_len=None):
+        ids = np.ascontiguousarray(prompt_ids, dtype=np.uint64)
+        off = np.ascontiguousarray(tok_off, dtype=np.int32)
+        tk = np.ascontiguousarray(toks, dtype=np.int32)
+        fl = None if forced_len is None else np.ascontiguousarray(forced_len, dtype=np.int32)
+        return check(self.lib.srl_submit_prompts(self.h, len(ids), _i32p(ids), _i32p(off), _i32p(tk),
+                                                 _i32p(fl) if fl is not None else None), "srl_submit_prompts")
+
+    def decode_step(self):
+        info = StepInfo()
+        rc = check(self.lib.srl_decode_step(self.h, C.byref(info)), "srl_decode_step")
+        return rc, info
+
+    def harvest_finished(self, cap_recs: int = 4096, cap_toks: int | None = None) -> Harvest:
+        cap_toks = cap_toks if cap_toks is not None else cap_recs * self.sched.cap
+        recs = (TrajRec * cap_recs)()
+        n = C.c_int32()
+        toks = np.empty(cap_toks, dtype=np.int32)
+        lps = np.empty(cap_toks, dtype=np.float32)
+        vers = np.empty(cap_toks, dtype=np.int32)
+        check(self.lib.srl_harvest_finished(self.h, cap_recs, recs, C.byref(n), _i32p(toks), _i32p(lps), _i32p(vers),
+                                            cap_toks), "srl_harvest_finished")
+        out = []
+        total = 0
+        for i in range(n.value):
+            r = recs[i]
+            out.append({f: getattr(r, f) for f, _ in TrajRec._fields_})
+            total = max(total, r.tok_offset + r.len)
+        return Harvest(out, toks[:total].copy(), lps[:total].copy(), vers[:total].copy())
+
+    def set_cache_bound(self, K: int):
+        return check(self.lib.srl_set_cache_bound(self.h, int(K)), "srl_set_cache_bound")
+
+    # ------------------------------------------------------------------ introspection
+    def trace(self, start: int = 0, cap: int = 1 << 20):
+        recs = (TraceRec * cap)()
+        n, tot = C.c_int32(), C.c_int64()
+        check(self.lib.srl_get_trace(self.h, start, cap, recs, C.byref(n), C.byref(tot)), "srl_get_trace")
+        return [(recs[i].kind, recs[i].a, recs[i].b, recs[i].c, recs[i].d, recs[i].e) for i in range(n.value)], tot.value
+
+    def counters(self):
+        v = [C.c_int64() for _ in range(5)]
+        check(self.lib.srl_get_counters(self.h, *[C.byref(x) for x in v]), "srl_get_counters")
+        return dict(zip(["raw_tokens", "discarded_tokens", "emitted", "groups", "kernel_launches"], [x.value for x in v]))
+
+    def debug_logits(self) -> np.ndarray:
+        out = np.empty((self.Q_g, self.V), dtype=np.float32)
+        check(self.lib.srl_debug_copy_logits(self.h, _i32p(out), out.size), "srl_debug_copy_logits")
+        return out
+
+    def close(self):
+        if self.h:
+            self.lib.srl_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def events_to_oracle_form(trace):
+    """Convert the engine's trace records into the oracle's event tuples
+    (oracle/sched.py) and the (k, r_k) step trace."""
+    ev, steps = [], []
+    i = 0
+    while i < len(trace):
+        kind, a, b, c, d, e = trace[i]
+        name = EV_NAMES[kind]
+        if name == "STEP":
+            steps.append((a, b))
+        elif name == "LOAD":
+            ev.append(("LOAD", a, b, c, d))
+        elif name in ("ADMIT", "PREEMPT", "FINISH"):
+            ev.append((name, a, b, c, d))
+        elif name == "EMIT":
+            members = tuple(trace[i + 1 + j][3] for j in range(c))
+            ev.append(("EMIT", a, b, members, d))
+            i += c
+        elif name == "DISCARD":
+            ev.append(("DISCARD", a, b, {1: "pending", 2: "running", 3: "ready"}[c]))
+        elif name == "SCAVENGE":
+            ev.append(("SCAVENGE", a, b, c))
+        i += 1
+    return ev, steps

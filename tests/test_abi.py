@@ -1,0 +1,80 @@
+"""The C-ABI library loads and exports every function include/*.h declares (CPU only,
+no compute calls)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+INC = os.path.join(ROOT, "include")
+LIB = os.path.join(ROOT, "paper_2603_23414_b200", "libsrl.so")
+
+
+def _declared():
+    names = []
+    for h in sorted(os.listdir(INC)):
+        if not h.endswith(".h"):
+            continue
+        src = open(os.path.join(INC, h)).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        names += re.findall(r"^\s*(?:const\s+)?\w+\s*\*?\s*(srl_\w+)\s*\(", src, flags=re.M)
+    return sorted(set(names))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(LIB):
+        from paper_2603_23414_b200 import build
+        build.build()
+    return ctypes.CDLL(LIB)
+
+
+def test_headers_declare_the_boundary():
+    names = _declared()
+    for n in ("srl_create", "srl_submit_prompts", "srl_decode_step", "srl_harvest_finished",
+              "srl_load_policy_weights", "srl_op_gemm_bf16", "srl_op_attention", "srl_op_sample"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    missing = [n for n in _declared() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_library_is_sm100a_and_uses_tcgen05_tma():
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", LIB], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    sass = out.stdout
+    assert "sm_100a" in subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-lelf", LIB], capture_output=True,
+                                       text=True).stdout
+    assert "UTCHMMA" in sass          # tcgen05.mma
+    assert "UTMALDG" in sass          # TMA tensor loads
+    assert "LDTM" in sass             # tcgen05.ld
+    assert "HMMA" in sass             # attention mma.sync
+
+
+def test_arena_sizes_and_validation_on_cpu(lib):
+    """Pure host calls (no GPU needed): sizing, weight layout, argument validation."""
+    from paper_2603_23414_b200 import _lib
+    from workload.configs import LLAMA8B, TINY
+    L = _lib.load()
+    m = _lib.ModelCfg(TINY.L, TINY.d, TINY.Hq, TINY.Hkv, TINY.dh, TINY.ff, TINY.V, 1e4, 1e-5, 0)
+    s = _lib.SchedCfg(16, 4, -1, 16, 1, 64, 64, 64, 0, 0, 0, 0, -1, 1, 1.0, 3, 64, 16, 256)
+    w, k, sc = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    assert L.srl_arena_sizes(ctypes.byref(m), ctypes.byref(s), 1, ctypes.byref(w), ctypes.byref(k), ctypes.byref(sc)) == 0
+    assert k.value == 2 * TINY.L * 64 * TINY.Hkv * 64 * TINY.dh * 4
+    n = ctypes.c_int64()
+    off_q = L.srl_weight_offset(ctypes.byref(m), b"L0.wq", ctypes.byref(n))
+    off_k = L.srl_weight_offset(ctypes.byref(m), b"L0.wk", None)
+    assert n.value == TINY.Hq * TINY.dh * TINY.d and off_k == off_q + 2 * n.value   # q,k,v contiguous
+    assert L.srl_weight_offset(ctypes.byref(m), b"nope", None) == -1
+    s.U = 999                                   # U > pool
+    assert L.srl_arena_sizes(ctypes.byref(m), ctypes.byref(s), 1, None, None, None) == -1
+    assert b"pool" in L.srl_last_error()
+    m8 = _lib.ModelCfg(LLAMA8B.L, LLAMA8B.d, LLAMA8B.Hq, LLAMA8B.Hkv, LLAMA8B.dh, LLAMA8B.ff, LLAMA8B.V, 5e5, 1e-5, 0)
+    s8 = _lib.SchedCfg(256, 64, -1, 1024, 1, 8192, 64, 12000, 0, 0, 0, 0, -1, 0, 1.0, 3, 2048, 256, 4096)
+    assert L.srl_arena_sizes(ctypes.byref(m8), ctypes.byref(s8), 1, ctypes.byref(w), ctypes.byref(k), ctypes.byref(sc)) == 0
+    assert abs(w.value - 16.06e9) / 16.06e9 < 0.01           # bf16 LLaMA-3.1-8B weights

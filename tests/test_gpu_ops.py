@@ -1,0 +1,164 @@
+"""GPU parity of the individual hot-path ops (C-ABI op entry points) against the CPU oracle."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle.attention import paged_attention  # noqa: E402
+from oracle.sampler import sample_row  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2603_23414_b200 import _lib
+    return _lib.load()
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+# ------------------------------------------------------------------ GEMM (tcgen05)
+@pytest.mark.parametrize("M,N,K", [(1, 128, 64), (16, 256, 128), (200, 384, 256), (256, 6144, 4096),
+                                   (64, 4096, 14336), (600, 512, 128), (37, 1000, 192), (256, 7168, 5120)])
+def test_gemm_matches_fp64_reference(lib, M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
+    X = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    sp = lib.srl_op_gemm_splits(M, N, K, 148)
+    out = torch.full((sp, M, N), float("nan"), device="cuda")
+    assert lib.srl_op_gemm_bf16(X.data_ptr(), M, W.data_ptr(), N, K, out.data_ptr(), sp, _stream()) == 0
+    torch.cuda.synchronize()
+    ref = X.double() @ W.double().t()
+    got = out.sum(0).double()
+    # fp32 accumulation of K products: |err| <= K * 2^-24 * sum|x||w| (loose), checked per element
+    bound = (X.double().abs() @ W.double().abs().t()) * (K * 2.0 ** -24) + 1e-12
+    assert ((got - ref).abs() <= bound).all()
+    assert ((got - ref).norm() / ref.norm()).item() < 1e-5
+
+
+def test_gemm_rejects_bad_shapes(lib):
+    assert lib.srl_op_gemm_bf16(0, 16, 0, 128, 100, 0, 1, _stream()) < 0      # K % 64
+    assert lib.srl_op_gemm_bf16(0, 16, 0, 128, 128, 0, 3, _stream()) < 0      # splits > K/64
+
+
+# ------------------------------------------------------------------ paged attention
+def _attn_case(M, Hq, Hkv, dh, ctxs, n_pages, seed, dtype):
+    rng = np.random.default_rng(seed)
+    max_ctx = max(ctxs)
+    max_pages = (max_ctx + 63) // 64
+    pt = np.zeros((M, max_pages), dtype=np.int32)
+    perm = rng.permutation(n_pages)
+    used = 0
+    for r in range(M):
+        need = (ctxs[r] + 63) // 64
+        pt[r, :need] = perm[used:used + need]
+        used += need
+    assert used <= n_pages
+    q = rng.normal(size=(M, Hq, dh)).astype(np.float32)
+    kp = rng.normal(size=(n_pages, Hkv, 64, dh)).astype(np.float32)
+    vp = rng.normal(size=(n_pages, Hkv, 64, dh)).astype(np.float32)
+    if dtype == torch.bfloat16:   # both sides see the same bf16 values
+        q, kp, vp = (torch.from_numpy(x).to(torch.bfloat16).float().numpy() for x in (q, kp, vp))
+    return q, kp, vp, pt, np.asarray(ctxs, dtype=np.int32) - 1, max_ctx, max_pages
+
+
+def _run_attn(lib, q, kp, vp, pt, pos, max_ctx, max_pages, dtype, Hq, Hkv, dh):
+    M = q.shape[0]
+    tq = torch.from_numpy(q).to(dtype).cuda()
+    tk = torch.from_numpy(kp).to(dtype).cuda()
+    tv = torch.from_numpy(vp).to(dtype).cuda()
+    tpt = torch.from_numpy(pt).cuda()
+    tpos = torch.from_numpy(pos).cuda()
+    ws = torch.empty(lib.srl_op_attention_workspace(M, Hq, Hkv, dh, max_ctx), dtype=torch.uint8, device="cuda")
+    out = torch.full((M, Hq, dh), float("nan"), device="cuda")
+    rc = lib.srl_op_attention(tq.data_ptr(), tk.data_ptr(), tv.data_ptr(), kp.shape[0], tpt.data_ptr(), max_pages,
+                              tpos.data_ptr(), M, Hq, Hkv, dh, 1 if dtype == torch.float32 else 0, max_ctx,
+                              ws.data_ptr(), out.data_ptr(), _stream())
+    assert rc == 0
+    torch.cuda.synchronize()
+    return out.cpu().numpy().astype(np.float64)
+
+
+SHAPES = [(4, 2, 32), (32, 8, 128), (40, 8, 128), (8, 8, 64)]   # tiny, LLaMA-8B, Qwen-32B (G=5), MHA
+
+
+@pytest.mark.parametrize("Hq,Hkv,dh", SHAPES)
+def test_attention_fp32_kv_max_abs_1e3(lib, Hq, Hkv, dh):
+    """North-star bar: attention outputs within max-abs 1e-3 in fp32 mode."""
+    ctxs = [1, 63, 64, 65, 300, 700, 1000]
+    q, kp, vp, pt, pos, mc, mp = _attn_case(len(ctxs), Hq, Hkv, dh, ctxs, 64, 1, torch.float32)
+    got = _run_attn(lib, q, kp, vp, pt, pos, mc, mp, torch.float32, Hq, Hkv, dh)
+    ref = paged_attention(q, kp, vp, pt, pos + 1)
+    assert np.abs(got - ref).max() <= 1e-3
+
+
+@pytest.mark.parametrize("Hq,Hkv,dh", SHAPES)
+def test_attention_bf16_kv(lib, Hq, Hkv, dh):
+    """bf16 KV (TMA + mma.sync path).  The only extra rounding is P -> bf16 in
+    the P.V product: |err| <= 2^-8 * max|V| (DESIGN.md tolerance derivation)."""
+    ctxs = [1, 2, 17, 63, 64, 65, 129, 256, 257, 555, 1024, 1500]
+    q, kp, vp, pt, pos, mc, mp = _attn_case(len(ctxs), Hq, Hkv, dh, ctxs, 128, 2, torch.bfloat16)
+    got = _run_attn(lib, q, kp, vp, pt, pos, mc, mp, torch.bfloat16, Hq, Hkv, dh)
+    ref = paged_attention(q, kp, vp, pt, pos + 1)
+    assert np.abs(got - ref).max() <= 2.0 ** -8 * np.abs(vp).max()
+
+
+def test_attention_inactive_rows_and_long_context(lib):
+    Hq, Hkv, dh = 32, 8, 128
+    ctxs = [16384, 1, 8000]
+    q, kp, vp, pt, pos, mc, mp = _attn_case(3, Hq, Hkv, dh, ctxs, 420, 3, torch.bfloat16)
+    pos = pos.copy()
+    pos[1] = -1                           # inactive row -> zeros
+    got = _run_attn(lib, q, kp, vp, pt, pos, mc, mp, torch.bfloat16, Hq, Hkv, dh)
+    assert np.all(got[1] == 0)
+    ref = paged_attention(q[[0, 2]], kp, vp, pt[[0, 2]], (pos + 1)[[0, 2]])
+    assert np.abs(got[[0, 2]] - ref).max() <= 2.0 ** -8 * np.abs(vp).max()
+
+
+# ------------------------------------------------------------------ sampler
+@pytest.mark.parametrize("V,scale", [(512, 1.0), (512, 8.0), (128256, 3.0), (152064, 1.0), (1000, 0.01)])
+def test_sampler_bit_exact_tokens(lib, V, scale):
+    """Identical fp32 logits -> identical token ids (bit-exact Philox + RN-only log)."""
+    M = 6
+    rng = np.random.default_rng(V)
+    z = (rng.normal(size=(M, V)) * scale).astype(np.float32)
+    n = np.array([0, 1, 5, 100, 4095, 7], dtype=np.int32)
+    traj = np.array([0, 3, 17, 255, 1023, 9], dtype=np.int32)
+    rs = np.array([0, 0, 1, 2, 0, 7], dtype=np.int32)
+    act = np.zeros(M, dtype=np.int32)
+    seed = 0x1234_5678_9ABC
+    tz, tn, tt, tr, ta = (torch.from_numpy(x).cuda() for x in (z, n, traj, rs, act))
+    tok = torch.empty(M, dtype=torch.int32, device="cuda")
+    lp = torch.empty(M, dtype=torch.float32, device="cuda")
+    assert lib.srl_op_sample(tz.data_ptr(), M, V, tn.data_ptr(), tt.data_ptr(), tr.data_ptr(), 1.0, seed,
+                             ta.data_ptr(), tok.data_ptr(), lp.data_ptr(), _stream()) == 0
+    torch.cuda.synchronize()
+    tok, lp = tok.cpu().numpy(), lp.cpu().numpy()
+    for r in range(M):
+        t_ref, lp_ref, _ = sample_row(z[r], np.float32(1.0), seed, int(n[r]), int(traj[r]), int(rs[r]))
+        assert tok[r] == t_ref
+        assert abs(lp[r] - lp_ref) <= 2e-5 * max(1.0, abs(lp_ref)) + 1e-5
+
+
+def test_sampler_temperature_and_inactive(lib):
+    M, V = 3, 4096
+    rng = np.random.default_rng(5)
+    z = rng.normal(size=(M, V)).astype(np.float32)
+    act = np.array([0, -1, 0], dtype=np.int32)
+    zeros = np.zeros(M, dtype=np.int32)
+    tz, ta, t0 = torch.from_numpy(z).cuda(), torch.from_numpy(act).cuda(), torch.from_numpy(zeros).cuda()
+    tok = torch.empty(M, dtype=torch.int32, device="cuda")
+    lp = torch.empty(M, dtype=torch.float32, device="cuda")
+    T = 0.7
+    assert lib.srl_op_sample(tz.data_ptr(), M, V, t0.data_ptr(), t0.data_ptr(), t0.data_ptr(), T, 3,
+                             ta.data_ptr(), tok.data_ptr(), lp.data_ptr(), _stream()) == 0
+    torch.cuda.synchronize()
+    tok = tok.cpu().numpy()
+    assert tok[1] == -1
+    invT = np.float32(1.0) / np.float32(T)
+    for r in (0, 2):
+        assert tok[r] == sample_row(z[r], invT, 3, 0, 0, 0)[0]
