@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""SortedRL rollout benchmark (BASELINE.json metric: rollout tokens/s + bubble
+ratio @1/2/4/8 B200; decode %HBM roofline).
+
+A "step" is one srl_decode_step: refill/admission (+ prefill of admitted
+prompts), the policy's decode forward over the ragged batch (tcgen05 GEMMs,
+paged attention), sampling, stop detection, compaction into the rollout
+buffer, and -- when an update group is ready -- harvest of the length-sorted
+group plus the policy refresh (load_policy_weights).
+
+Workload (configs[1], "cfg2"): LLaMA-3.1-8B-shaped random-init policy on one
+B200, rollout batch Q=256, max 8k tokens, update group U=64, K=inf (partial
+mode), pool 4*Q prompts, 256-token prompts, lognormal(1600, 0.55) + 3% cap
+FORCED response lengths (DESIGN.md input recipe).  The timed window is steps
+[P+W, P+W+K) of that rollout (P = --precondition untimed steps so contexts
+are mid-rollout; W = --warmup).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--precondition P]
+  python bench.py --impl reference ...   # the CPU oracle on a bounded sample
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workload.configs import (BARRIER_TRAINED, K_INF, KV_BF16, LLAMA8B, MODE_SORTED, RESUME_KEEP_KV,  # noqa: E402
+                              STOP_FORCED, SchedConfig)
+from workload.lengths import LengthModel, sample_lengths  # noqa: E402
+from workload.prompts import make_prompts  # noqa: E402
+
+METRIC = "rollout tokens/s + bubble ratio @1/2/4/8 B200; decode %HBM roofline"
+WORKLOAD = ("cfg2: LLaMA-3.1-8B-shaped random-init bf16 policy, 1 GPU per replica, rollout batch Q_g=256, "
+            "max 8192 new tokens, update group U=64, K=inf (partial), pool 1024 prompts x 2 epochs, "
+            "256-token prompts, FORCED lognormal(1600,0.55)+3%-at-cap lengths, TRAINED barrier, KEEP_KV")
+N_PROMPTS_PER_EPOCH = 1024
+PROMPT_LEN = 256
+
+
+def cfg2_sched():
+    return SchedConfig(Q_g=256, R=1, U=64, K=K_INF, pool_prompts=N_PROMPTS_PER_EPOCH, G=1, cap=8192, page_tokens=64,
+                       kv_pages=11000, mode=MODE_SORTED, resume=RESUME_KEEP_KV, barrier=BARRIER_TRAINED,
+                       stop=STOP_FORCED, kv_dtype=KV_BF16, temperature=1.0, sample_seed=3)
+
+
+def workload_inputs(rank=0, epochs=2):
+    n = N_PROMPTS_PER_EPOCH * epochs
+    off, toks = make_prompts(1 + 1000 * rank, n, LLAMA8B.V, PROMPT_LEN)
+    L = sample_lengths(LengthModel(median=1600, sigma=0.55, tail=0.03, floor=1, cap=8192), 0 + 1000 * rank, n)
+    return off, toks, L
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), d.get("bf16_tflops_sustained", 1400.0), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
+               0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.stop_ev = [], set(), threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.1)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self.stop_ev.set()
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": float(np.median(self.samples)) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ model byte / flop model
+def step_bytes_flops(m, r, sum_ctx):
+    wl = m.L * ((m.Hq + 2 * m.Hkv) * m.dh * m.d + m.d * m.Hq * m.dh + 3 * m.d * m.ff) * 2
+    w_step = wl + m.V * m.d * 2
+    kvb = 2 * m.L * m.Hkv * m.dh * 2                       # KV bytes per token (all layers)
+    B = w_step + kvb * sum_ctx + kvb * r                    # weights + KV read + KV append
+    p_mm = w_step / 2
+    a = 4 * m.L * m.Hq * m.dh                               # attention flops per context position
+    F = 2 * p_mm * r + a * sum_ctx
+    return B, F, w_step, kvb
+
+
+# ------------------------------------------------------------------ the GPU arm
+def run_gpu(args, rank, world, dist):
+    import torch
+    from paper_2603_23414_b200.engine import DONE, GROUP_READY, RolloutEngine
+    from workload.weights import fill_engine_weights
+    torch.cuda.set_device(rank % max(1, torch.cuda.device_count()))
+    dev = torch.cuda.current_device()
+    model, sched = LLAMA8B, cfg2_sched()
+    off, toks, L = workload_inputs(rank)
+    ids = np.arange(len(off) - 1, dtype=np.uint64) + 1 + 10_000_000 * rank
+    eng = RolloutEngine(model, sched, max_traj=2 * N_PROMPTS_PER_EPOCH, max_prompt=PROMPT_LEN, prefill_chunk=4096,
+                        device=dev)
+    fill_engine_weights(eng, model, 0)
+    trainer = eng.W.clone()          # the trainer's copy of the refreshed policy (K13: same bytes re-emitted)
+    eng.load_policy_weights(0)
+    torch.cuda.synchronize()
+
+    def drive(eng, nsteps, state, harvest_host=False, stats=None):
+        done = 0
+        while done < nsteps:
+            st, info = eng.decode_step()
+            if st == DONE:
+                break
+            if info.k >= 0:
+                done += 1
+                if stats is not None:
+                    stats.append((info.r_k, info.sum_ctx, info.dt_ms, info.n_prefill_tokens, info.n_finished))
+            if st == GROUP_READY:
+                h = eng.harvest_finished(cap_recs=2048, cap_toks=2048 * sched.cap)
+                state["useful"] += sum(r["len"] for r in h.records)
+                state["d2h"] += sum(r["len"] for r in h.records) * 12 + len(h.records) * 64
+                state["v"] += 1
+                eng.load_policy_weights(state["v"], trainer)
+        return done
+
+    # ---------------- value: device-timed window, prompts resident
+    eng.submit_prompts(ids, off, toks, L)
+    state = {"useful": 0, "d2h": 0, "v": 0}
+    drive(eng, args.precondition, state)
+    drive(eng, args.warmup, state)
+    stats = []
+    state["useful"] = 0
+    c0 = eng.counters()
+    eng.set_profiling(True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stream = eng.stream              # the stream every engine kernel is launched on
+    with ClockSampler(dev) as clk:
+        e0.record(stream)
+        ran = drive(eng, args.steps, state, stats=stats)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    prof = eng.profile()
+    eng.set_profiling(False)
+    c1 = eng.counters()
+    raw = c1["raw_tokens"] - c0["raw_tokens"]
+    useful = state["useful"]
+    launches = c1["kernel_launches"] - c0["kernel_launches"]
+    eng.close()
+    del eng
+
+    # ---------------- e2e: same window through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        eng = RolloutEngine(model, sched, max_traj=2 * N_PROMPTS_PER_EPOCH, max_prompt=PROMPT_LEN,
+                            prefill_chunk=4096, device=dev)
+        eng.W.copy_(trainer)
+        eng.load_policy_weights(0)
+        n0 = N_PROMPTS_PER_EPOCH
+        eng.submit_prompts(ids[:n0], off[:n0 + 1], toks[:off[n0]], L[:n0])
+        st2 = {"useful": 0, "d2h": 0, "v": 0}
+        drive(eng, args.precondition + args.warmup, st2)
+        st2["d2h"] = 0
+        # pinned host copies of the next epoch's prompts (the dataloader's batch)
+        import torch as _t
+        rest_off = (off[n0:] - off[n0]).astype(np.int32)
+        rest_tok = _t.from_numpy(toks[off[n0]:].copy()).pin_memory().numpy()
+        rest_len = _t.from_numpy(L[n0:].copy()).pin_memory().numpy()
+        c0 = eng.counters()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        eng.submit_prompts(ids[n0:], rest_off, rest_tok, rest_len)
+        h2d = rest_tok.nbytes + rest_off.nbytes + rest_len.nbytes + (len(ids) - n0) * 72
+        ran2 = drive(eng, args.steps, st2)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        if dist:
+            dist.barrier()
+        c1 = eng.counters()
+        raw2 = c1["raw_tokens"] - c0["raw_tokens"]
+        d2h = st2["d2h"] + ran2 * 48          # per-step status/info readbacks + harvested groups
+        e2e = {"value": raw2 / (t1 - t0), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d / max(1, ran2)),
+               "d2h_bytes_per_step": int(d2h / max(1, ran2)), "wall_ms_per_step": (t1 - t0) * 1e3 / max(1, ran2)}
+        eng.close()
+        del eng
+    return dict(ms=ms, ran=ran, raw=raw, useful=useful, stats=stats, prof=prof, launches=launches,
+                clocks=clk.summary(), e2e=e2e)
+
+
+# ------------------------------------------------------------------ CPU oracle sample
+def oracle_sample(seconds_budget=20.0, reps=None):
+    """Bounded sample of the same workload on the CPU oracle (fp64): one LLaMA-8B-shaped
+    decoder layer (1 of 32) for one row at context 1024 plus 1/32 of the LM head,
+    extrapolated to the full 32-layer model: tokens/s for one sequence."""
+    from oracle.model import Model
+    from workload.configs import ModelShape
+    from workload.weights import bf16_bits_to_f32, gen_weight_np
+    m1 = LLAMA8B.with_layers(1)
+    W = {}
+    for name in ["L0.attn_norm", "L0.wq", "L0.wk", "L0.wv", "L0.wo", "L0.mlp_norm", "L0.wg", "L0.wu", "L0.wd"]:
+        W[name] = bf16_bits_to_f32(gen_weight_np(m1, name)).astype(np.float64)
+    vs = LLAMA8B.V // 32
+    W["lm_head"] = bf16_bits_to_f32(gen_weight_np(m1, "lm_head", rows=np.arange(vs))).astype(np.float64)
+    W["final_norm"] = bf16_bits_to_f32(gen_weight_np(m1, "final_norm")).astype(np.float64)
+    mdl = Model(m1, W)
+    rng = np.random.default_rng(0)
+    ctx = 1024
+    k_hist = list(rng.normal(size=(ctx - 1, LLAMA8B.Hkv, LLAMA8B.dh)))
+    v_hist = list(rng.normal(size=(ctx - 1, LLAMA8B.Hkv, LLAMA8B.dh)))
+    x0 = rng.normal(size=LLAMA8B.d)
+    times = []
+    t_start = time.perf_counter()
+    n = 0
+    while (reps is None and time.perf_counter() - t_start < seconds_budget) or (reps is not None and n < reps):
+        K_, V_ = list(k_hist), list(v_hist)
+        t0 = time.perf_counter()
+        x = mdl.layer(0, x0, ctx - 1, K_, V_)
+        t1 = time.perf_counter()
+        _ = W["lm_head"] @ mdl.hidden(x)
+        t2 = time.perf_counter()
+        times.append(32 * (t1 - t0) + 32 * (t2 - t1))
+        n += 1
+    per_token = float(np.median(times))
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        threads = 1
+    return {"value": 1.0 / per_token, "unit": "tokens/s", "cores": threads, "kind": "oracle",
+            "host_cpus": os.cpu_count(),
+            "sample": f"oracle fp64 decode of one LLaMA-8B-shaped layer + 1/32 LM head for 1 row at ctx {ctx}, "
+                      f"x32 extrapolated to the full model; median of {len(times)} reps"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    # each reference "step" = one bounded oracle sample (see oracle_sample); the weight
+    # generation happens once inside oracle_sample and is not part of the per-step median
+    t0 = time.perf_counter()
+    res = oracle_sample(reps=max(1, args.steps) + args.warmup)
+    t1 = time.perf_counter()
+    line = {"metric": METRIC, "value": res["value"], "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 / res["value"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": WORKLOAD, "sample": res["sample"]},
+            "cpu_baseline": {"value": res["value"], "unit": "tokens/s", "cores": res["cores"], "kind": "oracle",
+                             "sample": res["sample"]},
+            "e2e": {"value": res["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--precondition", type=int, default=600)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        return run_reference(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as td
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+        td.init_process_group("nccl")
+        dist = td
+    r = run_gpu(args, rank, world, dist)
+    m = LLAMA8B
+    hbm, tf_burst, tf_sust, peak_src = load_peaks()
+    # per-rank aggregates
+    sum_ctx = sum(s[1] for s in r["stats"])
+    steps = r["ran"]
+    attn_ms, attn_n = r["prof"]["attention"]
+    # dominant kernel class (decode path)
+    dec = {k: v for k, v in r["prof"].items()
+           if k in ("attention", "gemm_qkv", "gemm_o", "gemm_gate_up", "gemm_down", "lm_head")}
+    dom = max(dec, key=lambda k: dec[k][0])
+    if dom == "attention":
+        per_unit = 2 * m.Hkv * m.dh * 2                         # K+V bytes per context token per layer
+        units = sum_ctx                                          # context tokens over all timed steps (per layer)
+        bytes_tot = per_unit * units * m.L
+        achieved = bytes_tot / (attn_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": "paged_attention", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None, "per_unit_bytes": per_unit,
+                "units_per_launch": units / max(1, steps), "launches": attn_n, "peak_source": peak_src}
+    else:
+        Nk = {"gemm_qkv": ((m.Hq + 2 * m.Hkv) * m.dh, m.d), "gemm_o": (m.d, m.Hq * m.dh),
+              "gemm_gate_up": (2 * m.ff, m.d), "gemm_down": (m.d, m.ff), "lm_head": (m.V, m.d)}[dom]
+        launches_per_step = 1 if dom == "lm_head" else m.L
+        bytes_tot = Nk[0] * Nk[1] * 2 * launches_per_step * steps
+        achieved = bytes_tot / (dec[dom][0] * 1e-3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None, "launches": dec[dom][1], "peak_source": peak_src}
+    # decode roofline fraction of the whole step
+    t_roof = 0.0
+    for (rk, sc, dt, npre, nfin) in r["stats"]:
+        B, F, _, _ = step_bytes_flops(m, rk, sc)
+        t_roof += max(B / (hbm * 1e9), F / (tf_sust * 1e12))
+    dec_frac = t_roof / (r["ms"] * 1e-3)
+    tok_s = r["raw"] / (r["ms"] * 1e-3)
+    Q = 256
+    bubble = sum(Q - s[0] for s in r["stats"]) / (Q * max(1, len(r["stats"])))
+    dts = [s[2] for s in r["stats"]]
+    bubble_t = sum((Q - s[0]) * s[2] for s in r["stats"]) / (Q * max(1e-9, sum(dts)))
+    if dist:
+        import torch
+        t = torch.tensor([r["raw"], r["useful"], r["ms"]], dtype=torch.float64, device="cuda")
+        tot = t.clone()
+        dist.all_reduce(tot)
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        tok_s = tot[0].item() / (mx[2].item() * 1e-3)
+        useful_s = tot[1].item() / (mx[2].item() * 1e-3)
+        ms = mx[2].item()
+    else:
+        useful_s = r["useful"] / (r["ms"] * 1e-3)
+        ms = r["ms"]
+    if rank != 0:
+        dist.barrier() if dist else None
+        return
+    line = {
+        "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": world, "steps": steps,
+        "warmup": args.warmup, "ms_per_step": ms / max(1, steps), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "window": f"decode steps [{args.precondition + args.warmup}, "
+                   f"{args.precondition + args.warmup + steps}) of the cfg2 rollout",
+                   "l2": "no flush needed: every step streams 15 GB of weights + the KV cache (>> 126 MB L2)",
+                   "parallelism": f"dp{world} (independent replicas)" if world > 1 else "dp1"},
+        "useful_tokens_per_s": useful_s,
+        "bubble_ratio": {"window_abstract": bubble, "window_time_weighted": bubble_t,
+                         "definition": "Eq.(bubble) P:339-342 over the timed decode steps, Q=Q_g"},
+        "decode_roofline_frac": {"value": dec_frac, "definition": "sum_k max(B_k/BW, F_k/TC) / sum_k dt_k (SURVEY 8(d))",
+                                 "BW_GBs": hbm, "TC_TFs": tf_sust},
+        "roofline": roof,
+        "kernel_ms_per_step": {k: v[0] / max(1, steps) for k, v in r["prof"].items()},
+        "gpu_launches": r["launches"],
+        "clocks": r["clocks"],
+        "e2e": r["e2e"],
+        "mean_ctx": sum_ctx / max(1, sum(s[0] for s in r["stats"])),
+    }
+    if not args.no_cpu and world == 1:
+        line["cpu_baseline"] = oracle_sample()
+    elif not args.no_cpu:
+        line["cpu_baseline"] = None
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+
+
+if __name__ == "__main__":
+    main()

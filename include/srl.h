@@ -103,7 +103,13 @@ typedef struct srl_step_info {
   int32_t n_prefill_tokens; /* prefill tokens processed on this GPU */
   int32_t v;          /* current policy version */
   float dt_ms;        /* device time of the step on this GPU (cudaEvent) */
+  int64_t sum_ctx;    /* sum over this GPU's running rows of the attended context (KV tokens read per layer) */
 } srl_step_info;
+
+/* Per-kernel-class device timing (CUDA events on the engine stream), enabled by
+ * srl_set_profiling.  Classes: */
+enum { SRL_K_GEMM_QKV = 0, SRL_K_GEMM_O = 1, SRL_K_GEMM_GU = 2, SRL_K_GEMM_DOWN = 3, SRL_K_LM_HEAD = 4,
+       SRL_K_ATTN = 5, SRL_K_ELEMWISE = 6, SRL_K_SAMPLE = 7, SRL_K_CTL = 8, SRL_K_PREFILL = 9, SRL_K_NCLASS = 10 };
 
 /* One harvested trajectory (SPEC BufferEntry / P:199). */
 typedef struct srl_traj {
@@ -192,6 +198,12 @@ int32_t srl_get_counters(srl_engine* e, int64_t* raw_tokens, int64_t* discarded_
 
 /* Change K between updates (SRL_E_STATE while a group is pending). */
 int32_t srl_set_cache_bound(srl_engine* e, int32_t K);
+
+/* Enable (1) / disable (0) per-class timing; enabling resets the accumulators. */
+int32_t srl_set_profiling(srl_engine* e, int32_t on);
+/* ms[SRL_K_NCLASS]: accumulated device milliseconds per class over decode steps
+ * (prefill passes are accumulated whole under SRL_K_PREFILL); launches[]: launch counts. */
+int32_t srl_get_profile(srl_engine* e, double* ms, int64_t* launches);
 
 /* Test accessor: copy the fp32 logits [Q_g, V] of the last decode step (local
  * slots; rows of empty slots are unspecified) to host memory. */

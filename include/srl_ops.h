@@ -19,18 +19,19 @@
 extern "C" {
 #endif
 
-/* Decode projection GEMM, split-K partials (
- * PAPER.md P:110 §2.2 "frequent loading of model weights").
- *   X   [M, K] bf16, W [N, K] bf16 (a linear layer's weight, y = x W^T),
- *   out [splits, M, N] fp32: out[s][m][n] = sum over the s-th contiguous
- *       K/64-block range of X[m][k]*W[n][k].  Sum the splits (in order) for Y.
- *   Requires K % 64 == 0, 1 <= splits <= K/64, M >= 0, N >= 0.
- *   tcgen05.mma (kind::f16, fp32 accumulate in TMEM), operands staged by TMA. */
-int32_t srl_op_gemm_bf16(const void* X, int32_t M, const void* W, int32_t N, int32_t K, float* out,
-                         int32_t splits, void* stream);
-
-/* Split count the engine would choose for an [M,N,K] GEMM on `num_sms` SMs. */
-int32_t srl_op_gemm_splits(int32_t M, int32_t N, int32_t K, int32_t num_sms);
+/* Decode projection GEMM with a fused epilogue (
+ * PAPER.md P:110 §2.2 "frequent loading of model weights").  Y = X W^T with
+ *   X [M, K] bf16, W [N, K] bf16 (a linear layer's weight), fp32 accumulation
+ *   (tcgen05.mma kind::f16, accumulator in TMEM, operands staged by TMA,
+ *   persistent stream-K with a fixed-order fixup: bit-reproducible), and
+ *   epi = 0: out fp32 [M, N]  = Y
+ *   epi = 1: out fp32 [M, N] += Y                       (residual add)
+ *   epi = 2: W has 2N rows (gate [0,N), up [N,2N)); out bf16 [M, N] = silu(Yg) * Yu
+ * workspace: device bytes >= srl_op_gemm_workspace(M, N, K, epi).
+ * Requires K % 64 == 0 and, for epi 2, N % 128 == 0. */
+int64_t srl_op_gemm_workspace(int32_t M, int32_t N, int32_t K, int32_t epi);
+int32_t srl_op_gemm_bf16(const void* X, int32_t M, const void* W, int32_t N, int32_t K, int32_t epi, void* out,
+                         void* workspace, void* stream);
 
 /* Paged decode attention with GQA (PagedAttention).
  *   q          [M, Hq, dh]  bf16 (kv_fp32 = 0) or fp32 (kv_fp32 = 1)

@@ -40,7 +40,11 @@ class Arena(C.Structure):
 
 class StepInfo(C.Structure):
     _fields_ = [("k", _I64), ("r_k", _I32), ("n_finished", _I32), ("n_ready", _I32), ("n_admitted", _I32),
-                ("n_prefill_tokens", _I32), ("v", _I32), ("dt_ms", C.c_float)]
+                ("n_prefill_tokens", _I32), ("v", _I32), ("dt_ms", C.c_float), ("sum_ctx", _I64)]
+
+
+KERNEL_CLASSES = ["gemm_qkv", "gemm_o", "gemm_gate_up", "gemm_down", "lm_head", "attention", "elementwise",
+                  "sample", "controller", "prefill"]
 
 
 class TrajRec(C.Structure):
@@ -59,8 +63,8 @@ _U64P, _I64P, _I32P = C.POINTER(_U64), C.POINTER(_I64), C.POINTER(_I32)
 # name -> (restype, argtypes)
 SIGNATURES = {
     "srl_last_error": (C.c_char_p, []),
-    "srl_op_gemm_bf16": (_I32, [_P, _I32, _P, _I32, _I32, _P, _I32, _P]),
-    "srl_op_gemm_splits": (_I32, [_I32, _I32, _I32, _I32]),
+    "srl_op_gemm_bf16": (_I32, [_P, _I32, _P, _I32, _I32, _I32, _P, _P, _P]),
+    "srl_op_gemm_workspace": (_I64, [_I32, _I32, _I32, _I32]),
     "srl_op_attention_workspace": (_I64, [_I32, _I32, _I32, _I32, _I32]),
     "srl_op_attention": (_I32, [_P, _P, _P, _I32, _P, _I32, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P, _P, _P]),
     "srl_op_sample": (_I32, [_P, _I32, _I32, _P, _P, _P, C.c_float, _U64, _P, _P, _P, _P]),
@@ -76,6 +80,8 @@ SIGNATURES = {
     "srl_get_counters": (_I32, [_P, _I64P, _I64P, _I64P, _I64P, _I64P]),
     "srl_set_cache_bound": (_I32, [_P, _I32]),
     "srl_debug_copy_logits": (_I32, [_P, _P, _I64]),
+    "srl_set_profiling": (_I32, [_P, _I32]),
+    "srl_get_profile": (_I32, [_P, C.POINTER(C.c_double), _I64P]),
 }
 
 _lib = None

@@ -424,6 +424,7 @@ __global__ void __launch_bounds__(kCtlThreads, 1) ctl_begin_kernel(Ctl c) {
     return;
   }
   // decode rows for the local slots
+  long long my_ctx = 0;
   for (int sl = threadIdx.x; sl < c.Q_g; sl += blockDim.x) {
     const int g = sl * c.R + c.rank;
     const int tid = c.slot_traj[g];
@@ -433,6 +434,7 @@ __global__ void __launch_bounds__(kCtlThreads, 1) ctl_begin_kernel(Ctl c) {
       c.row_tok[sl] = n > 0 ? c.tokens[(size_t)tid * c.cap + n - 1]
                             : c.prompt_tok[c.prompt_off[t.prompt_idx] + t.prompt_len - 1];
       c.row_pos[sl] = t.prompt_len + n - 1;
+      my_ctx += t.prompt_len + n;
       c.row_n[sl] = n;
       c.row_traj[sl] = tid;
       c.row_restarts[sl] = t.restarts;
@@ -446,8 +448,15 @@ __global__ void __launch_bounds__(kCtlThreads, 1) ctl_begin_kernel(Ctl c) {
   }
   // prefill rows of local admissions still running (prompt ++ kept[:-1])
   __shared__ int sh_off;
-  if (threadIdx.x == 0) sh_off = 0;
+  __shared__ unsigned long long sh_ctx;
+  if (threadIdx.x == 0) {
+    sh_off = 0;
+    sh_ctx = 0;
+  }
   __syncthreads();
+  atomicAdd(&sh_ctx, (unsigned long long)my_ctx);
+  __syncthreads();
+  if (threadIdx.x == 0) s->st.sum_ctx = (long long)sh_ctx;
   const int na = s->st.n_admit_local;
   for (int a = 0; a < na; ++a) {
     const int sl = c.admit_local[a];

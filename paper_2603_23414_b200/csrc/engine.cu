@@ -89,7 +89,7 @@ struct ScratchPlan {
 
 struct Sizes {
   int Q_g, R, Q_tot, max_pages, max_ctx, max_prompts, mmax, prefill_rows_max, max_items, G;
-  long long ev_cap, h_cap_tok, part_floats;
+  long long ev_cap, h_cap_tok, part_floats, n_counters;
   size_t qkv_n;
 };
 
@@ -100,7 +100,7 @@ int validate(const srl_model_cfg* m, const srl_sched_cfg* s, int world, std::str
   if (m->Hq % m->Hkv) return why = "Hq must be a multiple of Hkv", -1;
   if (m->Hq / m->Hkv > 8) return why = "GQA group > 8 not supported", -1;
   if (m->dh != 32 && m->dh != 64 && m->dh != 128) return why = "dh must be 32, 64 or 128", -1;
-  if (m->d % 64 || (m->Hq * m->dh) % 64 || m->ff % 64) return why = "d, Hq*dh, ff must be multiples of 64", -1;
+  if (m->d % 128 || (m->Hq * m->dh) % 64 || m->ff % 128) return why = "d, ff must be multiples of 128 and Hq*dh of 64", -1;
   if (s->Q_g <= 0 || s->U <= 0 || s->G <= 0 || s->cap <= 0 || s->pool_prompts <= 0 || s->kv_pages <= 0)
     return why = "Q_g, U, G, cap, pool_prompts, kv_pages must be positive", -1;
   if (s->page_tokens != kPage) return why = "page_tokens must be 64", -1;
@@ -133,19 +133,14 @@ Sizes compute_sizes(const srl_model_cfg* m, const srl_sched_cfg* s, int world) {
   const int gmax = s->max_traj < kMaxGroup ? s->max_traj : kMaxGroup;
   z.h_cap_tok = (long long)gmax * s->cap;
   z.qkv_n = (size_t)(m->Hq + 2 * m->Hkv) * m->dh;
-  // partial buffer: max over the four layer GEMMs and the LM head at the two M sizes
-  long long best = 0;
-  const int Ns[5] = {(int)z.qkv_n, m->d, 2 * m->ff, m->d, m->V};
-  const int Ks[5] = {m->d, m->Hq * m->dh, m->d, m->ff, m->d};
-  const int Ms[2] = {s->Q_g, s->prefill_chunk};
-  for (int mi = 0; mi < 2; ++mi)
-    for (int g = 0; g < 5; ++g) {
-      const int sp = gemm_choose_splits(Ms[mi], Ns[g], Ks[g], 148);
-      const long long f = (long long)sp * Ms[mi] * Ns[g];
-      if (g == 4 && (sp == 1 || mi == 1)) continue;  // LM head writes logits directly; no prefill LM head
-      if (f > best) best = f;
-    }
-  z.part_floats = best;
+  // fused-GEMM workspace: stream-K partials (2 slots per CTA, <= 2 weight tiles) + unit counters
+  z.part_floats = (long long)(gemm_workspace_bytes(z.mmax, 2, 160) / 4);
+  int nmax = (int)z.qkv_n;
+  if (m->d > nmax) nmax = m->d;
+  if (m->ff > nmax) nmax = m->ff;
+  if (m->V > nmax) nmax = m->V;
+  z.n_counters = (long long)gemm_counter_count(z.mmax, nmax);
+
   return z;
 }
 
@@ -170,7 +165,8 @@ struct srl_engine {
   float* x_res = nullptr;
   __nv_bfloat16 *xn = nullptr, *attn_out = nullptr, *act = nullptr;
   void* qbuf = nullptr;
-  float* part = nullptr;
+  float* part = nullptr;  // GEMM stream-K workspace
+  int* gcount = nullptr;  // GEMM unit counters (zero between launches)
   float* logits = nullptr;
   float *rope_cos = nullptr, *rope_sin = nullptr;
   int* row_slot_id = nullptr;  // identity rows 0..Q_g-1
@@ -186,12 +182,85 @@ struct srl_engine {
   long long v = -1;
   long long launches = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // profiling: event pairs bracketing kernel classes.  `direct` is refilled every
+  // step; `gset` belongs to the captured decode graph and is re-recorded by
+  // every replay.
+  struct EvSet {
+    std::vector<cudaEvent_t> ev;
+    size_t used = 0;
+    std::vector<int> cls, nl;
+  };
+  bool prof = false;
+  bool capturing = false;
+  EvSet direct, gset;
+  double prof_ms[SRL_K_NCLASS] = {0};
+  long long prof_launch[SRL_K_NCLASS] = {0};
+  // CUDA graph of the static decode tail (forward + sampler + ctl_end)
+  bool use_graph = true;
+  int direct_steps = 0;
+  cudaGraphExec_t gexec = nullptr;
+  long long g_launches = 0;
 };
 
 namespace {
 
-int cuda_fail(const char* what) {
-  cudaError_t e = cudaGetLastError();
+// Brackets a group of launches of one kernel class with CUDA events on the
+// engine stream (only when profiling is on).
+struct Prof {
+  srl_engine* e;
+  srl_engine::EvSet* S = nullptr;
+  int cls;
+  int nl;
+  Prof(srl_engine* e_, int cls_, int nlaunch = 1) : e(e_), cls(cls_), nl(nlaunch) {
+    if (cls < 0) return;
+    S = e->capturing ? &e->gset : (e->prof ? &e->direct : nullptr);
+    if (!S) return;
+    if (S->used + 2 > S->ev.size()) {
+      for (int i = 0; i < 256; ++i) {
+        cudaEvent_t ev;
+        cudaEventCreate(&ev);
+        S->ev.push_back(ev);
+      }
+    }
+    record(S->ev[S->used]);
+  }
+  // inside a stream capture the record must be an external event-record node
+  void record(cudaEvent_t ev) {
+    if (e->capturing)
+      cudaEventRecordWithFlags(ev, e->st, cudaEventRecordExternal);
+    else
+      cudaEventRecord(ev, e->st);
+  }
+  ~Prof() {
+    if (!S) return;
+    record(S->ev[S->used + 1]);
+    S->cls.push_back(cls);
+    S->nl.push_back(nl);
+    S->used += 2;
+  }
+};
+
+void prof_collect(srl_engine* e, srl_engine::EvSet& S, bool keep) {  // after a stream sync
+  if (e->prof) {
+    for (size_t i = 0; i < S.cls.size(); ++i) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, S.ev[2 * i], S.ev[2 * i + 1]) != cudaSuccess) {
+        cudaGetLastError();  // timing unavailable: never poison the engine's error state
+        ms = 0.f;
+      }
+      e->prof_ms[S.cls[i]] += ms;
+      e->prof_launch[S.cls[i]] += S.nl[i];
+    }
+  }
+  if (!keep) {
+    S.cls.clear();
+    S.nl.clear();
+    S.used = 0;
+  }
+}
+
+int cuda_fail(const char* what, cudaError_t e = cudaSuccess) {
+  if (e == cudaSuccess) e = cudaGetLastError();
   char buf[256];
   snprintf(buf, sizeof(buf), "%s: %s", what, cudaGetErrorString(e));
   g_last_error = buf;
@@ -246,6 +315,7 @@ void plan_scratch(srl_engine* e, ScratchPlan& p, bool assign) {
   e->act = (__nv_bfloat16*)P(2ull * z.mmax * m.ff);
   e->qbuf = P((e->kv_f32 ? 4ull : 2ull) * z.mmax * m.Hq * m.dh);
   e->part = (float*)P(4ull * z.part_floats);
+  e->gcount = (int*)P(4ull * z.n_counters);
   e->logits = (float*)P(4ull * z.Q_g * m.V);
   e->rope_cos = (float*)P(4ull * z.max_ctx * (m.dh / 2));
   e->rope_sin = (float*)P(4ull * z.max_ctx * (m.dh / 2));
@@ -263,14 +333,10 @@ size_t kv_bytes_for(const srl_model_cfg& m, const srl_sched_cfg& s) {
   return al((size_t)s.kv_pages * m.Hkv * kPage * m.dh * el) * 2 * m.L;
 }
 
-// ---- GEMM helper: Y partials -> returns split count used
-int run_gemm(srl_engine* e, const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N, int K, float* out,
-             long long cap_floats) {
-  int sp = gemm_choose_splits(M, N, K, e->num_sms);
-  while (sp > 1 && (long long)sp * M * N > cap_floats) --sp;
-  gemm_bf16_partials(X, M, W, N, K, out, sp, e->st);
+// ---- fused GEMM helper
+void run_gemm(srl_engine* e, const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N, int K, const GemmEpi& epi) {
+  gemm_bf16_fused(X, M, W, N, K, epi, e->part, e->gcount, e->num_sms, e->st);
   e->launches++;
-  return sp;
 }
 
 // One forward pass over M rows (decode: rows = local slots; prefill: rows = prompt tokens).
@@ -292,55 +358,112 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
   a.out = e->attn_out;
   a.max_items = e->z.max_items;
   a.scale = 1.0f / sqrtf((float)m.dh);
-  attn_plan(a, decode ? 1 : 0, st);
-  embed_norm(row_tok, row_pos, M, d, e->embed, e->lw[0].attn_norm, m.rms_eps, e->x_res, e->xn, st);
+  const int D = decode ? 0 : -1000;  // profiling class offset (prefill is timed as a whole)
+  {
+    Prof p1(e, D + SRL_K_ATTN);
+    attn_plan(a, decode ? 1 : 0, st);
+  }
+  {
+    Prof p2(e, D + SRL_K_ELEMWISE);
+    rmsnorm(e->x_res, row_tok, row_pos, M, d, e->embed, e->lw[0].attn_norm, m.rms_eps, e->xn, st);
+  }
   e->launches += 2;
-  const long long capf = e->z.part_floats;
+  GemmEpi qe{};
+  qe.kind = EPI_QKV;
+  qe.row_pos = row_pos;
+  qe.row_slot = row_slot;
+  qe.page_table = e->ctl.page_table;
+  qe.max_pages = e->z.max_pages;
+  qe.rope_cos = e->rope_cos;
+  qe.rope_sin = e->rope_sin;
+  qe.q_out = e->qbuf;
+  qe.Hq = m.Hq;
+  qe.Hkv = m.Hkv;
+  qe.dh = m.dh;
+  qe.kv_f32 = e->kv_f32 ? 1 : 0;
+  GemmEpi re{};
+  re.kind = EPI_RESID;
+  re.x_res = e->x_res;
+  re.ldo = d;
+  GemmEpi se{};
+  se.kind = EPI_SILU;
+  se.act = e->act;
+  se.ldo = m.ff;
   for (int l = 0; l < m.L; ++l) {
     const LayerW& w = e->lw[l];
-    int sp = run_gemm(e, e->xn, M, w.wqkv, Nqkv, d, e->part, capf);
-    QkvEpiArgs q{};
-    q.P = e->part;
-    q.S = sp;
-    q.M = M;
-    q.bias = m.qkv_bias ? w.bqkv : nullptr;
-    q.row_pos = row_pos;
-    q.row_slot = row_slot;
-    q.page_table = e->ctl.page_table;
-    q.max_pages = e->z.max_pages;
-    q.rope_cos = e->rope_cos;
-    q.rope_sin = e->rope_sin;
-    q.q_out = e->qbuf;
-    q.k_pool = e->kpool[l];
-    q.v_pool = e->vpool[l];
-    q.Hq = m.Hq;
-    q.Hkv = m.Hkv;
-    q.dh = m.dh;
-    qkv_epilogue(q, e->kv_f32, st);
+    {
+      Prof p(e, D + SRL_K_GEMM_QKV);
+      qe.bias = m.qkv_bias ? w.bqkv : nullptr;
+      qe.k_pool = e->kpool[l];
+      qe.v_pool = e->vpool[l];
+      run_gemm(e, e->xn, M, w.wqkv, Nqkv, d, qe);
+    }
     a.k_pool = e->kpool[l];
     a.v_pool = e->vpool[l];
-    attn_run(a, e->kv_f32, &e->tmK[l], &e->tmV[l], st);
-    sp = run_gemm(e, e->attn_out, M, w.wo, d, qd, e->part, capf);
-    resid_norm(e->part, sp, M, d, row_pos, e->x_res, w.mlp_norm, m.rms_eps, e->xn, st);
-    sp = run_gemm(e, e->xn, M, w.wgu, 2 * m.ff, d, e->part, capf);
-    silu_mul(e->part, sp, M, m.ff, e->act, st);
-    sp = run_gemm(e, e->act, M, w.wd, d, m.ff, e->part, capf);
-    const __nv_bfloat16* next = l + 1 < m.L ? e->lw[l + 1].attn_norm : e->final_norm;
-    resid_norm(e->part, sp, M, d, row_pos, e->x_res, next, m.rms_eps, e->xn, st);
-    e->launches += 6;
+    {
+      Prof p(e, D + SRL_K_ATTN, 2);
+      attn_run(a, e->kv_f32, &e->tmK[l], &e->tmV[l], st);
+    }
+    {
+      Prof p(e, D + SRL_K_GEMM_O);
+      run_gemm(e, e->attn_out, M, w.wo, d, qd, re);
+    }
+    {
+      Prof p(e, D + SRL_K_ELEMWISE);
+      rmsnorm(e->x_res, row_tok, row_pos, M, d, nullptr, w.mlp_norm, m.rms_eps, e->xn, st);
+    }
+    {
+      Prof p(e, D + SRL_K_GEMM_GU);
+      run_gemm(e, e->xn, M, w.wgu, m.ff, d, se);
+    }
+    {
+      Prof p(e, D + SRL_K_GEMM_DOWN);
+      run_gemm(e, e->act, M, w.wd, d, m.ff, re);
+    }
+    {
+      Prof p(e, D + SRL_K_ELEMWISE);
+      const __nv_bfloat16* next = l + 1 < m.L ? e->lw[l + 1].attn_norm : e->final_norm;
+      rmsnorm(e->x_res, row_tok, row_pos, M, d, nullptr, next, m.rms_eps, e->xn, st);
+    }
+    e->launches += 4;
   }
   if (decode) {
-    int sp = gemm_choose_splits(M, m.V, d, e->num_sms);
-    while (sp > 1 && (long long)sp * M * m.V > capf) --sp;
-    if (sp == 1) {
-      gemm_bf16_partials(e->xn, M, e->lm_head, m.V, d, e->logits, 1, st);
-      e->launches++;
-    } else {
-      gemm_bf16_partials(e->xn, M, e->lm_head, m.V, d, e->part, sp, st);
-      reduce_splits(e->part, sp, (long long)M * m.V, e->logits, st);
-      e->launches += 2;
-    }
+    Prof p(e, SRL_K_LM_HEAD);
+    GemmEpi fe{};
+    fe.kind = EPI_F32;
+    fe.out_f32 = e->logits;
+    fe.ldo = m.V;
+    run_gemm(e, e->xn, M, e->lm_head, m.V, d, fe);
   }
+}
+
+// decode forward over the local slots, sampler, controller END (static shapes)
+void decode_tail(srl_engine* e) {
+  const Ctl& c = e->ctl;
+  cudaStream_t st = e->st;
+  forward(e, e->s.Q_g, c.row_tok, c.row_pos, e->row_slot_id, true);
+  SampleArgs sa{};
+  sa.logits = e->logits;
+  sa.M = e->s.Q_g;
+  sa.V = e->m.V;
+  sa.row_pos = c.row_pos;
+  sa.row_n = c.row_n;
+  sa.row_traj = c.row_traj;
+  sa.row_restarts = c.row_restarts;
+  sa.invT = 1.0f / e->s.temperature;
+  sa.seed = e->s.sample_seed;
+  sa.tok_out = c.samp_tok + (size_t)e->rank * e->s.Q_g;
+  sa.lp_out = c.samp_lp + (size_t)e->rank * e->s.Q_g;
+  {
+    Prof p(e, SRL_K_SAMPLE);
+    sample(sa, st);
+  }
+  e->launches++;
+  {
+    Prof p(e, SRL_K_CTL);
+    ctl_end(c, st);
+  }
+  e->launches++;
 }
 
 void read_status(srl_engine* e) {
@@ -400,6 +523,7 @@ int32_t srl_create(const srl_model_cfg* m, const srl_sched_cfg* s, int32_t devic
   e->st = (cudaStream_t)stream;
   e->kv_f32 = s->kv_dtype == SRL_KV_FP32;
   e->z = compute_sizes(m, s, world);
+  e->use_graph = getenv("SRL_NO_GRAPH") == nullptr && stream != nullptr;  // the legacy stream cannot be captured
   cudaDeviceGetAttribute(&e->num_sms, cudaDevAttrMultiProcessorCount, device);
   e->W = (uint8_t*)mem->weights;
   e->KV = (uint8_t*)mem->kv;
@@ -469,6 +593,7 @@ int32_t srl_create(const srl_model_cfg* m, const srl_sched_cfg* s, int32_t devic
   e->prompt_tok_cap = (long long)e->z.max_prompts * s->max_prompt;
   // init device state
   cudaMemsetAsync(e->KV, 0, mem->kv_bytes, e->st);  // finite values in never-written KV rows
+  cudaMemsetAsync(e->gcount, 0, 4ull * e->z.n_counters, e->st);
   std::vector<int> ident(s->Q_g);
   for (int i = 0; i < s->Q_g; ++i) ident[i] = i;
   cudaMemcpyAsync(e->row_slot_id, ident.data(), 4 * s->Q_g, cudaMemcpyHostToDevice, e->st);
@@ -495,6 +620,9 @@ int32_t srl_destroy(srl_engine* e) {
   if (e->hst) cudaFreeHost(e->hst);
   if (e->ev0) cudaEventDestroy(e->ev0);
   if (e->ev1) cudaEventDestroy(e->ev1);
+  for (cudaEvent_t ev : e->direct.ev) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : e->gset.ev) cudaEventDestroy(ev);
+  if (e->gexec) cudaGraphExecDestroy(e->gexec);
   delete e;
   return SRL_OK;
 }
@@ -565,16 +693,20 @@ int32_t srl_decode_step(srl_engine* e, srl_step_info* info) {
   if (!e->v_valid) return fail(SRL_E_STATE, "srl_decode_step: no policy weights loaded");
   cudaStream_t st = e->st;
   cudaEventRecord(e->ev0, st);
-  ctl_begin(e->ctl, st);
+  {
+    Prof p(e, SRL_K_CTL);
+    ctl_begin(e->ctl, st);
+  }
   e->launches++;
   read_status(e);
-  if (cudaGetLastError() != cudaSuccess) return cuda_fail("ctl_begin");
+  if (cudaError_t ce = cudaGetLastError()) return cuda_fail("ctl_begin", ce);
   CtlStatus b = *e->hst;
   if (info) {
     info->v = b.v;
     info->n_ready = b.n_ready;
   }
   if (b.status != ST_CONTINUE) {
+    prof_collect(e, e->direct, false);
     if (b.status == SRL_GROUP_READY) e->group_state = 1;
     if (b.status < 0) return fail(b.status, b.status == SRL_E_CAPACITY ? "srl_decode_step: KV pool / prefill capacity"
                                                                      : (b.status == SRL_E_EMPTY ? "srl_decode_step: nothing submitted"
@@ -585,29 +717,46 @@ int32_t srl_decode_step(srl_engine* e, srl_step_info* info) {
   // prefill of newly admitted sequences (prompt ++ kept tokens), in chunks
   for (int r0 = 0; r0 < b.m_pre; r0 += e->s.prefill_chunk) {
     const int mc = b.m_pre - r0 < e->s.prefill_chunk ? b.m_pre - r0 : e->s.prefill_chunk;
+    Prof p(e, SRL_K_PREFILL, 2 + 8 * e->m.L);
     forward(e, mc, c.pre_tok + r0, c.pre_pos + r0, c.pre_slot + r0, false);
   }
-  // decode of every local slot
-  forward(e, e->s.Q_g, c.row_tok, c.row_pos, e->row_slot_id, true);
-  SampleArgs sa{};
-  sa.logits = e->logits;
-  sa.M = e->s.Q_g;
-  sa.V = e->m.V;
-  sa.row_pos = c.row_pos;
-  sa.row_n = c.row_n;
-  sa.row_traj = c.row_traj;
-  sa.row_restarts = c.row_restarts;
-  sa.invT = 1.0f / e->s.temperature;
-  sa.seed = e->s.sample_seed;
-  sa.tok_out = c.samp_tok + (size_t)e->rank * e->s.Q_g;
-  sa.lp_out = c.samp_lp + (size_t)e->rank * e->s.Q_g;
-  sample(sa, st);
-  e->launches++;
-  ctl_end(c, st);
-  e->launches++;
+  // decode of every local slot + sampling + stop/compaction/emission: a static
+  // launch sequence, replayed from a CUDA graph after the first step.
+  if (e->use_graph && e->direct_steps >= 1 && !e->gexec) {
+    const long long l0 = e->launches;
+    cudaGraph_t g = nullptr;
+    e->capturing = true;
+    bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+      decode_tail(e);
+      ok = cudaStreamEndCapture(st, &g) == cudaSuccess && g;
+    }
+    e->capturing = false;
+    if (ok) ok = cudaGraphInstantiate(&e->gexec, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    e->g_launches = e->launches - l0;
+    e->launches = l0;
+    if (!ok) {  // fall back to direct launches for good
+      e->gexec = nullptr;
+      e->use_graph = false;
+      e->gset.cls.clear();
+      e->gset.nl.clear();
+      e->gset.used = 0;
+    }
+  }
+  if (e->gexec) {
+    cudaGraphLaunch(e->gexec, st);
+    e->launches += e->g_launches;
+  } else {
+    decode_tail(e);
+    e->direct_steps++;
+  }
   cudaEventRecord(e->ev1, st);
   read_status(e);
-  if (cudaGetLastError() != cudaSuccess) return cuda_fail("decode step");
+  if (cudaError_t ce = cudaGetLastError()) return cuda_fail("decode step", ce);
+  prof_collect(e, e->direct, false);
+  if (e->gexec) prof_collect(e, e->gset, true);
   const CtlStatus& en = *e->hst;
   if (info) {
     info->k = en.k - 1;
@@ -616,6 +765,7 @@ int32_t srl_decode_step(srl_engine* e, srl_step_info* info) {
     info->n_ready = en.n_ready;
     info->n_admitted = b.n_admit;
     info->n_prefill_tokens = b.m_pre;
+    info->sum_ctx = b.sum_ctx;
     info->v = en.v;
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e->ev0, e->ev1);
@@ -664,7 +814,7 @@ int32_t srl_load_policy_weights(srl_engine* e, const void* flat_w, int64_t versi
   ctl_bump(e->ctl, (int)version, e->st);
   e->launches++;
   read_status(e);
-  if (cudaGetLastError() != cudaSuccess) return cuda_fail("srl_load_policy_weights");
+  if (cudaError_t ce = cudaGetLastError()) return cuda_fail("srl_load_policy_weights", ce);
   if (e->hst->status < 0) return fail(e->hst->status, "srl_load_policy_weights: capacity (resumed list)");
   e->v = version;
   e->v_valid = true;
@@ -707,6 +857,28 @@ int32_t srl_get_counters(srl_engine* e, int64_t* raw, int64_t* disc, int64_t* em
   if (emitted) *emitted = st.emitted;
   if (groups) *groups = st.n_groups;
   if (launches) *launches = e->launches;
+  return SRL_OK;
+}
+
+int32_t srl_set_profiling(srl_engine* e, int32_t on) {
+  if (!e) return fail(SRL_E_INVALID_ARG, "srl_set_profiling: null engine");
+  e->prof = on != 0;
+  for (int i = 0; i < SRL_K_NCLASS; ++i) {
+    e->prof_ms[i] = 0;
+    e->prof_launch[i] = 0;
+  }
+  e->direct.cls.clear();
+  e->direct.nl.clear();
+  e->direct.used = 0;
+  return SRL_OK;
+}
+
+int32_t srl_get_profile(srl_engine* e, double* ms, int64_t* launches) {
+  if (!e) return fail(SRL_E_INVALID_ARG, "srl_get_profile: null engine");
+  for (int i = 0; i < SRL_K_NCLASS; ++i) {
+    if (ms) ms[i] = e->prof_ms[i];
+    if (launches) launches[i] = e->prof_launch[i];
+  }
   return SRL_OK;
 }
 

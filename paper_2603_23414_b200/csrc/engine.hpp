@@ -42,6 +42,7 @@ struct CtlStatus {
   int v;
   int group_n, group_final, group_state;
   long long n_events, raw_tokens, discarded_tokens, emitted, n_groups;
+  long long sum_ctx;  // sum of (pos + 1) over this rank's running rows (BEGIN)
   int pad[4];
 };
 

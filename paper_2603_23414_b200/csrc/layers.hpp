@@ -7,29 +7,10 @@
 namespace srl {
 
 void rope_table(float* cos_t, float* sin_t, int max_pos, int dh, double theta, cudaStream_t st);
-void embed_norm(const int* row_tok, const int* row_pos, int M, int d, const __nv_bfloat16* embed,
-                const __nv_bfloat16* w, float eps, float* x_res, __nv_bfloat16* xn, cudaStream_t st);
-void resid_norm(const float* P, int S, int M, int d, const int* row_pos, float* x_res, const __nv_bfloat16* w,
-                float eps, __nv_bfloat16* xn, cudaStream_t st);
-void silu_mul(const float* P, int S, int M, int ff, __nv_bfloat16* act, cudaStream_t st);
-void reduce_splits(const float* P, int S, long long n, float* out, cudaStream_t st);
-
-struct QkvEpiArgs {
-  const float* P;  // [S][M][(Hq+2Hkv)*dh]
-  int S, M;
-  const __nv_bfloat16* bias;  // nullable
-  const int* row_pos;         // [M] (-1 inactive)
-  const int* row_slot;        // [M] local slot -> page-table row
-  const int* page_table;
-  int max_pages;
-  const float* rope_cos;
-  const float* rope_sin;
-  void* q_out;    // [M][Hq][dh] bf16 (bf16 KV) or fp32 (fp32 KV)
-  void* k_pool;   // this layer's K pool [pages][Hkv][64][dh]
-  void* v_pool;
-  int Hq, Hkv, dh;
-};
-void qkv_epilogue(const QkvEpiArgs& a, bool kv_fp32, cudaStream_t st);
+// RMSNorm of the fp32 residual rows into the bf16 GEMM operand; with `embed`
+// non-null the residual row is first set to the embedding of row_tok[m].
+void rmsnorm(float* x_res, const int* row_tok, const int* row_pos, int M, int d, const __nv_bfloat16* embed,
+             const __nv_bfloat16* w, float eps, __nv_bfloat16* y, cudaStream_t st);
 
 // ---- attention.cu
 // Work item = (row, kv head, chunk of kChunkPages pages).  The plan kernel

@@ -18,17 +18,51 @@ using namespace srl;
 
 extern "C" const char* srl_last_error(void) { return g_last_error.c_str(); }
 
-extern "C" int32_t srl_op_gemm_bf16(const void* X, int32_t M, const void* W, int32_t N, int32_t K, float* out,
-                                    int32_t splits, void* stream) {
-  int r = gemm_bf16_partials(reinterpret_cast<const __nv_bfloat16*>(X), M,
-                             reinterpret_cast<const __nv_bfloat16*>(W), N, K, out, splits,
-                             reinterpret_cast<cudaStream_t>(stream));
-  if (r) set_error("srl_op_gemm_bf16: %s (code %ld)", r == -1 ? "bad shape/splits" : "launch/tma failure", r);
-  return r;
+static int op_sms() {
+  int dev = 0, n = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
 }
 
-extern "C" int32_t srl_op_gemm_splits(int32_t M, int32_t N, int32_t K, int32_t num_sms) {
-  return gemm_choose_splits(M, N, K, num_sms);
+namespace srl {
+void gemm_set_debug(unsigned long long* buf, int target);
+}
+// Profiling hook (not part of the public headers): per-CTA phase timestamps of
+// the `target`-th GEMM launch after the call.
+extern "C" void srl_debug_gemm_timestamps(unsigned long long* dev_buf, int32_t target) {
+  srl::gemm_set_debug(dev_buf, target);
+}
+
+extern "C" int64_t srl_op_gemm_workspace(int32_t M, int32_t N, int32_t K, int32_t epi) {
+  if (M <= 0 || N <= 0 || K <= 0 || epi < 0 || epi > 2) return -1;
+  const int nt = epi == 2 ? 2 : 1;
+  const size_t ws = (gemm_workspace_bytes(M, nt, 148 > op_sms() ? 148 : op_sms()) + 255) / 256 * 256;
+  return (int64_t)(ws + 4 * gemm_counter_count(M, N));
+}
+
+extern "C" int32_t srl_op_gemm_bf16(const void* X, int32_t M, const void* W, int32_t N, int32_t K, int32_t epi,
+                                    void* out, void* workspace, void* stream) {
+  if (M <= 0 || N <= 0 || K <= 0 || K % 64 || epi < 0 || epi > 2 || (epi == 2 && N % 128)) {
+    set_error("srl_op_gemm_bf16: %s", "bad shape / epilogue", 0);
+    return -1;
+  }
+  const int nt = epi == 2 ? 2 : 1;
+  const int sms = op_sms();
+  const size_t wsb = (gemm_workspace_bytes(M, nt, 148 > sms ? 148 : sms) + 255) / 256 * 256;
+  int* counters = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(workspace) + wsb);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaMemsetAsync(counters, 0, 4 * gemm_counter_count(M, N), st);
+  GemmEpi e{};
+  e.kind = epi == 0 ? EPI_F32 : (epi == 1 ? EPI_RESID : EPI_SILU);
+  e.ldo = N;
+  e.out_f32 = reinterpret_cast<float*>(out);
+  e.x_res = reinterpret_cast<float*>(out);
+  e.act = reinterpret_cast<__nv_bfloat16*>(out);
+  int r = gemm_bf16_fused(reinterpret_cast<const __nv_bfloat16*>(X), M, reinterpret_cast<const __nv_bfloat16*>(W), N,
+                          K, e, reinterpret_cast<float*>(workspace), counters, sms, st);
+  if (r) set_error("srl_op_gemm_bf16: %s (code %ld)", r == -1 ? "bad shape" : "launch/tma failure", r);
+  return r;
 }
 
 // ---------------------------------------------------------------- attention op

@@ -55,7 +55,9 @@ class RolloutEngine:
         self.W = torch.empty(wb.value, dtype=torch.uint8, device=self.dev)
         self.KV = torch.empty(kb.value, dtype=torch.uint8, device=self.dev)
         self.S = torch.empty(sb.value, dtype=torch.uint8, device=self.dev)
-        self.stream = stream if stream is not None else torch.cuda.current_stream(self.dev)
+        # a dedicated stream: the decode tail is captured into a CUDA graph, which the
+        # legacy default stream does not allow
+        self.stream = stream if stream is not None else torch.cuda.Stream(self.dev)
         arena = Arena(self.W.data_ptr(), self.KV.data_ptr(), self.S.data_ptr(), wb.value, kb.value, sb.value)
         comm = None
         if world > 1:
@@ -76,7 +78,12 @@ class RolloutEngine:
         t = self.W[off:off + 2 * n.value].view(self.torch.bfloat16)
         return t
 
+    def _sync_in(self):
+        """Order the engine stream after work torch queued on the current stream."""
+        self.stream.wait_stream(self.torch.cuda.current_stream(self.dev))
+
     def load_policy_weights(self, version: int, flat=None):
+        self._sync_in()
         ptr = C.c_void_p(flat.data_ptr()) if flat is not None else None
         return check(self.lib.srl_load_policy_weights(self.h, ptr, int(version)), "srl_load_policy_weights")
 
@@ -86,10 +93,12 @@ class RolloutEngine:
         off = np.ascontiguousarray(tok_off, dtype=np.int32)
         tk = np.ascontiguousarray(toks, dtype=np.int32)
         fl = None if forced_len is None else np.ascontiguousarray(forced_len, dtype=np.int32)
+        self._sync_in()
         return check(self.lib.srl_submit_prompts(self.h, len(ids), _i32p(ids), _i32p(off), _i32p(tk),
                                                  _i32p(fl) if fl is not None else None), "srl_submit_prompts")
 
     def decode_step(self):
+        self._sync_in()
         info = StepInfo()
         rc = check(self.lib.srl_decode_step(self.h, C.byref(info)), "srl_decode_step")
         return rc, info
@@ -125,6 +134,16 @@ class RolloutEngine:
         v = [C.c_int64() for _ in range(5)]
         check(self.lib.srl_get_counters(self.h, *[C.byref(x) for x in v]), "srl_get_counters")
         return dict(zip(["raw_tokens", "discarded_tokens", "emitted", "groups", "kernel_launches"], [x.value for x in v]))
+
+    def set_profiling(self, on: bool):
+        return check(self.lib.srl_set_profiling(self.h, 1 if on else 0), "srl_set_profiling")
+
+    def profile(self):
+        """{class: (device ms, launches)} accumulated since set_profiling(True)."""
+        ms = (C.c_double * 10)()
+        nl = (C.c_int64 * 10)()
+        check(self.lib.srl_get_profile(self.h, ms, nl), "srl_get_profile")
+        return {k: (ms[i], nl[i]) for i, k in enumerate(_lib.KERNEL_CLASSES)}
 
     def debug_logits(self) -> np.ndarray:
         out = np.empty((self.Q_g, self.V), dtype=np.float32)

@@ -8,20 +8,13 @@ import numpy as np
 from workload.configs import SchedConfig
 from workload.lengths import LengthModel, sample_lengths
 from workload.prompts import make_prompts
-from workload.weights import gen_weight_torch, weight_names, weight_shape
+from workload.weights import fill_engine_weights
 
 
 def fill_weights(eng, model, version, seed=2, flat=None):
     """Write version-`version` weights (workload recipe) into the engine's weight
     region, or into `flat` (a uint8 tensor with the same layout) if given."""
-    import torch
-    for name in weight_names(model):
-        view = eng.weight_view(name)
-        if flat is not None:
-            off = view.data_ptr() - eng.W.data_ptr()
-            view = flat[off:off + view.numel() * 2].view(torch.bfloat16)
-        gen_weight_torch(model, name, seed=seed, version=version, device=view.device,
-                         out=view.view(*weight_shape(model, name)))
+    fill_engine_weights(eng, model, version, seed=seed, flat=flat)
 
 
 def tiny_workload(n_prompts=16, G=1, seed_len=0, seed_prompt=1, V=512, cap=64, lm=None, plen=(4, 16)):

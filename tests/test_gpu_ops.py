@@ -22,27 +22,70 @@ def _stream():
 
 
 # ------------------------------------------------------------------ GEMM (tcgen05)
-@pytest.mark.parametrize("M,N,K", [(1, 128, 64), (16, 256, 128), (200, 384, 256), (256, 6144, 4096),
-                                   (64, 4096, 14336), (600, 512, 128), (37, 1000, 192), (256, 7168, 5120)])
+GEMM_SHAPES = [(1, 128, 64), (16, 256, 128), (200, 384, 256), (256, 6144, 4096), (64, 4096, 14336),
+               (600, 512, 128), (37, 1000, 192), (256, 7168, 5120), (256, 128256, 4096), (4096, 4096, 4096),
+               (300, 1024, 14336)]
+
+
+def _gemm(lib, X, W, N, epi, out):
+    M, K = X.shape
+    ws = torch.empty(lib.srl_op_gemm_workspace(M, N, K, epi), dtype=torch.uint8, device="cuda")
+    rc = lib.srl_op_gemm_bf16(X.data_ptr(), M, W.data_ptr(), N, K, epi, out.data_ptr(), ws.data_ptr(), _stream())
+    torch.cuda.synchronize()
+    return rc
+
+
+def _bound(X, W):
+    # fp32 accumulation of K products: |err| <= K * 2^-24 * sum|x||w| (loose)
+    return (X.double().abs() @ W.double().abs().t()) * (X.shape[1] * 2.0 ** -24) + 1e-12
+
+
+@pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
 def test_gemm_matches_fp64_reference(lib, M, N, K):
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
     X = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
     W = (torch.randn(N, K, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
-    sp = lib.srl_op_gemm_splits(M, N, K, 148)
-    out = torch.full((sp, M, N), float("nan"), device="cuda")
-    assert lib.srl_op_gemm_bf16(X.data_ptr(), M, W.data_ptr(), N, K, out.data_ptr(), sp, _stream()) == 0
-    torch.cuda.synchronize()
+    out = torch.full((M, N), float("nan"), device="cuda")
+    assert _gemm(lib, X, W, N, 0, out) == 0
     ref = X.double() @ W.double().t()
-    got = out.sum(0).double()
-    # fp32 accumulation of K products: |err| <= K * 2^-24 * sum|x||w| (loose), checked per element
-    bound = (X.double().abs() @ W.double().abs().t()) * (K * 2.0 ** -24) + 1e-12
-    assert ((got - ref).abs() <= bound).all()
+    got = out.double()
+    assert ((got - ref).abs() <= _bound(X, W)).all()
     assert ((got - ref).norm() / ref.norm()).item() < 1e-5
+    # bit-reproducible run to run (fixed-order stream-K fixup)
+    out2 = torch.empty_like(out)
+    _gemm(lib, X, W, N, 0, out2)
+    assert torch.equal(out, out2)
+
+
+@pytest.mark.parametrize("M,N,K", [(16, 256, 128), (256, 4096, 4096), (77, 640, 14336)])
+def test_gemm_residual_epilogue(lib, M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(3)
+    X = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    base = torch.randn(M, N, device="cuda", generator=g)
+    out = base.clone()
+    assert _gemm(lib, X, W, N, 1, out) == 0
+    ref = base.double() + X.double() @ W.double().t()
+    assert ((out.double() - ref).abs() <= _bound(X, W) + 1e-6 * ref.abs()).all()
+
+
+@pytest.mark.parametrize("M,N,K", [(16, 384, 128), (256, 14336, 4096), (200, 1024, 512)])
+def test_gemm_silu_mul_epilogue(lib, M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(4)
+    X = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    W = (torch.randn(2 * N, K, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    assert _gemm(lib, X, W, N, 2, out) == 0
+    y = X.double() @ W.double().t()
+    gte, up = y[:, :N], y[:, N:]
+    ref = gte / (1 + torch.exp(-gte)) * up
+    # bf16 output rounding (2^-9 relative) dominates the fp32 accumulation error
+    assert ((out.double() - ref).abs() <= 2.0 ** -8 * ref.abs() + 1e-4).all()
 
 
 def test_gemm_rejects_bad_shapes(lib):
-    assert lib.srl_op_gemm_bf16(0, 16, 0, 128, 100, 0, 1, _stream()) < 0      # K % 64
-    assert lib.srl_op_gemm_bf16(0, 16, 0, 128, 128, 0, 3, _stream()) < 0      # splits > K/64
+    assert lib.srl_op_gemm_bf16(0, 16, 0, 128, 100, 0, 0, 0, _stream()) < 0      # K % 64
+    assert lib.srl_op_gemm_bf16(0, 16, 0, 100, 128, 2, 0, 0, _stream()) < 0      # silu needs N % 128
 
 
 # ------------------------------------------------------------------ paged attention

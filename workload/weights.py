@@ -119,6 +119,20 @@ def gen_weight_np(m: ModelShape, name: str, seed: int = 2, version: int = 0, row
     return _f32_to_bf16_bits_np(v).reshape(out_shape)
 
 
+def fill_engine_weights(eng, m: ModelShape, version: int = 0, seed: int = 2, flat=None):
+    """Write the version-`version` policy into an engine's flat weight region
+    (`eng.weight_view(name)` gives each tensor), or into `flat`, a uint8 tensor
+    with the same layout."""
+    import torch
+    for name in weight_names(m):
+        view = eng.weight_view(name)
+        if flat is not None:
+            off = view.data_ptr() - eng.W.data_ptr()
+            view = flat[off:off + view.numel() * 2].view(torch.bfloat16)
+        gen_weight_torch(m, name, seed=seed, version=version, device=view.device,
+                         out=view.view(*weight_shape(m, name)))
+
+
 # ------------------------------------------------------------------ torch (same bits, on device)
 def _lowbias32_t(h):
     h = h ^ (h >> 16)
