@@ -145,12 +145,23 @@ typedef struct srl_engine srl_engine;
 int32_t srl_arena_sizes(const srl_model_cfg* m, const srl_sched_cfg* s, int32_t world, uint64_t* weights_bytes,
                         uint64_t* kv_bytes, uint64_t* scratch_bytes);
 
-/* Byte offset and element count of a named weight tensor inside the flat
- * weight region ("embed", "lm_head", "final_norm", "L<i>.wq", "L<i>.wk",
+/* Byte offset (of row 0) and element count of a named weight tensor inside the
+ * flat weight region ("embed", "lm_head", "final_norm", "L<i>.wq", "L<i>.wk",
  * "L<i>.wv", "L<i>.bq", "L<i>.bk", "L<i>.bv", "L<i>.wo", "L<i>.attn_norm",
- * "L<i>.mlp_norm", "L<i>.wg", "L<i>.wu", "L<i>.wd"), all bf16 row-major in the
- * shapes of a linear layer's weight [out, in].  Returns -1 if unknown. */
+ * "L<i>.mlp_norm", "L<i>.wg", "L<i>.wu", "L<i>.wd"), bf16, in the shape of a
+ * linear layer's weight [out, in].  Returns -1 if unknown.  All tensors are
+ * dense row-major EXCEPT wg / wu, whose rows are interleaved in 64-row blocks
+ * (see srl_weight_layout). */
 int64_t srl_weight_offset(const srl_model_cfg* m, const char* name, int64_t* numel);
+
+/* Full placement of a named tensor: row i (of `rows`, each `cols` bf16 elements)
+ * starts at byte offset + ((i / row_block) * block_stride + i % row_block) * cols * 2.
+ * Dense tensors have row_block = block_stride = rows.  L<i>.wg / L<i>.wu have
+ * row_block = 64, block_stride = 128: each 128-row block of the gate/up region
+ * holds 64 gate rows followed by the 64 up rows of the same outputs, so one
+ * 128-row tensor-core tile carries both operands of the fused SiLU-mul. */
+int32_t srl_weight_layout(const srl_model_cfg* m, const char* name, int64_t* offset, int64_t* rows, int64_t* cols,
+                          int64_t* row_block, int64_t* block_stride);
 
 int32_t srl_create(const srl_model_cfg* m, const srl_sched_cfg* s, int32_t device, void* stream,
                    const srl_arena* mem, const srl_comm* comm /* NULL => R = 1 */, srl_engine** out);

@@ -26,9 +26,11 @@ extern "C" {
  *   persistent stream-K with a fixed-order fixup: bit-reproducible), and
  *   epi = 0: out fp32 [M, N]  = Y
  *   epi = 1: out fp32 [M, N] += Y                       (residual add)
- *   epi = 2: W has 2N rows (gate [0,N), up [N,2N)); out bf16 [M, N] = silu(Yg) * Yu
+ *   epi = 2: W has 2N rows, gate and up rows interleaved in 64-row blocks (rows
+ *            [128b, 128b+64) = gate rows [64b, 64b+64), rows [128b+64, 128b+128) =
+ *            the matching up rows); out bf16 [M, N] = silu(Yg) * Yu
  * workspace: device bytes >= srl_op_gemm_workspace(M, N, K, epi).
- * Requires K % 64 == 0 and, for epi 2, N % 128 == 0. */
+ * Requires K % 64 == 0 and, for epi 2, N % 64 == 0. */
 int64_t srl_op_gemm_workspace(int32_t M, int32_t N, int32_t K, int32_t epi);
 int32_t srl_op_gemm_bf16(const void* X, int32_t M, const void* W, int32_t N, int32_t K, int32_t epi, void* out,
                          void* workspace, void* stream);

@@ -70,6 +70,7 @@ SIGNATURES = {
     "srl_op_sample": (_I32, [_P, _I32, _I32, _P, _P, _P, C.c_float, _U64, _P, _P, _P, _P]),
     "srl_arena_sizes": (_I32, [_MP, _SP, _I32, _U64P, _U64P, _U64P]),
     "srl_weight_offset": (_I64, [_MP, C.c_char_p, _I64P]),
+    "srl_weight_layout": (_I32, [_MP, C.c_char_p, _I64P, _I64P, _I64P, _I64P, _I64P]),
     "srl_create": (_I32, [_MP, _SP, _I32, _P, _AP, _CP, C.POINTER(_P)]),
     "srl_destroy": (_I32, [_P]),
     "srl_submit_prompts": (_I32, [_P, _I32, _P, _P, _P, _P]),

@@ -23,11 +23,23 @@ namespace srl {
 constexpr float kLog2e = 1.4426950408889634f;
 
 // ---------------------------------------------------------------- plan
+// Split-KV only when the (row, kv head) pairs alone cannot fill the GPU (the
+// drain phase of a rollout: few long sequences); otherwise one item per pair
+// and the attention kernel writes the normalised output itself.
+constexpr int kMinItems = 4 * 148;
 __global__ void attn_plan_kernel(AttnArgs a, int split) {
   __shared__ int wsum[32];
-  __shared__ int base_s;
-  if (threadIdx.x == 0) base_s = 0;
+  __shared__ int base_s, active_s;
+  if (threadIdx.x == 0) {
+    base_s = 0;
+    active_s = 0;
+  }
   __syncthreads();
+  int my_active = 0;
+  for (int m = threadIdx.x; m < a.M; m += blockDim.x) my_active += a.row_pos[m] >= 0;
+  atomicAdd(&active_s, my_active);
+  __syncthreads();
+  if (active_s * a.Hkv >= kMinItems) split = 0;
   const int chunk_tok = 64 * kChunkPages;
   for (int b0 = 0; b0 < a.M; b0 += blockDim.x) {
     const int m = b0 + threadIdx.x;
@@ -91,6 +103,7 @@ __global__ void attn_combine_kernel(AttnArgs a, float* out_f32) {
   const int m = gw / a.Hq, h = gw % a.Hq;
   const int kvh = h / G, g = h % G;
   const int nch = a.row_nchunk[m];
+  if (nch == 1) return;  // written by the attention kernel
   if (nch == 0) {
     for (int d = lane; d < a.dh; d += 32) {
       if (F32OUT) out_f32[((size_t)m * a.Hq + h) * a.dh + d] = 0.f;
@@ -190,14 +203,26 @@ __global__ void __launch_bounds__(kF32Threads) attn_f32_kernel(AttnArgs a) {
         acc[k] = o;
       }
     }
-    for (int k = 0; k < 8; ++k) {
-      const int i = threadIdx.x + k * blockDim.x;
-      if (i >= G * a.dh) break;
-      a.part_o[(size_t)it * G * a.dh + i] = acc[k];
-    }
-    if (threadIdx.x < G) {
-      a.part_ml[((size_t)it * G + threadIdx.x) * 2 + 0] = run_m[threadIdx.x];
-      a.part_ml[((size_t)it * G + threadIdx.x) * 2 + 1] = run_l[threadIdx.x];
+    if (nch == 1) {  // the whole context in one item: final normalised output
+      for (int k = 0; k < 8; ++k) {
+        const int i = threadIdx.x + k * blockDim.x;
+        if (i >= G * a.dh) break;
+        const int g = i / a.dh;
+        const float o = acc[k] / run_l[g];
+        const size_t oi = ((size_t)m * a.Hq + kvh * G) * a.dh + i;
+        a.out[oi] = __float2bfloat16(o);
+        if (a.out_f32) a.out_f32[oi] = o;
+      }
+    } else {
+      for (int k = 0; k < 8; ++k) {
+        const int i = threadIdx.x + k * blockDim.x;
+        if (i >= G * a.dh) break;
+        a.part_o[(size_t)it * G * a.dh + i] = acc[k];
+      }
+      if (threadIdx.x < G) {
+        a.part_ml[((size_t)it * G + threadIdx.x) * 2 + 0] = run_m[threadIdx.x];
+        a.part_ml[((size_t)it * G + threadIdx.x) * 2 + 1] = run_l[threadIdx.x];
+      }
     }
   }
 }
@@ -404,6 +429,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       my[(c0 + 1) * (DH + 2) + d + 8] = o[mt][3];
     }
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32));
+    const bool single = a.row_nchunk[ii.m] == 1;
     for (int i = threadIdx.x; i < G * DH; i += kConsumerWarps * 32) {
       const int g = i / DH, d = i % DH;
       float mx = -INFINITY;
@@ -415,10 +441,17 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         acc += e[d] * f;
         l += e[DH + 1] * f;
       }
-      a.part_o[((size_t)it * G + g) * DH + d] = acc;
-      if (d == 0) {
-        a.part_ml[((size_t)it * G + g) * 2 + 0] = mx;
-        a.part_ml[((size_t)it * G + g) * 2 + 1] = l;
+      if (single) {  // the whole context in one item: final normalised output
+        const float o = acc / l;
+        const size_t oi = ((size_t)ii.m * a.Hq + ii.kvh * G + g) * DH + d;
+        a.out[oi] = __float2bfloat16(o);
+        if (a.out_f32) a.out_f32[oi] = o;
+      } else {
+        a.part_o[((size_t)it * G + g) * DH + d] = acc;
+        if (d == 0) {
+          a.part_ml[((size_t)it * G + g) * 2 + 0] = mx;
+          a.part_ml[((size_t)it * G + g) * 2 + 1] = l;
+        }
       }
     }
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32));

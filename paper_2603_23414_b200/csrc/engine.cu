@@ -32,24 +32,33 @@ struct LayerW {
 
 // ------------------------------------------------------------------ weight layout
 struct WeightLayout {
+  // row i of a tensor lives at byte off + ((i / row_block) * block_stride + i % row_block) * cols * 2
   struct Ent {
     std::string name;
     size_t off, numel;
+    size_t rows, cols, row_block, block_stride;
   };
   std::vector<Ent> ents;
   size_t total = 0;
-  void add(const std::string& n, size_t numel) {
-    ents.push_back({n, total, numel});
-    total += al(numel * 2);
+  void add(const std::string& n, size_t rows, size_t cols) {
+    ents.push_back({n, total, rows * cols, rows, cols, rows, rows});
+    total += al(rows * cols * 2);
   }
-  // q/k/v (and their biases, and gate/up) must be contiguous: add them unaligned in one run
-  void add_run(const std::vector<std::pair<std::string, size_t>>& run) {
+  // q/k/v (and their biases) must be contiguous: add them unaligned in one run
+  void add_run(const std::vector<std::pair<std::string, size_t>>& run, size_t cols) {
     size_t off = total;
     for (auto& e : run) {
-      ents.push_back({e.first, off, e.second});
-      off += e.second * 2;
+      ents.push_back({e.first, off, e.second * cols, e.second, cols, e.second, e.second});
+      off += e.second * cols * 2;
     }
     total = al(off);
+  }
+  // gate / up rows interleaved in 64-row blocks: one 128-row GEMM tile holds the
+  // gate and up rows of the same 64 outputs (fused SiLU-mul epilogue)
+  void add_gate_up(const std::string& g, const std::string& u, size_t ff, size_t cols) {
+    ents.push_back({g, total, ff * cols, ff, cols, 64, 128});
+    ents.push_back({u, total + 64 * cols * 2, ff * cols, ff, cols, 64, 128});
+    total += al(2 * ff * cols * 2);
   }
   const Ent* find(const std::string& n) const {
     for (auto& e : ents)
@@ -61,19 +70,19 @@ struct WeightLayout {
 WeightLayout make_layout(const srl_model_cfg& m) {
   WeightLayout w;
   const size_t d = m.d, qd = (size_t)m.Hq * m.dh, kd = (size_t)m.Hkv * m.dh, ff = m.ff;
-  w.add("embed", (size_t)m.V * d);
+  w.add("embed", m.V, d);
   for (int l = 0; l < m.L; ++l) {
     const std::string p = "L" + std::to_string(l) + ".";
-    w.add(p + "attn_norm", d);
-    w.add_run({{p + "wq", qd * d}, {p + "wk", kd * d}, {p + "wv", kd * d}});
-    if (m.qkv_bias) w.add_run({{p + "bq", qd}, {p + "bk", kd}, {p + "bv", kd}});
-    w.add(p + "wo", d * qd);
-    w.add(p + "mlp_norm", d);
-    w.add_run({{p + "wg", ff * d}, {p + "wu", ff * d}});
-    w.add(p + "wd", d * ff);
+    w.add(p + "attn_norm", d, 1);
+    w.add_run({{p + "wq", qd}, {p + "wk", kd}, {p + "wv", kd}}, d);
+    if (m.qkv_bias) w.add_run({{p + "bq", qd}, {p + "bk", kd}, {p + "bv", kd}}, 1);
+    w.add(p + "wo", d, qd);
+    w.add(p + "mlp_norm", d, 1);
+    w.add_gate_up(p + "wg", p + "wu", ff, d);
+    w.add(p + "wd", d, ff);
   }
-  w.add("final_norm", d);
-  w.add("lm_head", (size_t)m.V * d);
+  w.add("final_norm", d, 1);
+  w.add("lm_head", m.V, d);
   return w;
 }
 
@@ -101,6 +110,7 @@ int validate(const srl_model_cfg* m, const srl_sched_cfg* s, int world, std::str
   if (m->Hq / m->Hkv > 8) return why = "GQA group > 8 not supported", -1;
   if (m->dh != 32 && m->dh != 64 && m->dh != 128) return why = "dh must be 32, 64 or 128", -1;
   if (m->d % 128 || (m->Hq * m->dh) % 64 || m->ff % 128) return why = "d, ff must be multiples of 128 and Hq*dh of 64", -1;
+  if (m->d > 8192) return why = "d must be <= 8192", -1;
   if (s->Q_g <= 0 || s->U <= 0 || s->G <= 0 || s->cap <= 0 || s->pool_prompts <= 0 || s->kv_pages <= 0)
     return why = "Q_g, U, G, cap, pool_prompts, kv_pages must be positive", -1;
   if (s->page_tokens != kPage) return why = "page_tokens must be 64", -1;
@@ -414,7 +424,7 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
     }
     {
       Prof p(e, D + SRL_K_GEMM_GU);
-      run_gemm(e, e->xn, M, w.wgu, m.ff, d, se);
+      run_gemm(e, e->xn, M, w.wgu, 2 * m.ff, d, se);  // interleaved gate/up rows
     }
     {
       Prof p(e, D + SRL_K_GEMM_DOWN);
@@ -500,6 +510,20 @@ int64_t srl_weight_offset(const srl_model_cfg* m, const char* name, int64_t* num
   if (!e) return -1;
   if (numel) *numel = (int64_t)e->numel;
   return (int64_t)e->off;
+}
+
+int32_t srl_weight_layout(const srl_model_cfg* m, const char* name, int64_t* offset, int64_t* rows, int64_t* cols,
+                          int64_t* row_block, int64_t* block_stride) {
+  if (!m || !name) return fail(SRL_E_INVALID_ARG, "srl_weight_layout: null argument");
+  WeightLayout w = make_layout(*m);
+  const WeightLayout::Ent* e = w.find(name);
+  if (!e) return fail(SRL_E_INVALID_ARG, std::string("srl_weight_layout: unknown tensor ") + name);
+  if (offset) *offset = (int64_t)e->off;
+  if (rows) *rows = (int64_t)e->rows;
+  if (cols) *cols = (int64_t)e->cols;
+  if (row_block) *row_block = (int64_t)e->row_block;
+  if (block_stride) *block_stride = (int64_t)e->block_stride;
+  return SRL_OK;
 }
 
 int32_t srl_create(const srl_model_cfg* m, const srl_sched_cfg* s, int32_t device, void* stream, const srl_arena* mem,

@@ -98,15 +98,38 @@ __device__ __forceinline__ void apply_epilogue(const GemmParams& p, int unit_n0,
       break;
     }
     case EPI_SILU: {
-      if (ng < p.N)
+      if (NT == 2) {  // gate tile / up tile held by the same thread
+        if (ng < p.N)
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int m = m0 + j;
-          if (m < p.M) {
-            const float g = v[0][j], u = v[NT - 1][j];
-            e.act[(size_t)m * e.ldo + ng] = __float2bfloat16(g / (1.f + expf(-g)) * u);
+          for (int j = 0; j < 16; ++j) {
+            const int m = m0 + j;
+            if (m < p.M) {
+              const float g = v[0][j], u = v[NT - 1][j];
+              e.act[(size_t)m * e.ldo + ng] = __float2bfloat16(g / (1.f + expf(-g)) * u);
+            }
+          }
+      } else {
+        // 64-row interleave: tile rows [0,64) are gate rows, [64,128) the up rows of
+        // the same 64 outputs; meet through shared memory, split columns 8/8
+#pragma unroll
+        for (int j = 0; j < 16; ++j) xch[n * 17 + j] = v[0][j];
+        epi_bar();
+        const int o = n & 63;                      // output within the tile
+        const int out = (unit_n0 >> 1) + o;        // global output index
+        const int jb = n < 64 ? 0 : 8;
+        if (unit_n0 + o < p.N) {
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            const int j = jb + jj;
+            const int m = m0 + j;
+            if (m < p.M) {
+              const float g = xch[o * 17 + j], u = xch[(o + 64) * 17 + j];
+              e.act[(size_t)m * e.ldo + out] = __float2bfloat16(g / (1.f + expf(-g)) * u);
+            }
           }
         }
+        epi_bar();
+      }
       break;
     }
     case EPI_QKV: {
@@ -339,7 +362,8 @@ __global__ void __launch_bounds__(192, 1)
         }
       } else {
         // stream-K partial: publish; gemm_fixup_kernel reduces the unit in CTA order.
-        // Layout per (slot, chunk, tile): [128 rows][16 cols] -> 64 contiguous bytes per thread.
+        // Layout per (slot, chunk, tile): [4 col quads][128 rows][4 cols], so each warp
+        // store instruction writes 512 contiguous bytes.
         const int slot = (u == u_first) ? 0 : 1;
         float* my = p.ws + ((size_t)c * 2 + slot) * (size_t)NT * p.m_blk * 128;
         for (int cc = 0; cc < ncol; cc += 16) {
@@ -347,10 +371,10 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int j = 0; j < NT; ++j) {
             tmem_ld16(tl + (uint32_t)((a * NT + j) * p.m_blk + cc), v[j]);
-            float4* dst = reinterpret_cast<float4*>(my + (((size_t)(cc >> 4) * NT + j) * 128 + n) * 16);
+            float4* dst = reinterpret_cast<float4*>(my + ((size_t)(cc >> 4) * NT + j) * 2048) + n;
 #pragma unroll
             for (int q4 = 0; q4 < 4; ++q4)
-              __stcg(dst + q4, make_float4(v[j][4 * q4], v[j][4 * q4 + 1], v[j][4 * q4 + 2], v[j][4 * q4 + 3]));
+              __stcg(dst + q4 * 128, make_float4(v[j][4 * q4], v[j][4 * q4 + 1], v[j][4 * q4 + 2], v[j][4 * q4 + 3]));
           }
         }
       }
@@ -406,9 +430,9 @@ __global__ void __launch_bounds__(128) gemm_fixup_kernel(GemmParams p, int G) {
         const float* src = p.ws + ((size_t)cx * 2 + s2) * (size_t)NT * p.m_blk * 128;
 #pragma unroll
         for (int j = 0; j < NT; ++j) {
-          const float4* s4 = reinterpret_cast<const float4*>(src + (((size_t)ci * NT + j) * 128 + n) * 16);
+          const float4* s4 = reinterpret_cast<const float4*>(src + ((size_t)ci * NT + j) * 2048) + n;
 #pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) buf[b][j][q4] = __ldcg(s4 + q4);
+          for (int q4 = 0; q4 < 4; ++q4) buf[b][j][q4] = __ldcg(s4 + q4 * 128);
         }
       }
 #pragma unroll
@@ -465,9 +489,10 @@ int gemm_bf16_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N
   p.K = K;
   p.m_blk = pick_mblk(M);
   p.m_blocks = (M + p.m_blk - 1) / p.m_blk;
-  p.nt = epi.kind == EPI_SILU ? 2 : 1;
-  p.tile2_off = epi.kind == EPI_SILU ? N : 0;
-  if (p.nt == 2 && N % 128 != 0) return -1;
+  // EPI_SILU: W holds the interleaved gate/up rows (2 x outputs), N counts rows
+  p.nt = 1;
+  p.tile2_off = 0;
+  if (epi.kind == EPI_SILU && N % 128 != 0) return -1;
   p.n_tiles = (N + 127) / 128;
   p.kb = K / 64;
   p.total = (long long)p.n_tiles * p.m_blocks * p.kb;

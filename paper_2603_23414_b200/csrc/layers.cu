@@ -24,51 +24,73 @@ void rope_table(float* cos_t, float* sin_t, int max_pos, int dh, double theta, c
   rope_table_kernel<<<296, 256, 0, st>>>(cos_t, sin_t, max_pos, dh / 2, dh, theta);
 }
 
-// ---------------------------------------------------------------- RMSNorm: one warp per row
-// x fp32 [M][d] (d % 128 == 0), w bf16 [d] -> y bf16 [M][d]; when `embed` is set,
-// x is first overwritten with the fp32 embedding row of row_tok[m] (layer 0).
-__global__ void rmsnorm_kernel(float* __restrict__ x_res, const int* __restrict__ row_tok,
-                               const int* __restrict__ row_pos, int M, int d,
-                               const __nv_bfloat16* __restrict__ embed, const __nv_bfloat16* __restrict__ w,
-                               float eps, __nv_bfloat16* __restrict__ y) {
-  const int m = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (m >= M) return;
+// ---------------------------------------------------------------- RMSNorm: one CTA per row
+// x fp32 [M][d] (d % 4 == 0, d <= 4 * 256 * kNormVec), w bf16 [d] -> y bf16 [M][d];
+// when `embed` is set, x is first overwritten with the fp32 embedding row of
+// row_tok[m] (layer 0).  Every load of the row is issued before the reduction
+// (the kernel is latency-bound otherwise).
+constexpr int kNormThreads = 256;
+constexpr int kNormVec = 8;  // float4 per thread
+__global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(float* __restrict__ x_res, const int* __restrict__ row_tok,
+                                                                const int* __restrict__ row_pos, int M, int d,
+                                                                const __nv_bfloat16* __restrict__ embed,
+                                                                const __nv_bfloat16* __restrict__ w, float eps,
+                                                                __nv_bfloat16* __restrict__ y) {
+  __shared__ float red[kNormThreads / 32];
+  const int m = blockIdx.x;
   float* x = x_res + (size_t)m * d;
   __nv_bfloat16* out = y + (size_t)m * d;
   const bool active = row_pos[m] >= 0;
-  float ss = 0.f;
-  if (embed) {
-    const __nv_bfloat16* e = embed + (size_t)(active ? row_tok[m] : 0) * d;
-    for (int i = lane * 4; i < d; i += 128) {
-      const uint2 raw = *reinterpret_cast<const uint2*>(e + i);
-      float4 v = make_float4(bf16lo(raw.x), bf16hi(raw.x), bf16lo(raw.y), bf16hi(raw.y));
-      if (!active) v = make_float4(0.f, 0.f, 0.f, 0.f);
-      *reinterpret_cast<float4*>(x + i) = v;
-      ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  const int nv = d >> 2;
+  float4 v[kNormVec];
+  uint2 wr[kNormVec];
+  const __nv_bfloat16* e = embed ? embed + (size_t)(active ? row_tok[m] : 0) * d : nullptr;
+#pragma unroll
+  for (int k = 0; k < kNormVec; ++k) {
+    const int i = threadIdx.x + k * kNormThreads;
+    if (i < nv) {
+      if (e) {
+        const uint2 raw = __ldg(reinterpret_cast<const uint2*>(e) + i);
+        v[k] = make_float4(bf16lo(raw.x), bf16hi(raw.x), bf16lo(raw.y), bf16hi(raw.y));
+      } else {
+        v[k] = reinterpret_cast<const float4*>(x)[i];
+      }
+      wr[k] = __ldg(reinterpret_cast<const uint2*>(w) + i);
     }
-  } else {
-    for (int i = lane * 4; i < d; i += 128) {
-      const float4 v = *reinterpret_cast<const float4*>(x + i);
-      ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < kNormVec; ++k) {
+    const int i = threadIdx.x + k * kNormThreads;
+    if (i < nv) {
+      if (!active) v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (e) reinterpret_cast<float4*>(x)[i] = v[k];
+      ss += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
     }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  const float inv = active ? rsqrtf(ss / (float)d + eps) : 0.f;
-  for (int i = lane * 4; i < d; i += 128) {
-    const float4 v = *reinterpret_cast<const float4*>(x + i);
-    const uint2 wr = *reinterpret_cast<const uint2*>(w + i);
-    uint2 o;
-    o.x = pack_bf16(v.x * inv * bf16lo(wr.x), v.y * inv * bf16hi(wr.x));
-    o.y = pack_bf16(v.z * inv * bf16lo(wr.y), v.w * inv * bf16hi(wr.y));
-    *reinterpret_cast<uint2*>(out + i) = o;
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int i = 0; i < kNormThreads / 32; ++i) tot += red[i];
+  const float inv = active ? rsqrtf(tot / (float)d + eps) : 0.f;
+#pragma unroll
+  for (int k = 0; k < kNormVec; ++k) {
+    const int i = threadIdx.x + k * kNormThreads;
+    if (i < nv) {
+      uint2 o;
+      o.x = pack_bf16(v[k].x * inv * bf16lo(wr[k].x), v[k].y * inv * bf16hi(wr[k].x));
+      o.y = pack_bf16(v[k].z * inv * bf16lo(wr[k].y), v[k].w * inv * bf16hi(wr[k].y));
+      reinterpret_cast<uint2*>(out)[i] = o;
+    }
   }
 }
 
 void rmsnorm(float* x_res, const int* row_tok, const int* row_pos, int M, int d, const __nv_bfloat16* embed,
              const __nv_bfloat16* w, float eps, __nv_bfloat16* y, cudaStream_t st) {
-  if (M > 0) rmsnorm_kernel<<<(M + 3) / 4, 128, 0, st>>>(x_res, row_tok, row_pos, M, d, embed, w, eps, y);
+  if (M > 0) rmsnorm_kernel<<<M, kNormThreads, 0, st>>>(x_res, row_tok, row_pos, M, d, embed, w, eps, y);
 }
 
 }  // namespace srl

@@ -31,6 +31,7 @@ struct AttnArgs {
   float* part_o;         // [max_items][G][dh]
   float* part_ml;        // [max_items][G][2]
   __nv_bfloat16* out;    // [M][Hq*dh]
+  float* out_f32;        // optional fp32 copy of out (op-level tests)
   int max_items;
   float scale;
 };

@@ -36,31 +36,26 @@ extern "C" void srl_debug_gemm_timestamps(unsigned long long* dev_buf, int32_t t
 
 extern "C" int64_t srl_op_gemm_workspace(int32_t M, int32_t N, int32_t K, int32_t epi) {
   if (M <= 0 || N <= 0 || K <= 0 || epi < 0 || epi > 2) return -1;
-  const int nt = epi == 2 ? 2 : 1;
-  const size_t ws = (gemm_workspace_bytes(M, nt, 148 > op_sms() ? 148 : op_sms()) + 255) / 256 * 256;
-  return (int64_t)(ws + 4 * gemm_counter_count(M, N));
+  return (int64_t)((gemm_workspace_bytes(M, 1, 148 > op_sms() ? 148 : op_sms()) + 255) / 256 * 256);
 }
 
 extern "C" int32_t srl_op_gemm_bf16(const void* X, int32_t M, const void* W, int32_t N, int32_t K, int32_t epi,
                                     void* out, void* workspace, void* stream) {
-  if (M <= 0 || N <= 0 || K <= 0 || K % 64 || epi < 0 || epi > 2 || (epi == 2 && N % 128)) {
+  if (M <= 0 || N <= 0 || K <= 0 || K % 64 || epi < 0 || epi > 2 || (epi == 2 && N % 64)) {
     set_error("srl_op_gemm_bf16: %s", "bad shape / epilogue", 0);
     return -1;
   }
-  const int nt = epi == 2 ? 2 : 1;
   const int sms = op_sms();
-  const size_t wsb = (gemm_workspace_bytes(M, nt, 148 > sms ? 148 : sms) + 255) / 256 * 256;
-  int* counters = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(workspace) + wsb);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  cudaMemsetAsync(counters, 0, 4 * gemm_counter_count(M, N), st);
   GemmEpi e{};
   e.kind = epi == 0 ? EPI_F32 : (epi == 1 ? EPI_RESID : EPI_SILU);
   e.ldo = N;
   e.out_f32 = reinterpret_cast<float*>(out);
   e.x_res = reinterpret_cast<float*>(out);
   e.act = reinterpret_cast<__nv_bfloat16*>(out);
-  int r = gemm_bf16_fused(reinterpret_cast<const __nv_bfloat16*>(X), M, reinterpret_cast<const __nv_bfloat16*>(W), N,
-                          K, e, reinterpret_cast<float*>(workspace), counters, sms, st);
+  const int rows = epi == 2 ? 2 * N : N;  // SiLU-mul: interleaved gate/up rows
+  int r = gemm_bf16_fused(reinterpret_cast<const __nv_bfloat16*>(X), M, reinterpret_cast<const __nv_bfloat16*>(W),
+                          rows, K, e, reinterpret_cast<float*>(workspace), nullptr, sms, st);
   if (r) set_error("srl_op_gemm_bf16: %s (code %ld)", r == -1 ? "bad shape" : "launch/tma failure", r);
   return r;
 }
@@ -128,6 +123,7 @@ extern "C" int32_t srl_op_attention(const void* q, const void* k_pool, const voi
   a.part_o = reinterpret_cast<float*>(ws + offs[4]);
   a.part_ml = reinterpret_cast<float*>(ws + offs[5]);
   a.out = reinterpret_cast<__nv_bfloat16*>(ws + offs[6]);
+  a.out_f32 = out_f32;
   a.max_items = attn_max_items(M, Hkv, max_ctx);
   a.scale = 1.0f / sqrtf((float)dh);
   iota_kernel<<<(M + 255) / 256, 256, 0, st>>>(const_cast<int*>(a.row_slot), M);

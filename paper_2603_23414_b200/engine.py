@@ -71,12 +71,17 @@ class RolloutEngine:
 
     # ------------------------------------------------------------------ weights
     def weight_view(self, name: str):
-        n = C.c_int64()
-        off = self.lib.srl_weight_offset(C.byref(self.m), name.encode(), C.byref(n))
-        if off < 0:
+        """bf16 view of a named tensor in the flat weight region: [rows, cols] for dense
+        tensors, [rows/64, 64, cols] for the block-interleaved gate/up weights."""
+        off, rows, cols, rb, bs = (C.c_int64() for _ in range(5))
+        if self.lib.srl_weight_layout(C.byref(self.m), name.encode(), C.byref(off), C.byref(rows), C.byref(cols),
+                                      C.byref(rb), C.byref(bs)) != 0:
             raise KeyError(name)
-        t = self.W[off:off + 2 * n.value].view(self.torch.bfloat16)
-        return t
+        W16 = self.W.view(self.torch.bfloat16)
+        o, r, c, rb, bs = off.value // 2, rows.value, cols.value, rb.value, bs.value
+        if rb == r:
+            return W16[o:o + r * c].view(r, c) if c > 1 else W16[o:o + r]
+        return W16.as_strided((r // rb, rb, c), (bs * c, c, 1), o)
 
     def _sync_in(self):
         """Order the engine stream after work torch queued on the current stream."""

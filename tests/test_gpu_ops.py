@@ -73,11 +73,13 @@ def test_gemm_residual_epilogue(lib, M, N, K):
 def test_gemm_silu_mul_epilogue(lib, M, N, K):
     g = torch.Generator(device="cuda").manual_seed(4)
     X = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
-    W = (torch.randn(2 * N, K, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    Wg = (torch.randn(N, K, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    Wu = (torch.randn(N, K, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    # 64-row block interleave of gate / up rows (srl_ops.h)
+    W = torch.stack([Wg.view(N // 64, 64, K), Wu.view(N // 64, 64, K)], dim=1).reshape(2 * N, K).contiguous()
     out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     assert _gemm(lib, X, W, N, 2, out) == 0
-    y = X.double() @ W.double().t()
-    gte, up = y[:, :N], y[:, N:]
+    gte, up = X.double() @ Wg.double().t(), X.double() @ Wu.double().t()
     ref = gte / (1 + torch.exp(-gte)) * up
     # bf16 output rounding (2^-9 relative) dominates the fp32 accumulation error
     assert ((out.double() - ref).abs() <= 2.0 ** -8 * ref.abs() + 1e-4).all()
@@ -85,7 +87,7 @@ def test_gemm_silu_mul_epilogue(lib, M, N, K):
 
 def test_gemm_rejects_bad_shapes(lib):
     assert lib.srl_op_gemm_bf16(0, 16, 0, 128, 100, 0, 0, 0, _stream()) < 0      # K % 64
-    assert lib.srl_op_gemm_bf16(0, 16, 0, 100, 128, 2, 0, 0, _stream()) < 0      # silu needs N % 128
+    assert lib.srl_op_gemm_bf16(0, 16, 0, 100, 128, 2, 0, 0, _stream()) < 0      # silu needs N % 64
 
 
 # ------------------------------------------------------------------ paged attention

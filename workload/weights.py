@@ -126,11 +126,16 @@ def fill_engine_weights(eng, m: ModelShape, version: int = 0, seed: int = 2, fla
     import torch
     for name in weight_names(m):
         view = eng.weight_view(name)
-        if flat is not None:
-            off = view.data_ptr() - eng.W.data_ptr()
-            view = flat[off:off + view.numel() * 2].view(torch.bfloat16)
-        gen_weight_torch(m, name, seed=seed, version=version, device=view.device,
-                         out=view.view(*weight_shape(m, name)))
+        if flat is not None:   # same layout inside `flat`
+            base = flat.view(torch.bfloat16)
+            view = base.as_strided(view.shape, view.stride(), view.storage_offset())
+        if view.is_contiguous():
+            gen_weight_torch(m, name, seed=seed, version=version, device=view.device,
+                             out=view.view(*weight_shape(m, name)))
+        else:                  # block-interleaved gate/up rows
+            tmp = gen_weight_torch(m, name, seed=seed, version=version, device=view.device)
+            view.copy_(tmp.view(view.shape))
+            del tmp
 
 
 # ------------------------------------------------------------------ torch (same bits, on device)
