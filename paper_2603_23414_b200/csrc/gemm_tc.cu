@@ -35,7 +35,8 @@ struct GemmParams {
   int M, N, K;
   int m_blk, m_blocks, n_tiles, nt, tile2_off, kb;
   long long total;  // units * kb
-  int stages, tmem_cols, acc_stages;
+  int stages, xstages, tmem_cols, acc_stages;
+  int w_blocked;    // W stored tile-blocked: [N/128][K/64][128][64] (each TMA box contiguous)
   float* ws;        // [grid][2][nt][m_blk][128]
   int* counters;    // [units]
   GemmEpi epi;
@@ -221,8 +222,14 @@ __device__ __forceinline__ void apply_epilogue(const GemmParams& p, int unit_n0,
 }
 
 // ---------------------------------------------------------------- kernel
+// Warp roles: w0 weight (W) TMA producer, w6 activation (X) TMA producer, w1 TMEM
+// allocator + MMA issuer, w2..w5 epilogue.  W and X have separate smem rings:
+// the weights stream from HBM and need a deep ring, the activation k-slices are
+// L2-resident and only need a short one.
+constexpr int kGemmThreads = 224;
+
 template <int NT>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                         GemmParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -231,9 +238,11 @@ __global__ void __launch_bounds__(192, 1)
   const int stage_b = p.m_blk * 128;
   uint8_t* sA = smem;
   uint8_t* sB = smem + p.stages * stage_a;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + p.stages * stage_b);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + p.xstages * stage_b);
   uint64_t* empty = full + p.stages;
-  uint64_t* tfull = empty + p.stages;  // [2]
+  uint64_t* xfull = empty + p.stages;
+  uint64_t* xempty = xfull + p.xstages;
+  uint64_t* tfull = xempty + p.xstages;  // [2]
   uint64_t* tempty = tfull + 2;        // [2]
   uint32_t* tholder = reinterpret_cast<uint32_t*>(tempty + 2);
   int* sh_flag = reinterpret_cast<int*>(tholder + 1);
@@ -247,6 +256,10 @@ __global__ void __launch_bounds__(192, 1)
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < p.xstages; ++s) {
+      mbar_init(&xfull[s], 1);
+      mbar_init(&xempty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -272,27 +285,46 @@ __global__ void __launch_bounds__(192, 1)
 
   if (w == 0) {
     if (lane == 0) {
-      const uint64_t pol_w = policy_evict_first();
-      const uint64_t pol_x = policy_evict_last();
+      const uint64_t pol_w = policy_evict_first();  // weights: streamed once per step
       int q = 0;
       for (int u = u_first; u <= u_last; ++u) {
         const long long ub = (long long)u * p.kb;
         const int k0 = (int)((r0 > ub ? r0 : ub) - ub), k1 = (int)((r1 < ub + p.kb ? r1 : ub + p.kb) - ub);
-        const int mb = u / p.n_tiles, t = u % p.n_tiles;
+        const int t = u % p.n_tiles;
         for (int k = k0; k < k1; ++k, ++q) {
           const int s = q % p.stages;
           const uint32_t ph = (q / p.stages) & 1;
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], stage_a + stage_b);
+          mbar_arrive_expect_tx(&full[s], stage_a);
 #pragma unroll
-          for (int j = 0; j < NT; ++j)
-            tma_load_2d_hint(sA + s * stage_a + j * kStageA, &tmW, &full[s], k * 64, t * 128 + j * p.tile2_off,
-                             pol_w);
-          tma_load_2d_hint(sB + s * stage_b, &tmX, &full[s], k * 64, mb * p.m_blk, pol_x);
+          for (int j = 0; j < NT; ++j) {
+            if (p.w_blocked)
+              tma_load_2d_hint(sA + s * stage_a + j * kStageA, &tmW, &full[s], 0, (t * p.kb + k) * 128, pol_w);
+            else
+              tma_load_2d_hint(sA + s * stage_a + j * kStageA, &tmW, &full[s], k * 64, t * 128 + j * p.tile2_off,
+                               pol_w);
+          }
           if (q == 0) DBG(2);
         }
       }
       DBG(3);
+    }
+  } else if (w == 6) {
+    if (lane == 0) {
+      const uint64_t pol_x = policy_evict_last();  // activations: re-read by every tile
+      int q = 0;
+      for (int u = u_first; u <= u_last; ++u) {
+        const long long ub = (long long)u * p.kb;
+        const int k0 = (int)((r0 > ub ? r0 : ub) - ub), k1 = (int)((r1 < ub + p.kb ? r1 : ub + p.kb) - ub);
+        const int mb = u / p.n_tiles;
+        for (int k = k0; k < k1; ++k, ++q) {
+          const int s = q % p.xstages;
+          const uint32_t ph = (q / p.xstages) & 1;
+          mbar_wait(&xempty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&xfull[s], stage_b);
+          tma_load_2d_hint(sB + s * stage_b, &tmX, &xfull[s], k * 64, mb * p.m_blk, pol_x);
+        }
+      }
     }
   } else if (w == 1) {
     if (lane == 0) {
@@ -312,10 +344,13 @@ __global__ void __launch_bounds__(192, 1)
         for (int k = k0; k < k1; ++k, ++q) {
           const int s = q % p.stages;
           const uint32_t ph = (q / p.stages) & 1;
+          const int sx = q % p.xstages;
+          const uint32_t phx = (q / p.xstages) & 1;
           mbar_wait(&full[s], ph);
+          mbar_wait(&xfull[sx], phx);
           tc_fence_after();
           if (q == 0) DBG(4);
-          const uint32_t b = smem_u32(sB + s * stage_b);
+          const uint32_t b = smem_u32(sB + sx * stage_b);
 #pragma unroll
           for (int j = 0; j < NT; ++j) {
             const uint32_t aa = smem_u32(sA + s * stage_a + j * kStageA);
@@ -326,6 +361,7 @@ __global__ void __launch_bounds__(192, 1)
                           (k > k0 || kk > 0) ? 1u : 0u);
           }
           tc_commit(&empty[s]);
+          tc_commit(&xempty[sx]);
         }
         tc_commit(&tfull[a]);
       }
@@ -500,19 +536,33 @@ int gemm_bf16_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N
   p.ws = ws;
   p.counters = counters;
   p.dbg = (g_dbg && g_dbg_count++ == g_dbg_target) ? g_dbg : nullptr;
-  const int stage_bytes = p.nt * kStageA + p.m_blk * 128;
-  int stages = (190 * 1024) / stage_bytes;
-  if (stages > 8) stages = 8;
+  // smem: a short ring of activation k-slices (L2-resident) and the rest for a deep
+  // ring of weight k-slices streamed from HBM
+  const int stage_a = p.nt * kStageA, stage_b = p.m_blk * 128;
+  const int budget = 192 * 1024;
+  int xstages = stage_b <= 8192 ? 4 : (stage_b <= 16384 ? 3 : 2);
+  int stages = (budget - xstages * stage_b) / stage_a;
+  if (stages > 12) stages = 12;
   p.stages = stages;
+  p.xstages = xstages;
+  const int stage_bytes = 0;
+  (void)stage_bytes;
   p.acc_stages = (p.nt * p.m_blk * 2 <= 512) ? 2 : 1;
   int tc = 32;
   while (tc < p.nt * p.m_blk * p.acc_stages) tc <<= 1;
   p.tmem_cols = tc;
   CUtensorMap tmW, tmX;
   const int wrows = p.nt == 2 ? 2 * N : N;
-  if (tma_encode_2d(&tmW, W, wrows, K, (uint64_t)K * 2, 128, 64, 2, true)) return -2;
+  p.w_blocked = epi.w_blocked;
+  if (p.w_blocked) {
+    if (N % 128) return -1;
+    if (tma_encode_2d(&tmW, W, (uint64_t)wrows * p.kb, 64, 128, 128, 64, 2, true)) return -2;
+  } else if (tma_encode_2d(&tmW, W, wrows, K, (uint64_t)K * 2, 128, 64, 2, true)) {
+    return -2;
+  }
   if (tma_encode_2d(&tmX, X, M, K, (uint64_t)K * 2, p.m_blk, 64, 2, true)) return -2;
-  const size_t smem = 1024 + (size_t)stages * stage_bytes + (2 * stages + 8) * 8 + 32 + 128 * 17 * 4 + 128;
+  const size_t smem = 1024 + (size_t)stages * stage_a + (size_t)xstages * stage_b + (2 * stages + 2 * xstages + 8) * 8 +
+                      32 + 128 * 17 * 4 + 128;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(gemm_bf16_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -522,9 +572,9 @@ int gemm_bf16_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N
   int grid = num_sms;
   if (p.total < grid) grid = (int)p.total;
   if (p.nt == 2)
-    gemm_bf16_tc_kernel<2><<<grid, 192, smem, stream>>>(tmW, tmX, p);
+    gemm_bf16_tc_kernel<2><<<grid, kGemmThreads, smem, stream>>>(tmW, tmX, p);
   else
-    gemm_bf16_tc_kernel<1><<<grid, 192, smem, stream>>>(tmW, tmX, p);
+    gemm_bf16_tc_kernel<1><<<grid, kGemmThreads, smem, stream>>>(tmW, tmX, p);
   // units split across CTAs are finished by the parallel fixup kernel
   const int units = p.n_tiles * p.m_blocks;
   bool split = false;

@@ -12,6 +12,7 @@ enum EpiKind { EPI_F32 = 0, EPI_RESID = 1, EPI_SILU = 2, EPI_QKV = 3 };
 
 struct GemmEpi {
   int kind;
+  int w_blocked;              // W stored tile-blocked [N/128][K/64][128][64] (each TMA box contiguous)
   int ldo;                    // row stride of out_f32 / x_res / act
   float* out_f32;             // EPI_F32
   float* x_res;               // EPI_RESID

@@ -41,6 +41,7 @@ extern "C" int64_t srl_op_gemm_workspace(int32_t M, int32_t N, int32_t K, int32_
 
 extern "C" int32_t srl_op_gemm_bf16(const void* X, int32_t M, const void* W, int32_t N, int32_t K, int32_t epi,
                                     void* out, void* workspace, void* stream) {
+  const int blocked = 0;
   if (M <= 0 || N <= 0 || K <= 0 || K % 64 || epi < 0 || epi > 2 || (epi == 2 && N % 64)) {
     set_error("srl_op_gemm_bf16: %s", "bad shape / epilogue", 0);
     return -1;
@@ -48,6 +49,7 @@ extern "C" int32_t srl_op_gemm_bf16(const void* X, int32_t M, const void* W, int
   const int sms = op_sms();
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   GemmEpi e{};
+  e.w_blocked = blocked;
   e.kind = epi == 0 ? EPI_F32 : (epi == 1 ? EPI_RESID : EPI_SILU);
   e.ldo = N;
   e.out_f32 = reinterpret_cast<float*>(out);
