@@ -109,7 +109,8 @@ typedef struct srl_step_info {
 /* Per-kernel-class device timing (CUDA events on the engine stream), enabled by
  * srl_set_profiling.  Classes: */
 enum { SRL_K_GEMM_QKV = 0, SRL_K_GEMM_O = 1, SRL_K_GEMM_GU = 2, SRL_K_GEMM_DOWN = 3, SRL_K_LM_HEAD = 4,
-       SRL_K_ATTN = 5, SRL_K_ELEMWISE = 6, SRL_K_SAMPLE = 7, SRL_K_CTL = 8, SRL_K_PREFILL = 9, SRL_K_NCLASS = 10 };
+       SRL_K_ATTN = 5, SRL_K_ELEMWISE = 6, SRL_K_SAMPLE = 7, SRL_K_CTL = 8, SRL_K_PREFILL = 9,
+       SRL_K_NCLASS = 10 };
 
 /* One harvested trajectory (SPEC BufferEntry / P:199). */
 typedef struct srl_traj {
@@ -140,7 +141,9 @@ typedef struct srl_trace_rec {
 
 typedef struct srl_engine srl_engine;
 
-/* Byte sizes of the three arena regions for a configuration.  Returns < 0 for
+/* Byte sizes of the three arena regions for a configuration (weights = the
+ * staging image of srl_weight_layout followed by the packed GEMM copies, see
+ * srl_load_policy_weights).  Returns < 0 for
  * an invalid configuration (Q_g <= 0, U > pool*G in SORTED mode, ...). */
 int32_t srl_arena_sizes(const srl_model_cfg* m, const srl_sched_cfg* s, int32_t world, uint64_t* weights_bytes,
                         uint64_t* kv_bytes, uint64_t* scratch_bytes);
@@ -191,7 +194,13 @@ int32_t srl_harvest_finished(srl_engine* e, int32_t cap_recs, srl_traj* recs, in
 /* Collective over the replicas.  Install policy version `version` (> current;
  * the first call may use any version >= 0).  flat_w: device pointer to a flat
  * weight image (srl_weight_offset layout) on rank 0 (ignored elsewhere), or
- * NULL when the caller already wrote the engine's weight region.  Then applies
+ * NULL when the caller already wrote the staging part of the engine's weight
+ * region (the first srl_weight_layout bytes).  The projection matrices (wq/wk/wv,
+ * wo, wg/wu, wd, lm_head) are repacked from the source into the GEMM's packed
+ * layout (srl_op_pack_weight) in the rest of the weight region -- which is why
+ * srl_arena_sizes reports about twice the model size -- so the staging copy of
+ * those matrices is not read by decoding; the other tensors (embed, norms,
+ * biases) are copied from flat_w when it is given and read in place.  Then applies
  * the cache bound: trajectories with version - v_first > K are discarded and
  * re-queued (tokens dropped); under REPREFILL running ones are scavenged.
  * SRL_E_STATE if a group is ready but not harvested or version <= current. */

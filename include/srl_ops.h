@@ -23,17 +23,34 @@ extern "C" {
  * PAPER.md P:110 §2.2 "frequent loading of model weights").  Y = X W^T with
  *   X [M, K] bf16, W [N, K] bf16 (a linear layer's weight), fp32 accumulation
  *   (tcgen05.mma kind::f16, accumulator in TMEM, operands staged by TMA,
- *   persistent stream-K with a fixed-order fixup: bit-reproducible), and
+ *   split-K only inside a thread-block cluster, reduced over DSMEM in a fixed
+ *   order: bit-reproducible), and
  *   epi = 0: out fp32 [M, N]  = Y
  *   epi = 1: out fp32 [M, N] += Y                       (residual add)
  *   epi = 2: W has 2N rows, gate and up rows interleaved in 64-row blocks (rows
  *            [128b, 128b+64) = gate rows [64b, 64b+64), rows [128b+64, 128b+128) =
  *            the matching up rows); out bf16 [M, N] = silu(Yg) * Yu
- * workspace: device bytes >= srl_op_gemm_workspace(M, N, K, epi).
+ * epi | SRL_GEMM_W_PACKED: W is in the packed layout written by srl_op_pack_weight
+ *   (for epi 2: the packed image of the interleaved [2N, K] matrix) instead of
+ *   row-major; the weight stream then moves contiguous 16 KB blocks.
+ * workspace: device bytes >= srl_op_gemm_workspace(M, N, K, epi) (currently
+ *   unused by the kernel; kept so callers need not change if a variant needs it).
  * Requires K % 64 == 0 and, for epi 2, N % 64 == 0. */
+#define SRL_GEMM_W_PACKED 0x100
 int64_t srl_op_gemm_workspace(int32_t M, int32_t N, int32_t K, int32_t epi);
 int32_t srl_op_gemm_bf16(const void* X, int32_t M, const void* W, int32_t N, int32_t K, int32_t epi, void* out,
                          void* workspace, void* stream);
+
+/* Packed weight layout for srl_op_gemm_bf16 (and the engine's internal copy
+ * of its projection weights; written by srl_load_policy_weights).  W [N, K] bf16
+ * row-major -> dst of srl_op_packed_weight_bytes(N, K) bytes: blocks of 16 KB
+ * ordered [ceil(N/128)][K/64]; block (t, k) holds rows 128t..128t+127 and columns
+ * 64k..64k+63 exactly as the tcgen05 SWIZZLE_128B shared-memory image (row r at
+ * byte r*128, its 16-byte chunk c at chunk position c ^ (r % 8)); rows >= N are
+ * zero.  Requires K % 64 == 0.  srl_op_packed_weight_bytes returns -1 on bad
+ * shapes. */
+int64_t srl_op_packed_weight_bytes(int32_t N, int32_t K);
+int32_t srl_op_pack_weight(const void* W, int32_t N, int32_t K, void* dst, void* stream);
 
 /* Paged decode attention with GQA (PagedAttention).
  *   q          [M, Hq, dh]  bf16 (kv_fp32 = 0) or fp32 (kv_fp32 = 1)

@@ -65,6 +65,8 @@ SIGNATURES = {
     "srl_last_error": (C.c_char_p, []),
     "srl_op_gemm_bf16": (_I32, [_P, _I32, _P, _I32, _I32, _I32, _P, _P, _P]),
     "srl_op_gemm_workspace": (_I64, [_I32, _I32, _I32, _I32]),
+    "srl_op_packed_weight_bytes": (_I64, [_I32, _I32]),
+    "srl_op_pack_weight": (_I32, [_P, _I32, _I32, _P, _P]),
     "srl_op_attention_workspace": (_I64, [_I32, _I32, _I32, _I32, _I32]),
     "srl_op_attention": (_I32, [_P, _P, _P, _I32, _P, _I32, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P, _P, _P]),
     "srl_op_sample": (_I32, [_P, _I32, _I32, _P, _P, _P, C.c_float, _U64, _P, _P, _P, _P]),
@@ -84,6 +86,8 @@ SIGNATURES = {
     "srl_set_profiling": (_I32, [_P, _I32]),
     "srl_get_profile": (_I32, [_P, C.POINTER(C.c_double), _I64P]),
 }
+
+GEMM_W_PACKED = 0x100   # srl_ops.h SRL_GEMM_W_PACKED
 
 _lib = None
 

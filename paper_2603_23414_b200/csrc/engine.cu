@@ -27,7 +27,8 @@ constexpr size_t kAlign = 1024;
 inline size_t al(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct LayerW {
-  __nv_bfloat16 *attn_norm, *wqkv, *bqkv, *wo, *mlp_norm, *wgu, *wd;
+  __nv_bfloat16 *attn_norm, *wqkv, *bqkv, *wo, *mlp_norm, *wgu, *wd;  // staging (srl_weight_layout)
+  uint8_t *pqkv, *po, *pgu, *pd;                                     // packed GEMM copies (pack_weight)
 };
 
 // ------------------------------------------------------------------ weight layout
@@ -86,6 +87,34 @@ WeightLayout make_layout(const srl_model_cfg& m) {
   return w;
 }
 
+// Packed copies of the projection matrices (the GEMM weight stream), placed after
+// the staging region: per layer qkv, o, gate/up (interleaved rows), down; then lm_head.
+struct PackedLayout {
+  size_t base = 0, per_layer = 0, qkv = 0, o = 0, gu = 0, dn = 0, lm = 0, total = 0;
+};
+PackedLayout make_packed(const srl_model_cfg& m, size_t staging_total) {
+  PackedLayout p;
+  const int d = m.d, qd = m.Hq * m.dh, nqkv = (m.Hq + 2 * m.Hkv) * m.dh;
+  p.base = al(staging_total);
+  p.qkv = 0;
+  p.o = p.qkv + al(packed_weight_bytes(nqkv, d));
+  p.gu = p.o + al(packed_weight_bytes(d, qd));
+  p.dn = p.gu + al(packed_weight_bytes(2 * m.ff, d));
+  p.per_layer = p.dn + al(packed_weight_bytes(d, m.ff));
+  p.lm = (size_t)m.L * p.per_layer;
+  p.total = p.base + p.lm + al(packed_weight_bytes(m.V, d));
+  return p;
+}
+bool is_packed_tensor(const std::string& n) {
+  static const char* kSuffix[] = {".wq", ".wk", ".wv", ".wo", ".wg", ".wu", ".wd"};
+  if (n == "lm_head") return true;
+  for (const char* x : kSuffix) {
+    const size_t k = strlen(x);
+    if (n.size() > k && n.compare(n.size() - k, k, x) == 0) return true;
+  }
+  return false;
+}
+
 // ------------------------------------------------------------------ scratch layout
 struct ScratchPlan {
   size_t total = 0;
@@ -98,7 +127,7 @@ struct ScratchPlan {
 
 struct Sizes {
   int Q_g, R, Q_tot, max_pages, max_ctx, max_prompts, mmax, prefill_rows_max, max_items, G;
-  long long ev_cap, h_cap_tok, part_floats, n_counters;
+  long long ev_cap, h_cap_tok;
   size_t qkv_n;
 };
 
@@ -143,13 +172,6 @@ Sizes compute_sizes(const srl_model_cfg* m, const srl_sched_cfg* s, int world) {
   const int gmax = s->max_traj < kMaxGroup ? s->max_traj : kMaxGroup;
   z.h_cap_tok = (long long)gmax * s->cap;
   z.qkv_n = (size_t)(m->Hq + 2 * m->Hkv) * m->dh;
-  // fused-GEMM workspace: stream-K partials (2 slots per CTA, <= 2 weight tiles) + unit counters
-  z.part_floats = (long long)(gemm_workspace_bytes(z.mmax, 2, 160) / 4);
-  int nmax = (int)z.qkv_n;
-  if (m->d > nmax) nmax = m->d;
-  if (m->ff > nmax) nmax = m->ff;
-  if (m->V > nmax) nmax = m->V;
-  z.n_counters = (long long)gemm_counter_count(z.mmax, nmax);
 
   return z;
 }
@@ -169,14 +191,14 @@ struct srl_engine {
   WeightLayout wl;
   std::vector<LayerW> lw;
   __nv_bfloat16 *embed = nullptr, *final_norm = nullptr, *lm_head = nullptr;
+  uint8_t* plm_head = nullptr;  // packed copy
+  PackedLayout pk;
   std::vector<void*> kpool, vpool;
   std::vector<CUtensorMap> tmK, tmV;
   // scratch
   float* x_res = nullptr;
   __nv_bfloat16 *xn = nullptr, *attn_out = nullptr, *act = nullptr;
   void* qbuf = nullptr;
-  float* part = nullptr;  // GEMM stream-K workspace
-  int* gcount = nullptr;  // GEMM unit counters (zero between launches)
   float* logits = nullptr;
   float *rope_cos = nullptr, *rope_sin = nullptr;
   int* row_slot_id = nullptr;  // identity rows 0..Q_g-1
@@ -324,8 +346,6 @@ void plan_scratch(srl_engine* e, ScratchPlan& p, bool assign) {
   e->attn_out = (__nv_bfloat16*)P(2ull * z.mmax * m.Hq * m.dh);
   e->act = (__nv_bfloat16*)P(2ull * z.mmax * m.ff);
   e->qbuf = P((e->kv_f32 ? 4ull : 2ull) * z.mmax * m.Hq * m.dh);
-  e->part = (float*)P(4ull * z.part_floats);
-  e->gcount = (int*)P(4ull * z.n_counters);
   e->logits = (float*)P(4ull * z.Q_g * m.V);
   e->rope_cos = (float*)P(4ull * z.max_ctx * (m.dh / 2));
   e->rope_sin = (float*)P(4ull * z.max_ctx * (m.dh / 2));
@@ -344,8 +364,11 @@ size_t kv_bytes_for(const srl_model_cfg& m, const srl_sched_cfg& s) {
 }
 
 // ---- fused GEMM helper
-void run_gemm(srl_engine* e, const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N, int K, const GemmEpi& epi) {
-  gemm_bf16_fused(X, M, W, N, K, epi, e->part, e->gcount, e->num_sms, e->st);
+// one fused GEMM launch, profiled under `cls`
+void run_gemm(srl_engine* e, int cls, const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N, int K,
+              const GemmEpi& epi) {
+  Prof p(e, cls);
+  gemm_bf16_fused(X, M, W, N, K, epi, e->num_sms, e->st);
   e->launches++;
 }
 
@@ -391,45 +414,36 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
   qe.Hkv = m.Hkv;
   qe.dh = m.dh;
   qe.kv_f32 = e->kv_f32 ? 1 : 0;
+  qe.w_packed = 1;
   GemmEpi re{};
+  re.w_packed = 1;
   re.kind = EPI_RESID;
   re.x_res = e->x_res;
   re.ldo = d;
   GemmEpi se{};
+  se.w_packed = 1;
   se.kind = EPI_SILU;
   se.act = e->act;
   se.ldo = m.ff;
   for (int l = 0; l < m.L; ++l) {
     const LayerW& w = e->lw[l];
-    {
-      Prof p(e, D + SRL_K_GEMM_QKV);
-      qe.bias = m.qkv_bias ? w.bqkv : nullptr;
-      qe.k_pool = e->kpool[l];
-      qe.v_pool = e->vpool[l];
-      run_gemm(e, e->xn, M, w.wqkv, Nqkv, d, qe);
-    }
+    qe.bias = m.qkv_bias ? w.bqkv : nullptr;
+    qe.k_pool = e->kpool[l];
+    qe.v_pool = e->vpool[l];
+    run_gemm(e, D + SRL_K_GEMM_QKV, e->xn, M, (const __nv_bfloat16*)w.pqkv, Nqkv, d, qe);
     a.k_pool = e->kpool[l];
     a.v_pool = e->vpool[l];
     {
       Prof p(e, D + SRL_K_ATTN, 2);
       attn_run(a, e->kv_f32, &e->tmK[l], &e->tmV[l], st);
     }
-    {
-      Prof p(e, D + SRL_K_GEMM_O);
-      run_gemm(e, e->attn_out, M, w.wo, d, qd, re);
-    }
+    run_gemm(e, D + SRL_K_GEMM_O, e->attn_out, M, (const __nv_bfloat16*)w.po, d, qd, re);
     {
       Prof p(e, D + SRL_K_ELEMWISE);
       rmsnorm(e->x_res, row_tok, row_pos, M, d, nullptr, w.mlp_norm, m.rms_eps, e->xn, st);
     }
-    {
-      Prof p(e, D + SRL_K_GEMM_GU);
-      run_gemm(e, e->xn, M, w.wgu, 2 * m.ff, d, se);  // interleaved gate/up rows
-    }
-    {
-      Prof p(e, D + SRL_K_GEMM_DOWN);
-      run_gemm(e, e->act, M, w.wd, d, m.ff, re);
-    }
+    run_gemm(e, D + SRL_K_GEMM_GU, e->xn, M, (const __nv_bfloat16*)w.pgu, 2 * m.ff, d, se);  // interleaved gate/up
+    run_gemm(e, D + SRL_K_GEMM_DOWN, e->act, M, (const __nv_bfloat16*)w.pd, d, m.ff, re);
     {
       Prof p(e, D + SRL_K_ELEMWISE);
       const __nv_bfloat16* next = l + 1 < m.L ? e->lw[l + 1].attn_norm : e->final_norm;
@@ -438,12 +452,12 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
     e->launches += 4;
   }
   if (decode) {
-    Prof p(e, SRL_K_LM_HEAD);
     GemmEpi fe{};
     fe.kind = EPI_F32;
     fe.out_f32 = e->logits;
     fe.ldo = m.V;
-    run_gemm(e, e->xn, M, e->lm_head, m.V, d, fe);
+    fe.w_packed = 1;
+    run_gemm(e, SRL_K_LM_HEAD, e->xn, M, (const __nv_bfloat16*)e->plm_head, m.V, d, fe);
   }
 }
 
@@ -497,7 +511,7 @@ int32_t srl_arena_sizes(const srl_model_cfg* m, const srl_sched_cfg* s, int32_t 
   tmp.kv_f32 = s->kv_dtype == SRL_KV_FP32;
   ScratchPlan p;
   plan_scratch(&tmp, p, false);
-  if (wb) *wb = make_layout(*m).total;
+  if (wb) *wb = make_packed(*m, make_layout(*m).total).total;
   if (kb) *kb = kv_bytes_for(*m, *s);
   if (sb) *sb = p.total;
   return SRL_OK;
@@ -561,9 +575,16 @@ int32_t srl_create(const srl_model_cfg* m, const srl_sched_cfg* s, int32_t devic
   e->embed = wp("embed");
   e->final_norm = wp("final_norm");
   e->lm_head = wp("lm_head");
+  e->pk = make_packed(*m, e->wl.total);
+  e->plm_head = e->W + e->pk.base + e->pk.lm;
   for (int l = 0; l < m->L; ++l) {
     const std::string p = "L" + std::to_string(l) + ".";
     LayerW w;
+    uint8_t* lp = e->W + e->pk.base + (size_t)l * e->pk.per_layer;
+    w.pqkv = lp + e->pk.qkv;
+    w.po = lp + e->pk.o;
+    w.pgu = lp + e->pk.gu;
+    w.pd = lp + e->pk.dn;
     w.attn_norm = wp(p + "attn_norm");
     w.wqkv = wp(p + "wq");
     w.bqkv = m->qkv_bias ? wp(p + "bq") : nullptr;
@@ -617,7 +638,6 @@ int32_t srl_create(const srl_model_cfg* m, const srl_sched_cfg* s, int32_t devic
   e->prompt_tok_cap = (long long)e->z.max_prompts * s->max_prompt;
   // init device state
   cudaMemsetAsync(e->KV, 0, mem->kv_bytes, e->st);  // finite values in never-written KV rows
-  cudaMemsetAsync(e->gcount, 0, 4ull * e->z.n_counters, e->st);
   std::vector<int> ident(s->Q_g);
   for (int i = 0; i < s->Q_g; ++i) ident[i] = i;
   cudaMemcpyAsync(e->row_slot_id, ident.data(), 4 * s->Q_g, cudaMemcpyHostToDevice, e->st);
@@ -832,8 +852,34 @@ int32_t srl_load_policy_weights(srl_engine* e, const void* flat_w, int64_t versi
   if (e->group_state == 1) return fail(SRL_E_STATE, "srl_load_policy_weights: harvest the ready group first");
   if (version < 0 || (e->v_valid && version <= e->v))
     return fail(SRL_E_STATE, "srl_load_policy_weights: policy version must increase");
-  if (flat_w && flat_w != e->W) {
-    cudaMemcpyAsync(e->W, flat_w, e->wl.total, cudaMemcpyDeviceToDevice, e->st);
+  // Pack the projection matrices from the staging-layout source straight into the
+  // GEMM weight stream's layout; the remaining tensors (embedding, norms, biases)
+  // are read in place, so copy those when the source is the caller's buffer.
+  const uint8_t* src = flat_w ? (const uint8_t*)flat_w : e->W;
+  if (src != e->W) {
+    for (const auto& en : e->wl.ents)
+      if (!is_packed_tensor(en.name))
+        cudaMemcpyAsync(e->W + en.off, src + en.off, en.numel * 2, cudaMemcpyDeviceToDevice, e->st);
+  }
+  {
+    const srl_model_cfg& m = e->m;
+    const int d = m.d, qd = m.Hq * m.dh, nqkv = (m.Hq + 2 * m.Hkv) * m.dh;
+    auto sp = [&](const std::string& n) {
+      return (const __nv_bfloat16*)(src + e->wl.find(n)->off);
+    };
+    int rc = 0;
+    for (int l = 0; l < m.L; ++l) {
+      const std::string p = "L" + std::to_string(l) + ".";
+      const LayerW& w = e->lw[l];
+      rc |= pack_weight(sp(p + "wq"), nqkv, d, w.pqkv, e->st);
+      rc |= pack_weight(sp(p + "wo"), d, qd, w.po, e->st);
+      rc |= pack_weight(sp(p + "wg"), 2 * m.ff, d, w.pgu, e->st);
+      rc |= pack_weight(sp(p + "wd"), d, m.ff, w.pd, e->st);
+      e->launches += 4;
+    }
+    rc |= pack_weight(sp("lm_head"), m.V, d, e->plm_head, e->st);
+    e->launches++;
+    if (rc) return cuda_fail("srl_load_policy_weights: pack_weight", cudaGetLastError());
   }
   ctl_bump(e->ctl, (int)version, e->st);
   e->launches++;

@@ -1,0 +1,180 @@
+// gemm_epi.cuh — fused GEMM epilogues (included by gemm_tc.cu after GemmParams).
+//
+// A 16-column chunk of the accumulator arrives one weight row per thread
+// (thread n <-> TMEM lane n, 16 batch rows in registers).  Every epilogue first
+// transposes the chunk through shared memory so that thread t then owns batch
+// row m0 + t/8 and a run of 16 consecutive weight rows (8 outputs for SiLU):
+// the global writes become 16- or 64-byte vectors along the contiguous output
+// dimension instead of 2- or 4-byte scalars strided by the row pitch.
+#pragma once
+
+// named barrier of one epilogue group (4 warps covering the 128 TMEM lanes)
+__device__ __forceinline__ void epi_bar(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(kEpiThreads)); }
+
+// SiLU(g) * u with the hardware exp2 / reciprocal: |rel err| ~ 2^-21, far below
+// the bf16 rounding of the stored activation; g -> -inf gives 0 (fdividef by inf)
+__device__ __forceinline__ float silu_mul(float g, float u) { return __fdividef(g, 1.f + __expf(-g)) * u; }
+
+constexpr int kXchPitch = 132;                   // floats per staged batch row (128 + 4: conflict-free)
+constexpr int kXchFloats = 16 * kXchPitch + 64;  // staged chunk + 32 ints (QKV position / page lookups)
+
+__device__ __forceinline__ void store16_bf16(__nv_bfloat16* dst, const float (&y)[16]) {
+  uint4 a, b;
+  a.x = pack_bf16(y[0], y[1]);
+  a.y = pack_bf16(y[2], y[3]);
+  a.z = pack_bf16(y[4], y[5]);
+  a.w = pack_bf16(y[6], y[7]);
+  b.x = pack_bf16(y[8], y[9]);
+  b.y = pack_bf16(y[10], y[11]);
+  b.z = pack_bf16(y[12], y[13]);
+  b.w = pack_bf16(y[14], y[15]);
+  reinterpret_cast<uint4*>(dst)[0] = a;
+  reinterpret_cast<uint4*>(dst)[1] = b;
+}
+__device__ __forceinline__ void store16_f32(float* dst, const float (&y)[16]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) reinterpret_cast<float4*>(dst)[q] = make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
+}
+
+// ---------------------------------------------------------------- fused epilogue
+// v[j]: value of weight row unit_n0 + n for batch row m0 + j, j < 16.
+// xch: this group's shared staging buffer (kXchFloats); bar: its named barrier.
+__device__ __forceinline__ void apply_epilogue(const GemmParams& p, int unit_n0, int n, int m0, const float (&v)[16],
+                                               float* xch, int bar) {
+  const GemmEpi& e = p.epi;
+  int* spos = reinterpret_cast<int*>(xch + 16 * kXchPitch);
+  int* spage = spos + 16;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) xch[j * kXchPitch + n] = v[j];
+  if (e.kind == EPI_QKV && n < 16) {
+    // the chunk's 16 (position, KV page) pairs, looked up once
+    const int m = m0 + n;
+    const int pos = m < p.M ? __ldg(e.row_pos + m) : -1;
+    spos[n] = pos;
+    spage[n] = pos >= 0 ? __ldg(e.page_table + (size_t)__ldg(e.row_slot + m) * e.max_pages + pos / 64) : 0;
+  }
+  epi_bar(bar);
+  const int ml = n >> 3;  // batch row within the chunk owned from here on
+  const int m = m0 + ml;
+  const float* row = xch + ml * kXchPitch;
+  if (e.kind == EPI_SILU) {
+    // 64-row interleave: tile rows [0,64) are gate rows, [64,128) the up rows of
+    // the same 64 outputs; thread owns outputs ob..ob+7 of this tile
+    const int ob = (n & 7) * 8;
+    if (m < p.M) {
+      float g[8], u[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        g[k] = row[ob + k];
+        u[k] = row[64 + ob + k];
+      }
+      uint4 pk;
+      pk.x = pack_bf16(silu_mul(g[0], u[0]), silu_mul(g[1], u[1]));
+      pk.y = pack_bf16(silu_mul(g[2], u[2]), silu_mul(g[3], u[3]));
+      pk.z = pack_bf16(silu_mul(g[4], u[4]), silu_mul(g[5], u[5]));
+      pk.w = pack_bf16(silu_mul(g[6], u[6]), silu_mul(g[7], u[7]));
+      *reinterpret_cast<uint4*>(e.act + (size_t)m * e.ldo + (unit_n0 >> 1) + ob) = pk;
+    }
+  } else {
+    const int nb = (n & 7) * 16;  // first of the thread's 16 weight rows
+    const int ng0 = unit_n0 + nb;
+    float r[16];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 t = *reinterpret_cast<const float4*>(row + nb + 4 * q);
+      r[4 * q] = t.x;
+      r[4 * q + 1] = t.y;
+      r[4 * q + 2] = t.z;
+      r[4 * q + 3] = t.w;
+    }
+    if (m < p.M && ng0 < p.N) {
+      const bool full = ng0 + 16 <= p.N;
+      switch (e.kind) {
+        case EPI_F32: {
+          float* dst = e.out_f32 + (size_t)m * e.ldo + ng0;
+          if (full) {
+            store16_f32(dst, r);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+              if (ng0 + k < p.N) dst[k] = r[k];
+          }
+          break;
+        }
+        case EPI_RESID: {
+          // exactly one writer per element per launch: plain vector read-modify-write
+          float* dst = e.x_res + (size_t)m * e.ldo + ng0;
+          if (full) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float4 x = reinterpret_cast<float4*>(dst)[q];
+              x.x += r[4 * q];
+              x.y += r[4 * q + 1];
+              x.z += r[4 * q + 2];
+              x.w += r[4 * q + 3];
+              reinterpret_cast<float4*>(dst)[q] = x;
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+              if (ng0 + k < p.N) dst[k] += r[k];
+          }
+          break;
+        }
+        case EPI_QKV: {
+          // rows [q heads | k heads | v heads] x dh; a 16-row run stays inside one
+          // half of one head (dh/2 is a multiple of 16)
+          const int pos = spos[ml];
+          if (pos < 0) break;
+          const int dh = e.dh, half = dh / 2;
+          const int h = ng0 / dh, i0 = ng0 % dh;
+          float y[16];
+          if (e.bias) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) r[k] += __bfloat162float(e.bias[ng0 + k]);
+          }
+          if (h < e.Hq + e.Hkv) {
+            // RoPE pairs (i, i + half): the partner run is read from the staged chunk
+            const bool lo = i0 < half;
+            const int d0 = lo ? i0 : i0 - half;                  // frequency index of r[0]
+            const int pn = lo ? nb + half : nb - half;           // partner rows in the tile
+            float c[16], s[16];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float4 cq = __ldg(reinterpret_cast<const float4*>(e.rope_cos + (size_t)pos * half + d0) + q);
+              const float4 sq = __ldg(reinterpret_cast<const float4*>(e.rope_sin + (size_t)pos * half + d0) + q);
+              c[4 * q] = cq.x; c[4 * q + 1] = cq.y; c[4 * q + 2] = cq.z; c[4 * q + 3] = cq.w;
+              s[4 * q] = sq.x; s[4 * q + 1] = sq.y; s[4 * q + 2] = sq.z; s[4 * q + 3] = sq.w;
+            }
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              float x1 = row[pn + k];
+              if (e.bias) x1 += __bfloat162float(e.bias[unit_n0 + pn + k]);
+              // lo half: y = x*c - x_hi*s ; hi half: y = x*c + x_lo*s
+              y[k] = lo ? r[k] * c[k] - x1 * s[k] : r[k] * c[k] + x1 * s[k];
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) y[k] = r[k];
+          }
+          size_t off;
+          void* base;
+          if (h < e.Hq) {
+            off = ((size_t)m * e.Hq + h) * dh + i0;
+            base = e.q_out;
+          } else {
+            const int kvh = h < e.Hq + e.Hkv ? h - e.Hq : h - e.Hq - e.Hkv;
+            off = (((size_t)spage[ml] * e.Hkv + kvh) * 64 + pos % 64) * dh + i0;
+            base = h < e.Hq + e.Hkv ? e.k_pool : e.v_pool;
+          }
+          if (e.kv_f32)
+            store16_f32(reinterpret_cast<float*>(base) + off, y);
+          else
+            store16_bf16(reinterpret_cast<__nv_bfloat16*>(base) + off, y);
+          break;
+        }
+      }
+    }
+  }
+  epi_bar(bar);  // the staging buffer is reused by the next chunk
+}

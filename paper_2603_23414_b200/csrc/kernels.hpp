@@ -12,7 +12,7 @@ enum EpiKind { EPI_F32 = 0, EPI_RESID = 1, EPI_SILU = 2, EPI_QKV = 3 };
 
 struct GemmEpi {
   int kind;
-  int w_blocked;              // W stored tile-blocked [N/128][K/64][128][64] (each TMA box contiguous)
+  int w_packed;               // W in the packed layout of pack_weight() (else row-major [N, K])
   int ldo;                    // row stride of out_f32 / x_res / act
   float* out_f32;             // EPI_F32
   float* x_res;               // EPI_RESID
@@ -32,13 +32,20 @@ struct GemmEpi {
 };
 
 // ---- gemm_tc.cu
-// Y = X[M,K] . W[N,K]^T with the fused epilogue `epi` (for EPI_SILU, W holds
-// 2N rows: gate rows [0,N) then up rows [N,2N)).  ws / counters: workspace of
-// gemm_workspace_bytes(M, nt, num_sms) bytes and gemm_counter_count(M, N)
-// zero-initialised ints (left zeroed on return).
+// Y = X[M,K] . W[N,K]^T with the fused epilogue `epi` (for EPI_SILU, W's
+// N rows are the interleaved gate/up rows: 64 gate rows, then the matching 64 up
+// rows, per 128-row block).  One kernel launch, no workspace: split-K partials
+// are reduced over distributed shared memory inside a thread-block cluster.
+// Returns 0, -1 (bad shape) or -2/-3 (TMA encode / launch failure).
 int gemm_bf16_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N, int K, const GemmEpi& epi,
-                    float* ws, int* counters, int num_sms, cudaStream_t stream);
-size_t gemm_workspace_bytes(int M, int nt, int num_sms);
-size_t gemm_counter_count(int M, int N_units_rows);
+                    int num_sms, cudaStream_t stream);
+void gemm_set_debug(unsigned long long* buf, int target);
+
+// Packed weight layout for the GEMM's weight stream: [ceil(N/128)][K/64] blocks of
+// 16 KB, block (t, k) = rows 128t..128t+127 x cols 64k..64k+63 stored exactly as
+// the SWIZZLE_128B shared-memory image (row r at r*128 B, its 16-byte chunk c at
+// chunk c ^ (r % 8)); rows past N are zero.  One block = one contiguous bulk copy.
+size_t packed_weight_bytes(int N, int K);
+int pack_weight(const __nv_bfloat16* src, int N, int K, void* dst, cudaStream_t stream);
 
 }  // namespace srl

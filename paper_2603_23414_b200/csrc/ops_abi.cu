@@ -35,13 +35,16 @@ extern "C" void srl_debug_gemm_timestamps(unsigned long long* dev_buf, int32_t t
 }
 
 extern "C" int64_t srl_op_gemm_workspace(int32_t M, int32_t N, int32_t K, int32_t epi) {
+  epi &= ~SRL_GEMM_W_PACKED;
   if (M <= 0 || N <= 0 || K <= 0 || epi < 0 || epi > 2) return -1;
-  return (int64_t)((gemm_workspace_bytes(M, 1, 148 > op_sms() ? 148 : op_sms()) + 255) / 256 * 256);
+  (void)K;
+  return 256;
 }
 
 extern "C" int32_t srl_op_gemm_bf16(const void* X, int32_t M, const void* W, int32_t N, int32_t K, int32_t epi,
                                     void* out, void* workspace, void* stream) {
-  const int blocked = 0;
+  const int packed = (epi & SRL_GEMM_W_PACKED) ? 1 : 0;
+  epi &= ~SRL_GEMM_W_PACKED;
   if (M <= 0 || N <= 0 || K <= 0 || K % 64 || epi < 0 || epi > 2 || (epi == 2 && N % 64)) {
     set_error("srl_op_gemm_bf16: %s", "bad shape / epilogue", 0);
     return -1;
@@ -49,7 +52,7 @@ extern "C" int32_t srl_op_gemm_bf16(const void* X, int32_t M, const void* W, int
   const int sms = op_sms();
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   GemmEpi e{};
-  e.w_blocked = blocked;
+  e.w_packed = packed;
   e.kind = epi == 0 ? EPI_F32 : (epi == 1 ? EPI_RESID : EPI_SILU);
   e.ldo = N;
   e.out_f32 = reinterpret_cast<float*>(out);
@@ -57,8 +60,24 @@ extern "C" int32_t srl_op_gemm_bf16(const void* X, int32_t M, const void* W, int
   e.act = reinterpret_cast<__nv_bfloat16*>(out);
   const int rows = epi == 2 ? 2 * N : N;  // SiLU-mul: interleaved gate/up rows
   int r = gemm_bf16_fused(reinterpret_cast<const __nv_bfloat16*>(X), M, reinterpret_cast<const __nv_bfloat16*>(W),
-                          rows, K, e, reinterpret_cast<float*>(workspace), nullptr, sms, st);
+                          rows, K, e, sms, st);
+  (void)workspace;
   if (r) set_error("srl_op_gemm_bf16: %s (code %ld)", r == -1 ? "bad shape" : "launch/tma failure", r);
+  return r;
+}
+
+extern "C" int64_t srl_op_packed_weight_bytes(int32_t N, int32_t K) {
+  if (N <= 0 || K <= 0 || K % 64) return -1;
+  return (int64_t)packed_weight_bytes(N, K);
+}
+
+extern "C" int32_t srl_op_pack_weight(const void* W, int32_t N, int32_t K, void* dst, void* stream) {
+  if (!W || !dst || N <= 0 || K <= 0 || K % 64) {
+    set_error("srl_op_pack_weight: %s", "bad shape / null pointer", 0);
+    return -1;
+  }
+  const int r = pack_weight(reinterpret_cast<const __nv_bfloat16*>(W), N, K, dst, reinterpret_cast<cudaStream_t>(stream));
+  if (r) set_error("srl_op_pack_weight: %s (code %ld)", "launch failure", r);
   return r;
 }
 

@@ -145,8 +145,8 @@ class RolloutEngine:
 
     def profile(self):
         """{class: (device ms, launches)} accumulated since set_profiling(True)."""
-        ms = (C.c_double * 10)()
-        nl = (C.c_int64 * 10)()
+        ms = (C.c_double * len(_lib.KERNEL_CLASSES))()
+        nl = (C.c_int64 * len(_lib.KERNEL_CLASSES))()
         check(self.lib.srl_get_profile(self.h, ms, nl), "srl_get_profile")
         return {k: (ms[i], nl[i]) for i, k in enumerate(_lib.KERNEL_CLASSES)}
 

@@ -77,4 +77,7 @@ def test_arena_sizes_and_validation_on_cpu(lib):
     m8 = _lib.ModelCfg(LLAMA8B.L, LLAMA8B.d, LLAMA8B.Hq, LLAMA8B.Hkv, LLAMA8B.dh, LLAMA8B.ff, LLAMA8B.V, 5e5, 1e-5, 0)
     s8 = _lib.SchedCfg(256, 64, -1, 1024, 1, 8192, 64, 12000, 0, 0, 0, 0, -1, 0, 1.0, 3, 2048, 256, 4096)
     assert L.srl_arena_sizes(ctypes.byref(m8), ctypes.byref(s8), 1, ctypes.byref(w), ctypes.byref(k), ctypes.byref(sc)) == 0
-    assert abs(w.value - 16.06e9) / 16.06e9 < 0.01           # bf16 LLaMA-3.1-8B weights
+    # bf16 LLaMA-3.1-8B weights (staging image) + packed copies of the projection matrices
+    mats = LLAMA8B.L * ((LLAMA8B.Hq + 2 * LLAMA8B.Hkv) * LLAMA8B.dh * 4096 + 4096 * 4096 + 2 * 14336 * 4096
+                        + 4096 * 14336) + LLAMA8B.V * 4096
+    assert abs(w.value - (16.06e9 + 2 * mats)) / 16.06e9 < 0.01

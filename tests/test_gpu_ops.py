@@ -27,12 +27,43 @@ GEMM_SHAPES = [(1, 128, 64), (16, 256, 128), (200, 384, 256), (256, 6144, 4096),
                (300, 1024, 14336)]
 
 
-def _gemm(lib, X, W, N, epi, out):
+def _pack(lib, W):
+    rows, K = W.shape
+    dst = torch.empty(lib.srl_op_packed_weight_bytes(rows, K), dtype=torch.uint8, device="cuda")
+    assert lib.srl_op_pack_weight(W.data_ptr(), rows, K, dst.data_ptr(), _stream()) == 0
+    return dst
+
+
+def _gemm(lib, X, W, N, epi, out, packed=False):
     M, K = X.shape
     ws = torch.empty(lib.srl_op_gemm_workspace(M, N, K, epi), dtype=torch.uint8, device="cuda")
-    rc = lib.srl_op_gemm_bf16(X.data_ptr(), M, W.data_ptr(), N, K, epi, out.data_ptr(), ws.data_ptr(), _stream())
+    Wp = _pack(lib, W) if packed else W
+    flag = 0x100 if packed else 0                      # SRL_GEMM_W_PACKED
+    rc = lib.srl_op_gemm_bf16(X.data_ptr(), M, Wp.data_ptr(), N, K, epi | flag, out.data_ptr(), ws.data_ptr(),
+                              _stream())
     torch.cuda.synchronize()
     return rc
+
+
+def test_pack_weight_layout(lib):
+    """srl_op_pack_weight writes the layout srl_ops.h defines: 16 KB blocks [ceil(N/128)][K/64],
+    row r of a block at r*128 B with its 16-byte chunk c at chunk c ^ (r % 8), zero rows past N."""
+    N, K = 200, 192
+    W = torch.arange(N * K, device="cuda", dtype=torch.int32).remainder(30011).to(torch.bfloat16).view(N, K)
+    got = _pack(lib, W).cpu().view(torch.int16).numpy()
+    w = W.cpu().view(torch.int16).numpy()
+    nt, kb = (N + 127) // 128, K // 64
+    assert got.size == nt * kb * 128 * 64
+    exp = np.zeros((nt, kb, 128, 8, 8), dtype=np.int16)     # [tile][kblock][row][chunk position][8 elems]
+    for t in range(nt):
+        for k in range(kb):
+            for r in range(128):
+                row = t * 128 + r
+                if row >= N:
+                    continue
+                for c in range(8):
+                    exp[t, k, r, c ^ (r % 8)] = w[row, k * 64 + c * 8:k * 64 + c * 8 + 8]
+    assert np.array_equal(got, exp.reshape(-1))
 
 
 def _bound(X, W):
@@ -40,37 +71,40 @@ def _bound(X, W):
     return (X.double().abs() @ W.double().abs().t()) * (X.shape[1] * 2.0 ** -24) + 1e-12
 
 
+@pytest.mark.parametrize("packed", [False, True], ids=["rowmajor", "packed"])
 @pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
-def test_gemm_matches_fp64_reference(lib, M, N, K):
+def test_gemm_matches_fp64_reference(lib, M, N, K, packed):
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
     X = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
     W = (torch.randn(N, K, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
     out = torch.full((M, N), float("nan"), device="cuda")
-    assert _gemm(lib, X, W, N, 0, out) == 0
+    assert _gemm(lib, X, W, N, 0, out, packed) == 0
     ref = X.double() @ W.double().t()
     got = out.double()
     assert ((got - ref).abs() <= _bound(X, W)).all()
     assert ((got - ref).norm() / ref.norm()).item() < 1e-5
-    # bit-reproducible run to run (fixed-order stream-K fixup)
+    # bit-reproducible run to run (fixed-order split-K reduction)
     out2 = torch.empty_like(out)
-    _gemm(lib, X, W, N, 0, out2)
+    _gemm(lib, X, W, N, 0, out2, packed)
     assert torch.equal(out, out2)
 
 
+@pytest.mark.parametrize("packed", [False, True], ids=["rowmajor", "packed"])
 @pytest.mark.parametrize("M,N,K", [(16, 256, 128), (256, 4096, 4096), (77, 640, 14336)])
-def test_gemm_residual_epilogue(lib, M, N, K):
+def test_gemm_residual_epilogue(lib, M, N, K, packed):
     g = torch.Generator(device="cuda").manual_seed(3)
     X = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
     W = (torch.randn(N, K, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
     base = torch.randn(M, N, device="cuda", generator=g)
     out = base.clone()
-    assert _gemm(lib, X, W, N, 1, out) == 0
+    assert _gemm(lib, X, W, N, 1, out, packed) == 0
     ref = base.double() + X.double() @ W.double().t()
     assert ((out.double() - ref).abs() <= _bound(X, W) + 1e-6 * ref.abs()).all()
 
 
+@pytest.mark.parametrize("packed", [False, True], ids=["rowmajor", "packed"])
 @pytest.mark.parametrize("M,N,K", [(16, 384, 128), (256, 14336, 4096), (200, 1024, 512)])
-def test_gemm_silu_mul_epilogue(lib, M, N, K):
+def test_gemm_silu_mul_epilogue(lib, M, N, K, packed):
     g = torch.Generator(device="cuda").manual_seed(4)
     X = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
     Wg = (torch.randn(N, K, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
@@ -78,7 +112,7 @@ def test_gemm_silu_mul_epilogue(lib, M, N, K):
     # 64-row block interleave of gate / up rows (srl_ops.h)
     W = torch.stack([Wg.view(N // 64, 64, K), Wu.view(N // 64, 64, K)], dim=1).reshape(2 * N, K).contiguous()
     out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
-    assert _gemm(lib, X, W, N, 2, out) == 0
+    assert _gemm(lib, X, W, N, 2, out, packed) == 0
     gte, up = X.double() @ Wg.double().t(), X.double() @ Wu.double().t()
     ref = gte / (1 + torch.exp(-gte)) * up
     # bf16 output rounding (2^-9 relative) dominates the fp32 accumulation error

@@ -8,12 +8,21 @@ from paper_2603_23414_b200 import _lib
 lib = _lib.load()
 s = torch.cuda.current_stream().cuda_stream
 res = {}
+PACKED = os.environ.get("BENCH_PACKED", "1") == "1"
 def t_gemm(name, M, N, K, epi, nrot=4, it=20):
     rows = 2 * N if epi == 2 else N
     Ws = [(torch.randn(rows, K, device="cuda") * 0.02).to(torch.bfloat16) for _ in range(nrot)]
     X = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     out = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16 if epi == 2 else torch.float32)
     ws = torch.empty(lib.srl_op_gemm_workspace(M, N, K, epi), dtype=torch.uint8, device="cuda")
+    if PACKED:
+        packed = []
+        for Wr in Ws:
+            d = torch.empty(lib.srl_op_packed_weight_bytes(rows, K), dtype=torch.uint8, device="cuda")
+            lib.srl_op_pack_weight(Wr.data_ptr(), rows, K, d.data_ptr(), s)
+            packed.append(d)
+        Ws = packed
+        epi |= 0x100
     for i in range(3):
         lib.srl_op_gemm_bf16(X.data_ptr(), M, Ws[i % nrot].data_ptr(), N, K, epi, out.data_ptr(), ws.data_ptr(), s)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -26,7 +35,7 @@ def t_gemm(name, M, N, K, epi, nrot=4, it=20):
     res[name] = dict(M=M, N=N, K=K, us=ms * 1e3, weight_GBs=gbs, TFs=2 * M * rows * K / (ms * 1e-3) / 1e12)
     print(name, json.dumps(res[name]), flush=True)
 
-for M in (256, 128, 64, 16):
+for M in map(int, os.environ.get("BENCH_M", "256,128,64,16").split(",")):
     t_gemm(f"qkv_M{M}", M, 6144, 4096, 0)
     t_gemm(f"o_M{M}", M, 4096, 4096, 1)
     t_gemm(f"gu_M{M}", M, 14336, 4096, 2)

@@ -16,7 +16,7 @@ from paper_2603_23414_b200 import _lib
 lib = _lib.load()
 lib.srl_debug_gemm_timestamps.argtypes = [ctypes.c_void_p, ctypes.c_int32]
 NAMES = ["start", "setup", "tma0", "tma_done", "mma0", "mma_done", "e_full0", "e_full1", "e_full2", "e_done0",
-         "e_done1", "e_done2", "end", "fix_start", "fix_end"]
+         "e_done1", "e_done2", "end", "ep_start", "ep_bar", "ep_stored"]
 
 
 def report(title, dbg):
@@ -36,6 +36,14 @@ def report(title, dbg):
         if np.all(np.isnan(col)):
             continue
         print(f"  {nme:10s} min {np.nanmin(col):8.2f} med {np.nanmedian(col):8.2f} max {np.nanmax(col):8.2f}")
+    iss, arr = r[:, 16:112], r[:, 112:208]
+    if not np.all(np.isnan(iss)):
+        lat = arr - iss
+        print("  q: median W issue / arrival / latency (us)")
+        for q in list(range(0, 16)) + list(range(16, 96, 8)):
+            if np.all(np.isnan(lat[:, q])):
+                continue
+            print(f"    {q:3d} {np.nanmedian(iss[:, q]):8.2f} {np.nanmedian(arr[:, q]):8.2f} {np.nanmedian(lat[:, q]):7.2f}")
 
 
 def op(M, N, K, epi):
