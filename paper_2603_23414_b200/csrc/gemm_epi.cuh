@@ -16,7 +16,7 @@ __device__ __forceinline__ void epi_bar(int id) { asm volatile("bar.sync %0, %1;
 __device__ __forceinline__ float silu_mul(float g, float u) { return __fdividef(g, 1.f + __expf(-g)) * u; }
 
 constexpr int kXchPitch = 132;                   // floats per staged batch row (128 + 4: conflict-free)
-constexpr int kXchFloats = 16 * kXchPitch + 64;  // staged chunk + 32 ints (QKV position / page lookups)
+constexpr int kXchFloats = 16 * kXchPitch;  // one staged 16-column chunk
 
 __device__ __forceinline__ void store16_bf16(__nv_bfloat16* dst, const float (&y)[16]) {
   uint4 a, b;
@@ -36,23 +36,40 @@ __device__ __forceinline__ void store16_f32(float* dst, const float (&y)[16]) {
   for (int q = 0; q < 4; ++q) reinterpret_cast<float4*>(dst)[q] = make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
 }
 
+// vector reduction into global memory (fire-and-forget; .ftz: denormals flush)
+__device__ __forceinline__ void red_add_f4(float* dst, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
+// EPI_QKV: (position, KV page) of each batch row of a unit, looked up once per
+// unit into shared memory by the 256 epilogue threads (named barrier 3) so the
+// per-chunk epilogue does no dependent global loads.  tab[0..m_blk) positions
+// (-1 past M), tab[256..256+m_blk) pages.
+constexpr int kRowTab = 512;
+__device__ __forceinline__ void fill_row_table(const GemmParams& p, int m_base, int ncol, int* tab, int t) {
+  const GemmEpi& e = p.epi;
+  if (e.kind != EPI_QKV) return;
+  asm volatile("bar.sync 3, 256;" ::: "memory");  // previous unit's epilogue is done with the table
+  for (int r = t; r < ncol; r += 256) {
+    const int m = m_base + r;
+    const int pos = m < p.M ? __ldg(e.row_pos + m) : -1;
+    tab[r] = pos;
+    tab[256 + r] = pos >= 0 ? __ldg(e.page_table + (size_t)__ldg(e.row_slot + m) * e.max_pages + pos / 64) : 0;
+  }
+  asm volatile("bar.sync 3, 256;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- fused epilogue
 // v[j]: value of weight row unit_n0 + n for batch row m0 + j, j < 16.
-// xch: this group's shared staging buffer (kXchFloats); bar: its named barrier.
+// xch: this group's shared staging buffer (kXchFloats); bar: its named barrier;
+// rtab: the unit's row table (fill_row_table) advanced to row m0.
 __device__ __forceinline__ void apply_epilogue(const GemmParams& p, int unit_n0, int n, int m0, const float (&v)[16],
-                                               float* xch, int bar) {
+                                               float* xch, int bar, const int* rtab) {
   const GemmEpi& e = p.epi;
-  int* spos = reinterpret_cast<int*>(xch + 16 * kXchPitch);
-  int* spage = spos + 16;
+  const int* spos = rtab;
+  const int* spage = rtab + 256;
 #pragma unroll
   for (int j = 0; j < 16; ++j) xch[j * kXchPitch + n] = v[j];
-  if (e.kind == EPI_QKV && n < 16) {
-    // the chunk's 16 (position, KV page) pairs, looked up once
-    const int m = m0 + n;
-    const int pos = m < p.M ? __ldg(e.row_pos + m) : -1;
-    spos[n] = pos;
-    spage[n] = pos >= 0 ? __ldg(e.page_table + (size_t)__ldg(e.row_slot + m) * e.max_pages + pos / 64) : 0;
-  }
   epi_bar(bar);
   const int ml = n >> 3;  // batch row within the chunk owned from here on
   const int m = m0 + ml;
@@ -102,18 +119,12 @@ __device__ __forceinline__ void apply_epilogue(const GemmParams& p, int unit_n0,
           break;
         }
         case EPI_RESID: {
-          // exactly one writer per element per launch: plain vector read-modify-write
+          // exactly one contribution per element per launch, so a fire-and-forget
+          // vector reduction equals the read-modify-write without its read latency
           float* dst = e.x_res + (size_t)m * e.ldo + ng0;
           if (full) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              float4 x = reinterpret_cast<float4*>(dst)[q];
-              x.x += r[4 * q];
-              x.y += r[4 * q + 1];
-              x.z += r[4 * q + 2];
-              x.w += r[4 * q + 3];
-              reinterpret_cast<float4*>(dst)[q] = x;
-            }
+            for (int q = 0; q < 4; ++q) red_add_f4(dst + 4 * q, r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
           } else {
 #pragma unroll
             for (int k = 0; k < 16; ++k)

@@ -1,0 +1,328 @@
+// gemm_pair.cuh — the decode GEMM on CTA pairs (tcgen05 cta_group::2), included
+// by gemm_tc.cu after the single-CTA kernel (shares GemmParams, the epilogues
+// and the cluster helpers).
+//
+// Why pairs: at a wide decode batch (M_b = 256) one SM streaming a 128-row weight
+// tile must also stage the whole 256-row activation slice and feed both to the
+// tensor core; shared-memory traffic per k-block (TMA writes + UMMA operand
+// reads, ~96 KB) then bounds the mainloop, not HBM.  With cta_group::2 two SMs
+// of a TPC run one M = 256 MMA: each holds 128 weight rows (A) and HALF of the
+// activation rows (B), and the pair shares B, so per-SM staging and operand
+// traffic drop by a third and each SM's W stream runs at the tensor rate.
+//
+// Pair unit = 256 weight rows (CTA r2 of the pair owns rows 128*r2..+127) x one
+// <= 256-row batch block.  The leader CTA (even cluster rank) issues the MMAs;
+// both CTAs' TMA loads signal the leader's "full" barriers (.cta_group::2); the
+// leader's commits multicast "empty" / "tfull" arrivals to both CTAs; both
+// CTAs' epilogue warps arrive on the leader's "tempty".  Each CTA's TMEM holds
+// its 128 rows x N accumulator and it runs the same fused epilogues.
+//
+// Decomposition: persistent pairs over pair units when there are enough units;
+// otherwise split-K over the S pairs of a (2S)-CTA cluster, with a push-style
+// reduction: every CTA sends each 16-column chunk of its partial to the CTA
+// (same row half) that owns the chunk, straight into that CTA's shared memory
+// (st.shared::cluster), and the owner sums the S partials in pair (= k) order
+// from local memory: fire-and-forget remote stores instead of remote loads.
+
+SRL_DEV uint32_t mapa_u32(uint32_t local_addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_addr), "r"(rank));
+  return r;
+}
+SRL_DEV void st_dsmem_f4(uint32_t cluster_addr, float4 v) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(cluster_addr), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+SRL_DEV void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+SRL_DEV void mbar_expect_tx_only(uint64_t* bar, uint32_t tx) { mbar_arrive_expect_tx(bar, tx); }
+// 2-D TMA load into this CTA's shared memory whose completion is counted on the
+// pair leader's mbarrier (cluster address)
+SRL_DEV void tma_load_2d_pair(void* dst, const CUtensorMap* m, uint32_t bar_cluster, int c0, int c1, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+SRL_DEV void tc_mma_bf16_pair(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(desc_a), "l"(desc_b), "r"(idesc), "r"(accumulate));
+}
+SRL_DEV void tc_commit_pair(uint64_t* bar, uint16_t cta_mask) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "h"(cta_mask)
+               : "memory");
+}
+SRL_DEV void tmem_alloc_pair(uint32_t* holder, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(holder)),
+               "r"(ncols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+}
+SRL_DEV void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
+}
+
+// pair unit u -> (pair tile, batch block); pair tile t covers weight rows 256t..256t+255
+template <int SPLIT>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int stage_b = (p.m_blk >> 1) * 128;  // this CTA's half of the activation slice
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + p.stages * kStageA;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + p.xstages * stage_b);
+  uint64_t* empty = full + p.stages;
+  uint64_t* xfull = empty + p.stages;
+  uint64_t* xempty = xfull + p.xstages;
+  uint64_t* tfull = xempty + p.xstages;  // [2]
+  uint64_t* tempty = tfull + 2;          // [2]
+  uint32_t* tholder = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* xch = reinterpret_cast<float*>(tholder + 4);  // [2 groups][kXchFloats]
+  int* rtab = reinterpret_cast<int*>(xch + 2 * kXchFloats);  // [kRowTab] (QKV row table)
+  float* red = reinterpret_cast<float*>(smem);         // SPLIT: received partials, reuses the rings
+
+  const int w = warp_id(), lane = lane_id();
+  const uint32_t rank = cluster_rank();
+  const uint32_t r2 = rank & 1u, leader = rank & ~1u;
+  const uint16_t pair_mask = (uint16_t)(3u << leader);
+  const bool is_leader = r2 == 0;
+  // units: SPLIT -> cluster id (one unit per cluster, pair index = k split);
+  //        else  -> pair id, round-robin over pair units
+  const int npairs = gridDim.x >> 1;
+  const int pid = blockIdx.x >> 1;
+  const int cl = SPLIT ? (int)(blockIdx.x / (2 * p.S)) : 0;
+  const int pi = SPLIT ? (int)(rank >> 1) : 0;
+  const int nseg = SPLIT ? 1 : (pid < p.units ? (p.units - pid + npairs - 1) / npairs : 0);
+  auto unit_of = [&](int i) { return SPLIT ? cl : pid + i * npairs; };
+  const int k0 = SPLIT ? pi * p.kb / p.S : 0, k1 = SPLIT ? (pi + 1) * p.kb / p.S : p.kb;
+
+  if (threadIdx.x == 0) {
+    DBG(0);
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < p.xstages; ++s) {
+      mbar_init(&xfull[s], 1);
+      mbar_init(&xempty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 16);  // 8 epilogue warps x 2 CTAs (the leader's copy is used)
+    }
+    fence_barrier_init();
+    tma_prefetch(&tmW);
+    tma_prefetch(&tmX);
+  }
+  if (w == 1) tmem_alloc_pair(tholder, p.tmem_cols);
+  tc_fence_before();
+  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
+  tc_fence_after();
+  const uint32_t tbase = *tholder;
+  if (threadIdx.x == 0) DBG(1);
+
+  if (w == 0) {
+    if (lane == 0) {
+      const uint64_t pol_w = policy_evict_first();
+      const uint32_t full_l = mapa_u32(smem_u32(full), leader);
+      int s = 0;
+      uint32_t ph = 1;
+      bool first = true;
+      for (int i = 0; i < nseg; ++i) {
+        const int u = unit_of(i);
+        const int t128 = (u % p.n_tiles) * 2 + (int)r2;  // this CTA's 128-row tile
+        for (int k = k0; k < k1; ++k) {
+          mbar_wait(&empty[s], ph);
+          if (is_leader) mbar_arrive_expect_tx(&full[s], 2 * kStageA);  // both CTAs' halves
+          const int c1 = p.wp ? (t128 * p.kb + k) * 128 : t128 * 128;
+          const int c0 = p.wp ? 0 : k * 64;
+          tma_load_2d_pair(sA + s * kStageA, &tmW, full_l + 8u * s, c0, c1, pol_w);
+          if (first) {
+            DBG(2);
+            first = false;
+          }
+          if (++s == p.stages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+      DBG(3);
+    }
+  } else if (w == 10) {
+    if (lane == 0) {
+      const uint64_t pol_x = policy_evict_last();
+      const uint32_t xfull_l = mapa_u32(smem_u32(xfull), leader);
+      int s = 0;
+      uint32_t ph = 1;
+      for (int i = 0; i < nseg; ++i) {
+        const int u = unit_of(i);
+        const int ncol = unit_cols(p, u);
+        const int mrow = (u / p.n_tiles) * p.m_blk + (int)r2 * (ncol >> 1);
+        for (int k = k0; k < k1; ++k) {
+          mbar_wait(&xempty[s], ph);
+          if (is_leader) mbar_arrive_expect_tx(&xfull[s], 2 * stage_b);
+          tma_load_2d_pair(sB + s * stage_b, &tmX, xfull_l + 8u * s, k * 64, mrow, pol_x);
+          if (++s == p.xstages) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (w == 1) {
+    if (lane == 0 && is_leader) {
+      const uint64_t da0 = umma_desc_sw128(smem_u32(sA)), db0 = umma_desc_sw128(smem_u32(sB));
+      const uint32_t sa16 = (uint32_t)kStageA >> 4, sb16 = (uint32_t)stage_b >> 4;
+      int s = 0, sx = 0;
+      uint32_t ph = 0, phx = 0;
+      bool first = true;
+      for (int i = 0; i < nseg; ++i) {
+        const int u = unit_of(i);
+        const uint32_t idesc = umma_idesc_bf16(256, unit_cols(p, u));
+        const int a = i % p.acc_stages;
+        mbar_wait(&tempty[a], ((i / p.acc_stages) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tacc = tbase + (uint32_t)(a * p.m_blk);
+        uint32_t acc = 0;
+        for (int k = k0; k < k1; ++k) {
+          mbar_wait(&full[s], ph);
+          mbar_wait(&xfull[sx], phx);
+          tc_fence_after();
+          const uint64_t da = da0 + (uint64_t)(s * sa16), db = db0 + (uint64_t)(sx * sb16);
+          tc_mma_bf16_pair(tacc, da, db, idesc, acc);
+          tc_mma_bf16_pair(tacc, da + 2, db + 2, idesc, 1u);
+          tc_mma_bf16_pair(tacc, da + 4, db + 4, idesc, 1u);
+          tc_mma_bf16_pair(tacc, da + 6, db + 6, idesc, 1u);
+          acc = 1;
+          tc_commit_pair(&empty[s], pair_mask);  // frees both CTAs' slots once the MMAs retire
+          tc_commit_pair(&xempty[sx], pair_mask);
+          if (first) {
+            DBG(4);
+            first = false;
+          }
+          if (++s == p.stages) {
+            s = 0;
+            ph ^= 1;
+          }
+          if (++sx == p.xstages) {
+            sx = 0;
+            phx ^= 1;
+          }
+        }
+        tc_commit_pair(&tfull[a], pair_mask);
+      }
+      DBG(5);
+    }
+    __syncwarp();
+  } else if (!SPLIT) {
+    // ------------------------------ epilogue warps (2..9): TMEM -> fused op
+    const int qw = w & 3, n = qw * 32 + lane, eg = (w - 2) >> 2;
+    float* xg = xch + eg * kXchFloats;
+    const uint32_t tempty_l = mapa_u32(smem_u32(tempty), leader);
+    for (int i = 0; i < nseg; ++i) {
+      const int u = unit_of(i);
+      const int unit_n0 = (u % p.n_tiles) * 256 + (int)r2 * 128, m_base = (u / p.n_tiles) * p.m_blk;
+      const int ncol = unit_cols(p, u);
+      const int a = i % p.acc_stages;
+      fill_row_table(p, m_base, ncol, rtab, (int)threadIdx.x - 64);  // overlaps the MMAs
+      mbar_wait(&tfull[a], (i / p.acc_stages) & 1);
+      tc_fence_after();
+      if (lane == 0 && qw == 0 && i < 3) DBG(6 + i);
+      if (unit_n0 < p.N) {
+        const uint32_t tl = tbase + ((uint32_t)(qw * 32) << 16) + (uint32_t)(a * p.m_blk);
+        for (int cc = eg * 16; cc < ncol; cc += 32) {
+          float v[16];
+          tmem_ld16(tl + cc, v);
+          apply_epilogue(p, unit_n0, n, m_base + cc, v, xg, 1 + eg, rtab + cc);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_l + 8u * a);
+      if (lane == 0 && qw == 0 && i < 3) DBG(9 + i);
+    }
+  }
+
+  if (SPLIT) {
+    // ------------------------------ split-K reduction: push partials to chunk owners
+    const int u = cl;
+    const int unit_n0 = (u % p.n_tiles) * 256 + (int)r2 * 128, m_base = (u / p.n_tiles) * p.m_blk;
+    const int ncol = unit_cols(p, u), nchunk = ncol >> 4;
+    const int cpr = ((p.m_blk >> 4) + p.S - 1) / p.S;  // receive slots per source pair
+    const bool epi = w >= 2 && w <= 9;
+    const int qw = w & 3, n = qw * 32 + lane, eg = (w - 2) >> 2;
+    float* xg = xch + eg * kXchFloats;
+    if (epi) {
+      fill_row_table(p, m_base, ncol, rtab, (int)threadIdx.x - 64);
+      mbar_wait(&tfull[0], 0);
+      tc_fence_after();
+      if (lane == 0 && qw == 0) DBG(6);
+    }
+    cluster_sync_all();  // every CTA's mainloop is done: all rings may be overwritten
+    if (threadIdx.x == 0) DBG(13);
+    if (epi) {
+      const uint32_t tl = tbase + ((uint32_t)(qw * 32) << 16);
+      const uint32_t red_u32 = smem_u32(red);
+      // chunk c is owned by pair j = the largest j with j * nchunk / S <= c
+      auto push = [&](int c, const float (&v)[16]) {
+        int j = (c * p.S) / nchunk;
+        while (j + 1 < p.S && (j + 1) * nchunk / p.S <= c) ++j;
+        while (j > 0 && j * nchunk / p.S > c) --j;
+        const int cl0 = j * nchunk / p.S;
+        const uint32_t dst = mapa_u32(red_u32, (uint32_t)(2 * j) + r2) +
+                             (uint32_t)((((pi * cpr + (c - cl0)) * 4) * 128 + n) * 16);
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4)
+          st_dsmem_f4(dst + (uint32_t)(q4 * 2048), make_float4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]));
+      };
+      int c = eg;
+      for (; c + 2 < nchunk; c += 4) {  // two TMEM loads in flight per wait
+        float va[16], vb[16];
+        tmem_ld16x2(tl + (uint32_t)(c * 16), tl + (uint32_t)((c + 2) * 16), va, vb);
+        push(c, va);
+        push(c + 2, vb);
+      }
+      for (; c < nchunk; c += 2) {
+        float v[16];
+        tmem_ld16(tl + (uint32_t)(c * 16), v);
+        push(c, v);
+      }
+    }
+    cluster_sync_all();  // all partials delivered
+    if (threadIdx.x == 0) DBG(14);
+    if (epi && unit_n0 < p.N) {
+      const int c0 = pi * nchunk / p.S, c1 = (pi + 1) * nchunk / p.S;
+      for (int c = c0 + eg; c < c1; c += 2) {
+        float v[16];
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) v[jj] = 0.f;
+        for (int src = 0; src < p.S; ++src) {  // pair order = k order: deterministic
+          const float4* b = reinterpret_cast<const float4*>(red + (size_t)((src * cpr + (c - c0)) * 4) * 512) + n;
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const float4 x = b[q4 * 128];
+            v[4 * q4] += x.x;
+            v[4 * q4 + 1] += x.y;
+            v[4 * q4 + 2] += x.z;
+            v[4 * q4 + 3] += x.w;
+          }
+        }
+        apply_epilogue(p, unit_n0, n, m_base + c * 16, v, xg, 1 + eg, rtab + c * 16);
+      }
+      if (w == 2 && lane == 0) DBG(15);
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();  // both CTAs done with the pair's TMEM before it is freed
+  if (threadIdx.x == 0) DBG(12);
+  if (w == 1) tmem_dealloc_pair(tbase, p.tmem_cols);
+}

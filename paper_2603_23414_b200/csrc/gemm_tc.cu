@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tempty = tfull + 2;          // [2]
   uint32_t* tholder = reinterpret_cast<uint32_t*>(tempty + 2);
   float* xch = reinterpret_cast<float*>(tholder + 4);  // [2 groups][kXchFloats]
+  int* rtab = reinterpret_cast<int*>(xch + 2 * kXchFloats);  // [kRowTab] (QKV row table)
   float* red = reinterpret_cast<float*>(smem);         // SPLIT: this CTA's partial, reuses the rings
 
   const int w = warp_id(), lane = lane_id();
@@ -304,6 +305,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int t = sg.u % p.n_tiles, m_base = (sg.u / p.n_tiles) * p.m_blk;
       const int ncol = unit_cols(p, sg.u), nh = halves_valid(p, sg.u);
       const int a = i % p.acc_stages;
+      fill_row_table(p, m_base, ncol, rtab, (int)threadIdx.x - 64);  // overlaps the MMAs
       mbar_wait(&tfull[a], (i / p.acc_stages) & 1);
       tc_fence_after();
       if (lane == 0 && qw == 0 && i < 3) DBG(6 + i);
@@ -312,7 +314,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int cc = eg * 16; cc < ncol; cc += 32) {
           float v[16];
           tmem_ld16(tl + cc, v);
-          apply_epilogue(p, (t * p.H + h) * 128, n, m_base + cc, v, xg, 1 + eg);
+          apply_epilogue(p, (t * p.H + h) * 128, n, m_base + cc, v, xg, 1 + eg, rtab + cc);
         }
       }
       tc_fence_before();
@@ -335,6 +337,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     float* xg = xch + eg * kXchFloats;
     const uint32_t red_u32 = smem_u32(red);
     if (epi) {
+      fill_row_table(p, m_base, ncol, rtab, (int)threadIdx.x - 64);
       mbar_wait(&tfull[0], 0);
       tc_fence_after();
       if (lane == 0 && qw == 0) DBG(6);
@@ -387,7 +390,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                   v[4 * q4 + 3] += x[rr][q4].w;
                 }
           }
-          apply_epilogue(p, (t * p.H + h0 + hl) * 128, n, m_base + ci * 16, v, xg, 1 + eg);
+          apply_epilogue(p, (t * p.H + h0 + hl) * 128, n, m_base + ci * 16, v, xg, 1 + eg, rtab + ci * 16);
         }
         if (w == 2 && lane == 0) DBG(14);
       }
@@ -399,6 +402,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (threadIdx.x == 0) DBG(12);
   if (w == 1) tmem_dealloc(tbase, p.tmem_cols);
 }
+
+#include "gemm_pair.cuh"
 
 // debug hook: when set, the target-th gemm launch records per-CTA phase timestamps
 static unsigned long long* g_dbg = nullptr;
@@ -415,30 +420,129 @@ static int pick_mblk(int M) {
   return (mb + 15) & ~15;
 }
 
-// co-resident clusters of S GEMM CTAs (1 CTA per SM), queried once per S
-static int max_clusters(int S) {
-  static int cache[9] = {0};
-  if (cache[S] == 0) {
+// co-resident clusters of `size` GEMM CTAs (1 CTA per SM), queried once per size
+template <class Kern>
+static int max_clusters_of(Kern kern, int size, int* cache) {
+  if (cache[size] == 0) {
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(S * 64);
+    cfg.gridDim = dim3(size * 64);
     cfg.blockDim = dim3(kGemmThreads);
     cfg.dynamicSmemBytes = 190 * 1024;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = S;
+    attr[0].val.clusterDim.x = size;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int n = 0;
-    cudaFuncSetAttribute(gemm_bf16_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (cudaOccupancyMaxActiveClusters(&n, gemm_bf16_tc_kernel<1>, &cfg) != cudaSuccess || n <= 0) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
       cudaGetLastError();
       n = 1;
     }
-    cache[S] = n;
+    cache[size] = n;
   }
-  return cache[S];
+  return cache[size];
+}
+static int max_clusters(int S) {
+  static int cache[17] = {0};
+  return max_clusters_of(gemm_bf16_tc_kernel<1>, S, cache);
+}
+static int max_clusters_pair(int size) {
+  static int cache[17] = {0};
+  return max_clusters_of(gemm_pair_kernel<1>, size, cache);
+}
+
+static int launch_cluster(void (*kern)(const CUtensorMap, const CUtensorMap, GemmParams), int grid, int csize,
+                          size_t smem, cudaStream_t stream, const CUtensorMap& tmW, const CUtensorMap& tmX,
+                          const GemmParams& p) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = csize;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, tmW, tmX, p) == cudaSuccess ? 0 : -3;
+}
+
+// CTA-pair variant (gemm_pair.cuh) for wide batches; returns 1 when not applicable
+static int gemm_pair_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N, int K, const GemmEpi& epi,
+                           int num_sms, cudaStream_t stream) {
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.m_blk = pick_mblk(M);
+  p.m_blocks = (M + p.m_blk - 1) / p.m_blk;
+  p.H = 1;
+  p.n_tiles = (N + 255) / 256;  // pair tiles
+  p.kb = K / 64;
+  p.units = p.n_tiles * p.m_blocks;
+  p.epi = epi;
+  p.dbg = (g_dbg && g_dbg_count++ == g_dbg_target) ? g_dbg : nullptr;
+  const int pairs = num_sms / 2;
+  int S = 1;
+  if (p.units < pairs) {
+    S = pairs / p.units;
+    if (S > 4) S = 4;
+    if (S > p.kb) S = p.kb;
+    while (S > 1 && p.units > max_clusters_pair(2 * S)) --S;
+  }
+  p.S = S;
+  const int stage_b = (p.m_blk >> 1) * 128;
+  const int budget = 200 * 1024;
+  int xstages = stage_b <= 4096 ? 8 : (stage_b <= 8192 ? 6 : 4);
+  int stages = (budget - xstages * stage_b) / kStageA;
+  if (stages > 12) stages = 12;
+  p.stages = stages;
+  p.xstages = xstages;
+  const size_t rings = (size_t)stages * kStageA + (size_t)xstages * stage_b;
+  if (S > 1) {
+    const int cpr = ((p.m_blk >> 4) + S - 1) / S;
+    if ((size_t)S * cpr * 8192 > rings) return 1;
+  }
+  p.acc_stages = (S == 1 && 2 * p.m_blk <= 512) ? 2 : 1;
+  int tc = 32;
+  while (tc < p.m_blk * p.acc_stages) tc <<= 1;
+  p.tmem_cols = tc;
+  CUtensorMap tmW, tmX;
+  if (epi.w_packed) {
+    // the packed image viewed as [blocks * 128 rows, 64 cols]: one box = one 16 KB block
+    p.wp = reinterpret_cast<const uint8_t*>(W);
+    const uint64_t rows = (uint64_t)((N + 127) / 128) * p.kb * 128;
+    if (tma_encode_2d(&tmW, W, rows, 64, 128, 128, 64, 2, false)) return -2;
+  } else if (tma_encode_2d(&tmW, W, N, K, (uint64_t)K * 2, 128, 64, 2, true)) {
+    return -2;
+  }
+  if (tma_encode_2d(&tmX, X, M, K, (uint64_t)K * 2, p.m_blk >> 1, 64, 2, true)) return -2;
+  const size_t smem = 1024 + rings + (2 * stages + 2 * xstages + 4) * 8 + 16 + 2 * kXchFloats * 4 + kRowTab * 4;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gemm_pair_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(gemm_pair_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr_set = true;
+  }
+  static const bool verbose = getenv("SRL_GEMM_VERBOSE") != nullptr;
+  if (verbose)
+    fprintf(stderr, "gemm(pair) M=%d N=%d K=%d units=%d S=%d stages=%d/%d smem=%zu\n", M, N, K, p.units, S, stages,
+            xstages, smem);
+  int rc;
+  if (S == 1) {
+    const int np = p.units < pairs ? p.units : pairs;
+    rc = launch_cluster(gemm_pair_kernel<0>, 2 * np, 2, smem, stream, tmW, tmX, p);
+  } else {
+    rc = launch_cluster(gemm_pair_kernel<1>, p.units * 2 * S, 2 * S, smem, stream, tmW, tmX, p);
+  }
+  if (rc) cudaGetLastError();
+  return rc;
 }
 
 int gemm_bf16_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N, int K, const GemmEpi& epi,
@@ -446,6 +550,12 @@ int gemm_bf16_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N
   if (M <= 0 || N <= 0) return 0;
   if (K % 64 != 0) return -1;
   if (epi.kind == EPI_SILU && N % 128 != 0) return -1;  // N counts interleaved gate/up rows
+  static const int pair_env = getenv("SRL_GEMM_PAIR") ? atoi(getenv("SRL_GEMM_PAIR")) : -1;
+  const bool pair = pair_env >= 0 ? pair_env > 0 : M >= 128;
+  if (pair) {
+    const int r = gemm_pair_fused(X, M, W, N, K, epi, num_sms, stream);
+    if (r <= 0) return r;
+  }
   GemmParams p;
   memset(&p, 0, sizeof(p));
   p.M = M;
@@ -503,7 +613,7 @@ int gemm_bf16_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N
     return -2;
   }
   if (tma_encode_2d(&tmX, X, M, K, (uint64_t)K * 2, p.m_blk, 64, 2, true)) return -2;
-  const size_t smem = 1024 + rings + (2 * stages + 2 * xstages + 4) * 8 + 16 + 2 * kXchFloats * 4;
+  const size_t smem = 1024 + rings + (2 * stages + 2 * xstages + 4) * 8 + 16 + 2 * kXchFloats * 4 + kRowTab * 4;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(gemm_bf16_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);

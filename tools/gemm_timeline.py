@@ -16,7 +16,7 @@ from paper_2603_23414_b200 import _lib
 lib = _lib.load()
 lib.srl_debug_gemm_timestamps.argtypes = [ctypes.c_void_p, ctypes.c_int32]
 NAMES = ["start", "setup", "tma0", "tma_done", "mma0", "mma_done", "e_full0", "e_full1", "e_full2", "e_done0",
-         "e_done1", "e_done2", "end", "ep_start", "ep_bar", "ep_stored"]
+         "e_done1", "e_done2", "end", "csync1", "pushed", "reduced"]
 
 
 def report(title, dbg):
