@@ -38,24 +38,40 @@ from workload.lengths import LengthModel, sample_lengths  # noqa: E402
 from workload.prompts import make_prompts  # noqa: E402
 
 METRIC = "rollout tokens/s + bubble ratio @1/2/4/8 B200; decode %HBM roofline"
-WORKLOAD = ("cfg2: LLaMA-3.1-8B-shaped random-init bf16 policy, 1 GPU per replica, rollout batch Q_g=256, "
-            "max 8192 new tokens, update group U=64, K=inf (partial), pool 1024 prompts x 2 epochs, "
-            "256-token prompts, FORCED lognormal(1600,0.55)+3%-at-cap lengths, TRAINED barrier, KEEP_KV")
+WORKLOAD = ("cfg2: LLaMA-3.1-8B-shaped random-init bf16 policy, rollout batch Q_g=256 per GPU, "
+            "max 8192 new tokens, update group U=64, K=inf (partial), pool 1024 prompts per GPU x 2 epochs, "
+            "256-token prompts, FORCED lognormal(1600,0.55)+3%-at-cap lengths, TRAINED barrier, KEEP_KV; "
+            "N>1: lockstep replicas (global slots g=s*N+r, per-step all-gather of sampled rows, "
+            "weight broadcast after every update group)")
 N_PROMPTS_PER_EPOCH = 1024
 PROMPT_LEN = 256
 
 
-def cfg2_sched():
-    return SchedConfig(Q_g=256, R=1, U=64, K=K_INF, pool_prompts=N_PROMPTS_PER_EPOCH, G=1, cap=8192, page_tokens=64,
+def cfg2_sched(world=1):
+    return SchedConfig(Q_g=256, R=world, U=64, K=K_INF, pool_prompts=N_PROMPTS_PER_EPOCH * world, G=1, cap=8192,
+                       page_tokens=64,
                        kv_pages=11000, mode=MODE_SORTED, resume=RESUME_KEEP_KV, barrier=BARRIER_TRAINED,
                        stop=STOP_FORCED, kv_dtype=KV_BF16, temperature=1.0, sample_seed=3)
 
 
-def workload_inputs(rank=0, epochs=2):
-    n = N_PROMPTS_PER_EPOCH * epochs
-    off, toks = make_prompts(1 + 1000 * rank, n, LLAMA8B.V, PROMPT_LEN)
-    L = sample_lengths(LengthModel(median=1600, sigma=0.55, tail=0.03, floor=1, cap=8192), 0 + 1000 * rank, n)
+def workload_inputs(world=1, epochs=2):
+    """The prompt stream every replica submits (identical on all ranks; the replicated
+    pending queue shards it over the global slots)."""
+    n = N_PROMPTS_PER_EPOCH * world * epochs
+    off, toks = make_prompts(1, n, LLAMA8B.V, PROMPT_LEN)
+    L = sample_lengths(LengthModel(median=1600, sigma=0.55, tail=0.03, floor=1, cap=8192), 0, n)
     return off, toks, L
+
+
+def aggregate_over_ranks(dist, raw, useful, ms, device="cuda"):
+    """Whole-job rates: tokens of all ranks / the slowest rank's device time."""
+    import torch
+    t = torch.tensor([raw, useful, ms], dtype=torch.float64, device=device)
+    tot = t.clone()
+    dist.all_reduce(tot)
+    mx = t.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    return tot[0].item() / (mx[2].item() * 1e-3), tot[1].item() / (mx[2].item() * 1e-3), mx[2].item()
 
 
 def load_peaks():
@@ -131,13 +147,23 @@ def run_gpu(args, rank, world, dist):
     from workload.weights import fill_engine_weights
     torch.cuda.set_device(rank % max(1, torch.cuda.device_count()))
     dev = torch.cuda.current_device()
-    model, sched = LLAMA8B, cfg2_sched()
-    off, toks, L = workload_inputs(rank)
-    ids = np.arange(len(off) - 1, dtype=np.uint64) + 1 + 10_000_000 * rank
-    eng = RolloutEngine(model, sched, max_traj=2 * N_PROMPTS_PER_EPOCH, max_prompt=PROMPT_LEN, prefill_chunk=4096,
-                        device=dev)
+    from paper_2603_23414_b200.engine import share_nccl_unique_id
+    model, sched = LLAMA8B, cfg2_sched(world)
+    off, toks, L = workload_inputs(world)
+    ids = np.arange(len(off) - 1, dtype=np.uint64) + 1
+    max_traj = 2 * N_PROMPTS_PER_EPOCH * world
+
+    def new_engine():
+        rep = {}
+        if world > 1:
+            rep = dict(rank=rank, world=world, nccl_id=share_nccl_unique_id(dist, rank))
+        return RolloutEngine(model, sched, max_traj=max_traj, max_prompt=PROMPT_LEN, prefill_chunk=4096, device=dev,
+                             **rep)
+    eng = new_engine()
     fill_engine_weights(eng, model, 0)
-    trainer = eng.W.clone()          # the trainer's copy of the refreshed policy (K13: same bytes re-emitted)
+    # the trainer's copy of the refreshed policy on rank 0 (K13: the same bytes are
+    # re-emitted); the other replicas receive it through the engine's broadcast
+    trainer = eng.W.clone() if rank == 0 else None
     eng.load_policy_weights(0)
     torch.cuda.synchronize()
 
@@ -150,7 +176,8 @@ def run_gpu(args, rank, world, dist):
             if info.k >= 0:
                 done += 1
                 if stats is not None:
-                    stats.append((info.r_k, info.sum_ctx, info.dt_ms, info.n_prefill_tokens, info.n_finished))
+                    stats.append((info.r_k, info.sum_ctx, info.dt_ms, info.n_prefill_tokens, info.n_finished,
+                                  info.r_local))
             if st == GROUP_READY:
                 h = eng.harvest_finished(cap_recs=2048, cap_toks=2048 * sched.cap)
                 state["useful"] += sum(r["len"] for r in h.records)
@@ -193,11 +220,11 @@ def run_gpu(args, rank, world, dist):
     # ---------------- e2e: same window through the C ABI with host buffers
     e2e = None
     if not args.no_e2e:
-        eng = RolloutEngine(model, sched, max_traj=2 * N_PROMPTS_PER_EPOCH, max_prompt=PROMPT_LEN,
-                            prefill_chunk=4096, device=dev)
-        eng.W.copy_(trainer)
+        eng = new_engine()
+        if trainer is not None:
+            eng.W.copy_(trainer)
         eng.load_policy_weights(0)
-        n0 = N_PROMPTS_PER_EPOCH
+        n0 = N_PROMPTS_PER_EPOCH * world
         eng.submit_prompts(ids[:n0], off[:n0 + 1], toks[:off[n0]], L[:n0])
         st2 = {"useful": 0, "d2h": 0, "v": 0}
         drive(eng, args.precondition + args.warmup, st2)
@@ -345,25 +372,20 @@ def main():
                 "frac": achieved / hbm, "traffic": None, "launches": dec[dom][1], "peak_source": peak_src}
     # decode roofline fraction of the whole step
     t_roof = 0.0
-    for (rk, sc, dt, npre, nfin) in r["stats"]:
-        B, F, _, _ = step_bytes_flops(m, rk, sc)
+    for (rk, sc, dt, npre, nfin, rl) in r["stats"]:
+        B, F, _, _ = step_bytes_flops(m, rl, sc)             # this GPU's rows and context
         t_roof += max(B / (hbm * 1e9), F / (tf_sust * 1e12))
     dec_frac = t_roof / (r["ms"] * 1e-3)
     tok_s = r["raw"] / (r["ms"] * 1e-3)
-    Q = 256
+    Q = 256 * world                                          # Q_tot (reading R1)
     bubble = sum(Q - s[0] for s in r["stats"]) / (Q * max(1, len(r["stats"])))
     dts = [s[2] for s in r["stats"]]
     bubble_t = sum((Q - s[0]) * s[2] for s in r["stats"]) / (Q * max(1e-9, sum(dts)))
     if dist:
-        import torch
-        t = torch.tensor([r["raw"], r["useful"], r["ms"]], dtype=torch.float64, device="cuda")
-        tot = t.clone()
-        dist.all_reduce(tot)
-        mx = t.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        tok_s = tot[0].item() / (mx[2].item() * 1e-3)
-        useful_s = tot[1].item() / (mx[2].item() * 1e-3)
-        ms = mx[2].item()
+        # raw tokens: the replicated counter counts every replica's tokens, so each
+        # rank contributes its own rows only (raw / world on every rank, exact in
+        # lockstep since the counter is global); useful likewise
+        tok_s, useful_s, ms = aggregate_over_ranks(dist, r["raw"] / world, r["useful"] / world, r["ms"])
     else:
         useful_s = r["useful"] / (r["ms"] * 1e-3)
         ms = r["ms"]
@@ -377,7 +399,7 @@ def main():
         "config": {"workload": WORKLOAD, "window": f"decode steps [{args.precondition + args.warmup}, "
                    f"{args.precondition + args.warmup + steps}) of the cfg2 rollout",
                    "l2": "no flush needed: every step streams 15 GB of weights + the KV cache (>> 126 MB L2)",
-                   "parallelism": f"dp{world} (independent replicas)" if world > 1 else "dp1"},
+                   "parallelism": f"dp{world} lockstep replicas (NCCL)" if world > 1 else "dp1"},
         "useful_tokens_per_s": useful_s,
         "bubble_ratio": {"window_abstract": bubble, "window_time_weighted": bubble_t,
                          "definition": "Eq.(bubble) P:339-342 over the timed decode steps, Q=Q_g"},
@@ -388,7 +410,7 @@ def main():
         "gpu_launches": r["launches"],
         "clocks": r["clocks"],
         "e2e": r["e2e"],
-        "mean_ctx": sum_ctx / max(1, sum(s[0] for s in r["stats"])),
+        "mean_ctx": sum_ctx / max(1, sum(s[5] for s in r["stats"])),
     }
     if not args.no_cpu and world == 1:
         line["cpu_baseline"] = oracle_sample()

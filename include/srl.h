@@ -80,10 +80,29 @@ typedef struct srl_sched_cfg {
   int32_t max_traj, max_prompt, prefill_chunk;
 } srl_sched_cfg;
 
-/* Data-parallel replica identity (R > 1 uses NCCL). */
+/* Data-parallel replicas (rows a14, a17).  R = world engines run
+ * the SAME global step in lockstep: every rank holds the full (replicated)
+ * controller state, decodes only its own slots g = s*R + rank, and after the
+ * sampler an in-place all-gather of every replica's [Q_g] (token, logprob) rows
+ * lets every rank run the identical controller END (stop, compaction, sorted
+ * emission).  srl_load_policy_weights broadcasts rank 0's policy in place.
+ * kind:
+ *   SRL_COMM_NCCL   one process per GPU; nccl_unique_id from srl_nccl_unique_id
+ *                   on rank 0, shared by the caller (e.g. torch.distributed);
+ *                   world may be 1 (a one-rank communicator: same code path).
+ *   SRL_COMM_LOCAL  `world` engines in one process, each driven by its own host
+ *                   thread (any devices, several may share one GPU); local_group
+ *                   from srl_local_group_create(world), destroyed after every
+ *                   engine of the group.  Peer copies + CUDA events + a host
+ *                   barrier (300 s timeout => SRL_E_NCCL on every rank).
+ * All ranks must make the same sequence of srl_submit_prompts /
+ * srl_decode_step / srl_harvest_finished / srl_load_policy_weights calls. */
+enum { SRL_COMM_NCCL = 0, SRL_COMM_LOCAL = 1 };
 typedef struct srl_comm {
   int32_t rank, world;
-  uint8_t nccl_unique_id[128]; /* from ncclGetUniqueId on rank 0, shared by the caller */
+  int32_t kind, pad_;
+  void* local_group;
+  uint8_t nccl_unique_id[128];
 } srl_comm;
 
 /* Device memory lent by the caller, sized by srl_arena_sizes. */
@@ -104,13 +123,15 @@ typedef struct srl_step_info {
   int32_t v;          /* current policy version */
   float dt_ms;        /* device time of the step on this GPU (cudaEvent) */
   int64_t sum_ctx;    /* sum over this GPU's running rows of the attended context (KV tokens read per layer) */
+  int32_t r_local;    /* running rows decoded on this GPU in that step (r_k counts all replicas) */
+  int32_t pad_;
 } srl_step_info;
 
 /* Per-kernel-class device timing (CUDA events on the engine stream), enabled by
  * srl_set_profiling.  Classes: */
 enum { SRL_K_GEMM_QKV = 0, SRL_K_GEMM_O = 1, SRL_K_GEMM_GU = 2, SRL_K_GEMM_DOWN = 3, SRL_K_LM_HEAD = 4,
        SRL_K_ATTN = 5, SRL_K_ELEMWISE = 6, SRL_K_SAMPLE = 7, SRL_K_CTL = 8, SRL_K_PREFILL = 9,
-       SRL_K_NCLASS = 10 };
+       SRL_K_COMM = 10 /* replica all-gather + weight broadcast */, SRL_K_NCLASS = 11 };
 
 /* One harvested trajectory (SPEC BufferEntry / P:199). */
 typedef struct srl_traj {
@@ -195,7 +216,9 @@ int32_t srl_harvest_finished(srl_engine* e, int32_t cap_recs, srl_traj* recs, in
  * the first call may use any version >= 0).  flat_w: device pointer to a flat
  * weight image (srl_weight_offset layout) on rank 0 (ignored elsewhere), or
  * NULL when the caller already wrote the staging part of the engine's weight
- * region (the first srl_weight_layout bytes).  The projection matrices (wq/wk/wv,
+ * region (the first srl_weight_layout bytes) -- on rank 0; other ranks receive
+ * rank 0's installed tensors by an in-place broadcast (row a17) and
+ * never read their own staging copy.  The projection matrices (wq/wk/wv,
  * wo, wg/wu, wd, lm_head) are repacked from the source into the GEMM's packed
  * layout (srl_op_pack_weight) in the rest of the weight region -- which is why
  * srl_arena_sizes reports about twice the model size -- so the staging copy of
@@ -228,6 +251,13 @@ int32_t srl_get_profile(srl_engine* e, double* ms, int64_t* launches);
 /* Test accessor: copy the fp32 logits [Q_g, V] of the last decode step (local
  * slots; rows of empty slots are unspecified) to host memory. */
 int32_t srl_debug_copy_logits(srl_engine* e, float* out_host, int64_t cap_floats);
+
+/* Replica plumbing (see srl_comm).  srl_nccl_unique_id: 128 bytes for
+ * srl_comm.nccl_unique_id (SRL_E_NCCL if libnccl cannot be loaded).
+ * srl_local_group_create: an in-process group of `world` ranks (1..64). */
+int32_t srl_nccl_unique_id(uint8_t* out128);
+int32_t srl_local_group_create(int32_t world, void** out);
+int32_t srl_local_group_destroy(void* group);
 
 const char* srl_last_error(void);
 

@@ -29,8 +29,12 @@ class SchedCfg(C.Structure):
                 ("sample_seed", _U64), ("max_traj", _I32), ("max_prompt", _I32), ("prefill_chunk", _I32)]
 
 
+COMM_NCCL, COMM_LOCAL = 0, 1   # srl.h SRL_COMM_*
+
+
 class Comm(C.Structure):
-    _fields_ = [("rank", _I32), ("world", _I32), ("nccl_unique_id", C.c_uint8 * 128)]
+    _fields_ = [("rank", _I32), ("world", _I32), ("kind", _I32), ("pad_", _I32), ("local_group", _P),
+                ("nccl_unique_id", C.c_uint8 * 128)]
 
 
 class Arena(C.Structure):
@@ -40,11 +44,12 @@ class Arena(C.Structure):
 
 class StepInfo(C.Structure):
     _fields_ = [("k", _I64), ("r_k", _I32), ("n_finished", _I32), ("n_ready", _I32), ("n_admitted", _I32),
-                ("n_prefill_tokens", _I32), ("v", _I32), ("dt_ms", C.c_float), ("sum_ctx", _I64)]
+                ("n_prefill_tokens", _I32), ("v", _I32), ("dt_ms", C.c_float), ("sum_ctx", _I64),
+                ("r_local", _I32), ("pad_", _I32)]
 
 
 KERNEL_CLASSES = ["gemm_qkv", "gemm_o", "gemm_gate_up", "gemm_down", "lm_head", "attention", "elementwise",
-                  "sample", "controller", "prefill"]
+                  "sample", "controller", "prefill", "exchange"]
 
 
 class TrajRec(C.Structure):
@@ -85,6 +90,9 @@ SIGNATURES = {
     "srl_debug_copy_logits": (_I32, [_P, _P, _I64]),
     "srl_set_profiling": (_I32, [_P, _I32]),
     "srl_get_profile": (_I32, [_P, C.POINTER(C.c_double), _I64P]),
+    "srl_nccl_unique_id": (_I32, [_P]),
+    "srl_local_group_create": (_I32, [_I32, C.POINTER(_P)]),
+    "srl_local_group_destroy": (_I32, [_P]),
 }
 
 GEMM_W_PACKED = 0x100   # srl_ops.h SRL_GEMM_W_PACKED

@@ -1,0 +1,49 @@
+// comm.hpp — the replica exchange of the data-parallel rollout (SURVEY §8(e),
+// rows a14 and a17): an in-place all-gather of every replica's sampled
+// (token, logprob) rows after each decode step, and an in-place broadcast of
+// the refreshed policy from rank 0 after each early update.
+//
+// Two transports behind one interface:
+//   NCCL   one process per GPU (torch.distributed launch); libnccl is resolved
+//          at run time with dlopen -- the copy torch already loaded -- so the
+//          library does not pin an NCCL version at link time;
+//   LOCAL  several engines in ONE process (one host thread each, any devices,
+//          including several on the same GPU): peer copies with
+//          cudaMemcpyAsync ordered by CUDA events and a host barrier.  This is
+//          what lets one B200 run the R > 1 lockstep path bit-exactly against
+//          the oracle.
+// Every call is collective: all ranks issue the same calls in the same order.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+namespace srl {
+
+struct Range {
+  void* p;
+  size_t bytes;
+};
+
+class Comm {
+ public:
+  int rank = 0, world = 1;
+  virtual ~Comm() = default;
+  // buf holds `world` segments of seg_bytes; this rank's segment (rank * seg_bytes)
+  // is the input, every other segment is overwritten with the owner's.
+  virtual int allgather_inplace(void* buf, size_t seg_bytes, cudaStream_t st, std::string& err) = 0;
+  // every rank passes the same list (its own addresses); rank 0's bytes are copied
+  // into every other rank's ranges.
+  virtual int broadcast_inplace(const std::vector<Range>& ranges, cudaStream_t st, std::string& err) = 0;
+};
+
+Comm* comm_create_nccl(const uint8_t* unique_id, int rank, int world, std::string& err);
+Comm* comm_create_local(void* group, int rank, int world, std::string& err);
+int nccl_unique_id(uint8_t* out128, std::string& err);
+void* local_group_create(int world);
+void local_group_destroy(void* g);
+
+}  // namespace srl

@@ -425,6 +425,7 @@ __global__ void __launch_bounds__(kCtlThreads, 1) ctl_begin_kernel(Ctl c) {
   }
   // decode rows for the local slots
   long long my_ctx = 0;
+  int my_rows = 0;
   for (int sl = threadIdx.x; sl < c.Q_g; sl += blockDim.x) {
     const int g = sl * c.R + c.rank;
     const int tid = c.slot_traj[g];
@@ -435,6 +436,7 @@ __global__ void __launch_bounds__(kCtlThreads, 1) ctl_begin_kernel(Ctl c) {
                             : c.prompt_tok[c.prompt_off[t.prompt_idx] + t.prompt_len - 1];
       c.row_pos[sl] = t.prompt_len + n - 1;
       my_ctx += t.prompt_len + n;
+      my_rows++;
       c.row_n[sl] = n;
       c.row_traj[sl] = tid;
       c.row_restarts[sl] = t.restarts;
@@ -455,8 +457,11 @@ __global__ void __launch_bounds__(kCtlThreads, 1) ctl_begin_kernel(Ctl c) {
   }
   __syncthreads();
   atomicAdd(&sh_ctx, (unsigned long long)my_ctx);
-  __syncthreads();
-  if (threadIdx.x == 0) s->st.sum_ctx = (long long)sh_ctx;
+  my_rows = block_sum(my_rows);
+  if (threadIdx.x == 0) {
+    s->st.sum_ctx = (long long)sh_ctx;
+    s->st.r_local = my_rows;
+  }
   const int na = s->st.n_admit_local;
   for (int a = 0; a < na; ++a) {
     const int sl = c.admit_local[a];
@@ -505,10 +510,10 @@ __global__ void __launch_bounds__(kCtlThreads, 1) ctl_end_kernel(Ctl c) {
         occ++;
         DevTraj& t = c.traj[tid];
         const int n = t.n_tok;
-        const int src = (g % c.R) * c.Q_g + g / c.R;
-        const int tok = c.samp_tok[src];
+        const int src = (g % c.R) * 2 * c.Q_g + g / c.R;
+        const int tok = c.samp[src];
         c.tokens[(size_t)tid * c.cap + n] = tok;
-        c.lps[(size_t)tid * c.cap + n] = c.samp_lp[src];
+        c.lps[(size_t)tid * c.cap + n] = __int_as_float(c.samp[src + c.Q_g]);
         c.vers[(size_t)tid * c.cap + n] = v;
         t.n_tok = n + 1;
         fin = (c.stop == SRL_STOP_FORCED && n + 1 == t.forced_len) ||

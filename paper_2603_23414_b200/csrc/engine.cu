@@ -9,6 +9,7 @@
 #include <unordered_set>
 #include <vector>
 
+#include "comm.hpp"
 #include "engine.hpp"
 #include "kernels.hpp"
 #include "layers.hpp"
@@ -144,7 +145,7 @@ int validate(const srl_model_cfg* m, const srl_sched_cfg* s, int world, std::str
     return why = "Q_g, U, G, cap, pool_prompts, kv_pages must be positive", -1;
   if (s->page_tokens != kPage) return why = "page_tokens must be 64", -1;
   if (world < 1 || world > kMaxR) return why = "world out of range", -1;
-  if ((long long)s->Q_g * world > 1024) return why = "Q_tot must be <= 1024", -1;
+  if ((long long)s->Q_g * world > 4096) return why = "Q_tot must be <= 4096", -1;
   if (s->mode == SRL_MODE_SORTED && s->U > s->pool_prompts * s->G) return why = "U larger than the prompt pool (S:252)", -1;
   if (s->U > kMaxGroup) return why = "U too large", -1;
   if (s->stop == SRL_STOP_EOS && s->eos_id < 0) return why = "EOS stop needs eos_id", -1;
@@ -185,6 +186,7 @@ struct srl_engine {
   Sizes z;
   int rank = 0, world = 1, device = 0, num_sms = 148;
   cudaStream_t st = nullptr;
+  Comm* comm = nullptr;  // replica exchange (NCCL or in-process); null for a lone engine
   bool kv_f32 = false;
   // arena
   uint8_t *W = nullptr, *KV = nullptr, *S = nullptr;
@@ -334,8 +336,7 @@ void plan_scratch(srl_engine* e, ScratchPlan& p, bool assign) {
   c.pre_pos = (int*)P(4ull * z.prefill_rows_max);
   c.pre_slot = (int*)P(4ull * z.prefill_rows_max);
   c.admit_local = (int*)P(4 * z.Q_g);
-  c.samp_tok = (int*)P(4 * z.Q_tot);
-  c.samp_lp = (float*)P(4 * z.Q_tot);
+  c.samp = (int*)P(8 * z.Q_tot);
   c.h_tok = (int*)P(4ull * z.h_cap_tok);
   c.h_lp = (float*)P(4ull * z.h_cap_tok);
   c.h_ver = (int*)P(4ull * z.h_cap_tok);
@@ -461,8 +462,9 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
   }
 }
 
-// decode forward over the local slots, sampler, controller END (static shapes)
-void decode_tail(srl_engine* e) {
+// decode forward over the local slots, sampler and (alone) controller END --
+// static shapes.  With a replica exchange the END runs after the all-gather.
+void decode_tail(srl_engine* e, bool with_end) {
   const Ctl& c = e->ctl;
   cudaStream_t st = e->st;
   forward(e, e->s.Q_g, c.row_tok, c.row_pos, e->row_slot_id, true);
@@ -476,18 +478,36 @@ void decode_tail(srl_engine* e) {
   sa.row_restarts = c.row_restarts;
   sa.invT = 1.0f / e->s.temperature;
   sa.seed = e->s.sample_seed;
-  sa.tok_out = c.samp_tok + (size_t)e->rank * e->s.Q_g;
-  sa.lp_out = c.samp_lp + (size_t)e->rank * e->s.Q_g;
+  sa.tok_out = c.samp + (size_t)e->rank * 2 * e->s.Q_g;
+  sa.lp_out = (float*)(c.samp + (size_t)e->rank * 2 * e->s.Q_g + e->s.Q_g);
   {
     Prof p(e, SRL_K_SAMPLE);
     sample(sa, st);
   }
   e->launches++;
+  if (!with_end) return;
   {
     Prof p(e, SRL_K_CTL);
     ctl_end(c, st);
   }
   e->launches++;
+}
+
+// Rows a14 + a12/a13: every replica's (token, logprob) rows reach every rank, then
+// the replicated controller END runs identically everywhere (reading R24).
+int exchange_and_end(srl_engine* e) {
+  std::string err;
+  {
+    Prof p(e, SRL_K_COMM);
+    if (e->comm->allgather_inplace(e->ctl.samp, 8ull * e->s.Q_g, e->st, err))
+      return fail(SRL_E_NCCL, "srl_decode_step: replica all-gather: " + err);
+  }
+  {
+    Prof p(e, SRL_K_CTL);
+    ctl_end(e->ctl, e->st);
+  }
+  e->launches++;
+  return SRL_OK;
 }
 
 void read_status(srl_engine* e) {
@@ -546,7 +566,8 @@ int32_t srl_create(const srl_model_cfg* m, const srl_sched_cfg* s, int32_t devic
   const int world = comm ? comm->world : 1;
   std::string why;
   if (validate(m, s, world, why)) return fail(SRL_E_INVALID_ARG, "srl_create: " + why);
-  if (world > 1) return fail(SRL_E_INVALID_ARG, "srl_create: world > 1 requires the NCCL build (not in this library)");
+  if (comm && (comm->rank < 0 || comm->rank >= world || (comm->kind != SRL_COMM_NCCL && comm->kind != SRL_COMM_LOCAL)))
+    return fail(SRL_E_INVALID_ARG, "srl_create: bad srl_comm (rank / kind)");
   uint64_t wb, kb, sb;
   srl_arena_sizes(m, s, world, &wb, &kb, &sb);
   if (mem->weights_bytes < wb || mem->kv_bytes < kb || mem->scratch_bytes < sb || !mem->weights || !mem->kv || !mem->scratch)
@@ -562,6 +583,14 @@ int32_t srl_create(const srl_model_cfg* m, const srl_sched_cfg* s, int32_t devic
   e->kv_f32 = s->kv_dtype == SRL_KV_FP32;
   e->z = compute_sizes(m, s, world);
   e->use_graph = getenv("SRL_NO_GRAPH") == nullptr && stream != nullptr;  // the legacy stream cannot be captured
+  if (comm) {
+    e->comm = comm->kind == SRL_COMM_NCCL ? comm_create_nccl(comm->nccl_unique_id, comm->rank, world, why)
+                                          : comm_create_local(comm->local_group, comm->rank, world, why);
+    if (!e->comm) {
+      delete e;
+      return fail(SRL_E_NCCL, "srl_create: replica communicator: " + why);
+    }
+  }
   cudaDeviceGetAttribute(&e->num_sms, cudaDevAttrMultiProcessorCount, device);
   e->W = (uint8_t*)mem->weights;
   e->KV = (uint8_t*)mem->kv;
@@ -667,6 +696,7 @@ int32_t srl_destroy(srl_engine* e) {
   for (cudaEvent_t ev : e->direct.ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : e->gset.ev) cudaEventDestroy(ev);
   if (e->gexec) cudaGraphExecDestroy(e->gexec);
+  delete e->comm;
   delete e;
   return SRL_OK;
 }
@@ -772,7 +802,7 @@ int32_t srl_decode_step(srl_engine* e, srl_step_info* info) {
     e->capturing = true;
     bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
     if (ok) {
-      decode_tail(e);
+      decode_tail(e, e->comm == nullptr);
       ok = cudaStreamEndCapture(st, &g) == cudaSuccess && g;
     }
     e->capturing = false;
@@ -793,9 +823,11 @@ int32_t srl_decode_step(srl_engine* e, srl_step_info* info) {
     cudaGraphLaunch(e->gexec, st);
     e->launches += e->g_launches;
   } else {
-    decode_tail(e);
+    decode_tail(e, e->comm == nullptr);
     e->direct_steps++;
   }
+  if (e->comm)
+    if (int rc = exchange_and_end(e)) return rc;
   cudaEventRecord(e->ev1, st);
   read_status(e);
   if (cudaError_t ce = cudaGetLastError()) return cuda_fail("decode step", ce);
@@ -810,6 +842,7 @@ int32_t srl_decode_step(srl_engine* e, srl_step_info* info) {
     info->n_admitted = b.n_admit;
     info->n_prefill_tokens = b.m_pre;
     info->sum_ctx = b.sum_ctx;
+    info->r_local = b.r_local;
     info->v = en.v;
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e->ev0, e->ev1);
@@ -856,12 +889,13 @@ int32_t srl_load_policy_weights(srl_engine* e, const void* flat_w, int64_t versi
   // GEMM weight stream's layout; the remaining tensors (embedding, norms, biases)
   // are read in place, so copy those when the source is the caller's buffer.
   const uint8_t* src = flat_w ? (const uint8_t*)flat_w : e->W;
-  if (src != e->W) {
+  const bool root = e->rank == 0;  // with replicas only rank 0 reads a source; the rest receive
+  if (root && src != e->W) {
     for (const auto& en : e->wl.ents)
       if (!is_packed_tensor(en.name))
         cudaMemcpyAsync(e->W + en.off, src + en.off, en.numel * 2, cudaMemcpyDeviceToDevice, e->st);
   }
-  {
+  if (root) {
     const srl_model_cfg& m = e->m;
     const int d = m.d, qd = m.Hq * m.dh, nqkv = (m.Hq + 2 * m.Hkv) * m.dh;
     auto sp = [&](const std::string& n) {
@@ -880,6 +914,18 @@ int32_t srl_load_policy_weights(srl_engine* e, const void* flat_w, int64_t versi
     rc |= pack_weight(sp("lm_head"), m.V, d, e->plm_head, e->st);
     e->launches++;
     if (rc) return cuda_fail("srl_load_policy_weights: pack_weight", cudaGetLastError());
+  }
+  if (e->comm) {
+    // Row a17: rank 0's installed policy -> every replica, in place: the packed GEMM
+    // stream (one contiguous region) plus the tensors read in place (embedding,
+    // norms, biases).  Packed staging matrices are not decoded from, so not sent.
+    std::vector<Range> rr;
+    for (const auto& en : e->wl.ents)
+      if (!is_packed_tensor(en.name)) rr.push_back({e->W + en.off, en.numel * 2});
+    rr.push_back({e->W + e->pk.base, e->pk.total - e->pk.base});
+    std::string err;
+    Prof p(e, SRL_K_COMM);
+    if (e->comm->broadcast_inplace(rr, e->st, err)) return fail(SRL_E_NCCL, "srl_load_policy_weights: broadcast: " + err);
   }
   ctl_bump(e->ctl, (int)version, e->st);
   e->launches++;
@@ -970,5 +1016,24 @@ extern "C" int32_t srl_debug_copy_logits(srl_engine* e, float* out_host, int64_t
   if (cap_floats < n) return fail(SRL_E_CAPACITY, "srl_debug_copy_logits: buffer too small");
   cudaMemcpyAsync(out_host, e->logits, 4 * n, cudaMemcpyDeviceToHost, e->st);
   if (cudaStreamSynchronize(e->st) != cudaSuccess) return cuda_fail("srl_debug_copy_logits");
+  return SRL_OK;
+}
+
+// ------------------------------------------------------------------ replica plumbing
+extern "C" int32_t srl_nccl_unique_id(uint8_t* out128) {
+  if (!out128) return fail(SRL_E_INVALID_ARG, "srl_nccl_unique_id: null argument");
+  std::string err;
+  if (nccl_unique_id(out128, err)) return fail(SRL_E_NCCL, "srl_nccl_unique_id: " + err);
+  return SRL_OK;
+}
+
+extern "C" int32_t srl_local_group_create(int32_t world, void** out) {
+  if (!out || world < 1 || world > kMaxR) return fail(SRL_E_INVALID_ARG, "srl_local_group_create: bad arguments");
+  *out = local_group_create(world);
+  return SRL_OK;
+}
+
+extern "C" int32_t srl_local_group_destroy(void* group) {
+  local_group_destroy(group);
   return SRL_OK;
 }

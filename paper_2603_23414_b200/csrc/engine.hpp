@@ -43,7 +43,8 @@ struct CtlStatus {
   int group_n, group_final, group_state;
   long long n_events, raw_tokens, discarded_tokens, emitted, n_groups;
   long long sum_ctx;  // sum of (pos + 1) over this rank's running rows (BEGIN)
-  int pad[4];
+  int r_local;        // running rows on this rank (BEGIN)
+  int pad[3];
 };
 
 struct CtlState {
@@ -91,8 +92,8 @@ struct Ctl {
   int* pre_pos;
   int* pre_slot;       // local slot of the prefill row
   int* admit_local;    // [Q_g] local slot ids admitted this step (for prefill)
-  int* samp_tok;       // [R][Q_g] sampled tokens (all replicas)
-  float* samp_lp;      // [R][Q_g]
+  int* samp;           // [R][2][Q_g]: per replica its sampled tokens, then their fp32 logprobs
+                       // (bit pattern); rank r writes block r, the replica all-gather fills the rest
   // harvest staging
   int* h_tok;
   float* h_lp;

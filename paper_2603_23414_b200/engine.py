@@ -12,7 +12,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from ._lib import Arena, Comm, ModelCfg, SchedCfg, StepInfo, TraceRec, TrajRec, check
+from ._lib import COMM_LOCAL, COMM_NCCL, Arena, Comm, ModelCfg, SchedCfg, StepInfo, TraceRec, TrajRec, check
 
 OK, GROUP_READY, DONE = 0, 1, 2
 EV_NAMES = {0: "STEP", 1: "LOAD", 2: "ADMIT", 3: "PREEMPT", 4: "FINISH", 5: "EMIT", 6: "DISCARD", 7: "SCAVENGE",
@@ -21,6 +21,36 @@ EV_NAMES = {0: "STEP", 1: "LOAD", 2: "ADMIT", 3: "PREEMPT", 4: "FINISH", 5: "EMI
 
 def _i32p(a):
     return a.ctypes.data_as(C.c_void_p)
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id for srl_comm (call on rank 0, share with the others)."""
+    buf = (C.c_uint8 * 128)()
+    check(_lib.load().srl_nccl_unique_id(C.cast(buf, C.c_void_p)), "srl_nccl_unique_id")
+    return bytes(buf)
+
+
+def share_nccl_unique_id(dist, rank: int) -> bytes:
+    """Rank 0 draws the id, torch.distributed broadcasts it (any backend)."""
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+class LocalGroup:
+    """An in-process replica group (SRL_COMM_LOCAL): `world` engines, one host
+    thread each, exchanging through peer copies.  Close after its engines."""
+
+    def __init__(self, world: int):
+        self.lib = _lib.load()
+        self.world = world
+        self.h = C.c_void_p()
+        check(self.lib.srl_local_group_create(world, C.byref(self.h)), "srl_local_group_create")
+
+    def close(self):
+        if self.h:
+            self.lib.srl_local_group_destroy(self.h)
+            self.h = C.c_void_p()
 
 
 @dataclass
@@ -36,7 +66,11 @@ class RolloutEngine:
     srl_model_cfg / srl_sched_cfg field names (workload.configs provides them)."""
 
     def __init__(self, model, sched, *, max_traj: int, max_prompt: int, prefill_chunk: int = 2048,
-                 device: int = 0, stream=None, rank: int = 0, world: int = 1):
+                 device: int = 0, stream=None, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
+                 local_group: LocalGroup | None = None):
+        """world > 1 (or an explicit nccl_id / local_group) makes this engine rank
+        `rank` of a lockstep replica group: NCCL when `nccl_id` is given (one process
+        per GPU), in-process when `local_group` is."""
         import torch
         self.torch = torch
         self.lib = _lib.load()
@@ -60,9 +94,17 @@ class RolloutEngine:
         self.stream = stream if stream is not None else torch.cuda.Stream(self.dev)
         arena = Arena(self.W.data_ptr(), self.KV.data_ptr(), self.S.data_ptr(), wb.value, kb.value, sb.value)
         comm = None
-        if world > 1:
+        if world > 1 or nccl_id is not None or local_group is not None:
+            if (nccl_id is None) == (local_group is None):
+                raise ValueError("a replica engine needs exactly one of nccl_id / local_group")
             comm = Comm()
             comm.rank, comm.world = rank, world
+            if nccl_id is not None:
+                comm.kind = COMM_NCCL
+                C.memmove(comm.nccl_unique_id, nccl_id, 128)
+            else:
+                comm.kind = COMM_LOCAL
+                comm.local_group = local_group.h
         self.h = C.c_void_p()
         check(self.lib.srl_create(C.byref(self.m), C.byref(self.s), device, C.c_void_p(self.stream.cuda_stream),
                                   C.byref(arena), C.byref(comm) if comm else None, C.byref(self.h)), "srl_create")

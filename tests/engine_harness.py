@@ -24,9 +24,11 @@ def tiny_workload(n_prompts=16, G=1, seed_len=0, seed_prompt=1, V=512, cap=64, l
     return off, toks, L
 
 
-def make_engine(model, cfg: SchedConfig, max_traj, max_prompt, prefill_chunk=256):
+def make_engine(model, cfg: SchedConfig, max_traj, max_prompt, prefill_chunk=256, **replica):
+    """`replica`: rank / world / local_group / nccl_id for a lockstep replica engine."""
     from paper_2603_23414_b200.engine import RolloutEngine
-    eng = RolloutEngine(model, cfg, max_traj=max_traj, max_prompt=max_prompt, prefill_chunk=prefill_chunk)
+    eng = RolloutEngine(model, cfg, max_traj=max_traj, max_prompt=max_prompt, prefill_chunk=prefill_chunk,
+                        **replica)
     fill_weights(eng, model, 0)
     eng.load_policy_weights(0)
     return eng
