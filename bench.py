@@ -2,18 +2,23 @@
 """SortedRL rollout benchmark (BASELINE.json metric: rollout tokens/s + bubble
 ratio @1/2/4/8 B200; decode %HBM roofline).
 
-A "step" is one srl_decode_step: refill/admission (+ prefill of admitted
-prompts), the policy's decode forward over the ragged batch (tcgen05 GEMMs,
-paged attention), sampling, stop detection, compaction into the rollout
-buffer, and -- when an update group is ready -- harvest of the length-sorted
-group plus the policy refresh (load_policy_weights).
+A "step" is one early-update round of the rollout -- SortedRL's unit of work
+(P:169-177): srl_decode_step repeatedly (refill/admission + prefill of
+admitted prompts, the policy's decode forward over the ragged batch -- tcgen05
+GEMMs, paged attention -- Philox sampling, stop detection, compaction into the
+rollout buffer) until the length-sorted update group is ready, then its
+harvest and the policy refresh (load_policy_weights with the cache bound).
+Every SURVEY §8(a) row runs in every step.
 
 Workload (configs[1], "cfg2"): LLaMA-3.1-8B-shaped random-init policy on one
 B200, rollout batch Q=256, max 8k tokens, update group U=64, K=inf (partial
-mode), pool 4*Q prompts, 256-token prompts, lognormal(1600, 0.55) + 3% cap
-FORCED response lengths (DESIGN.md input recipe).  The timed window is steps
-[P+W, P+W+K) of that rollout (P = --precondition untimed steps so contexts
-are mid-rollout; W = --warmup).
+mode), pool 4*Q prompts per epoch, 256-token prompts, lognormal(1600, 0.55) +
+3% cap FORCED response lengths (DESIGN.md input recipe).  P untimed decode
+steps (--precondition) bring contexts mid-rollout, W untimed rounds follow,
+then K rounds are timed on the device (CUDA events on the engine stream,
+barrier + max over ranks).  `value` = tokens generated per second of device
+time; `e2e` = the same through the public API, prompts streamed from pinned
+host memory each round and groups copied back, wall-clock.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--precondition P]
   python bench.py --impl reference ...   # the CPU oracle on a bounded sample
@@ -45,6 +50,7 @@ WORKLOAD = ("cfg2: LLaMA-3.1-8B-shaped random-init bf16 policy, rollout batch Q_
             "weight broadcast after every update group)")
 N_PROMPTS_PER_EPOCH = 1024
 PROMPT_LEN = 256
+EPOCHS = 4          # prompt stream long enough for precondition + warmup + timed + e2e rounds
 
 
 def cfg2_sched(world=1):
@@ -149,112 +155,137 @@ def run_gpu(args, rank, world, dist):
     dev = torch.cuda.current_device()
     from paper_2603_23414_b200.engine import share_nccl_unique_id
     model, sched = LLAMA8B, cfg2_sched(world)
-    off, toks, L = workload_inputs(world)
+    off, toks, L = workload_inputs(world, epochs=EPOCHS)
     ids = np.arange(len(off) - 1, dtype=np.uint64) + 1
-    max_traj = 2 * N_PROMPTS_PER_EPOCH * world
-
-    def new_engine():
-        rep = {}
-        if world > 1:
-            rep = dict(rank=rank, world=world, nccl_id=share_nccl_unique_id(dist, rank))
-        return RolloutEngine(model, sched, max_traj=max_traj, max_prompt=PROMPT_LEN, prefill_chunk=4096, device=dev,
-                             **rep)
-    eng = new_engine()
+    n_prompts = len(ids)
+    max_traj = EPOCHS * N_PROMPTS_PER_EPOCH * world
+    rep = {}
+    if world > 1:
+        rep = dict(rank=rank, world=world, nccl_id=share_nccl_unique_id(dist, rank))
+    eng = RolloutEngine(model, sched, max_traj=max_traj, max_prompt=PROMPT_LEN, prefill_chunk=4096, device=dev,
+                        **rep)
     fill_engine_weights(eng, model, 0)
     # the trainer's copy of the refreshed policy on rank 0 (K13: the same bytes are
     # re-emitted); the other replicas receive it through the engine's broadcast
     trainer = eng.W.clone() if rank == 0 else None
     eng.load_policy_weights(0)
     torch.cuda.synchronize()
+    stream = eng.stream              # the stream every engine kernel is launched on
+    st = {"v": 0, "useful": 0, "d2h": 0, "sub": 0, "done": False}
+    trace = []                       # every decode step: (r_k, sum_ctx, dt_ms, prefill_tokens, n_fin, r_local)
 
-    def drive(eng, nsteps, state, harvest_host=False, stats=None):
-        done = 0
-        while done < nsteps:
-            st, info = eng.decode_step()
-            if st == DONE:
-                break
-            if info.k >= 0:
-                done += 1
-                if stats is not None:
-                    stats.append((info.r_k, info.sum_ctx, info.dt_ms, info.n_prefill_tokens, info.n_finished,
-                                  info.r_local))
-            if st == GROUP_READY:
-                h = eng.harvest_finished(cap_recs=2048, cap_toks=2048 * sched.cap)
-                state["useful"] += sum(r["len"] for r in h.records)
-                state["d2h"] += sum(r["len"] for r in h.records) * 12 + len(h.records) * 64
-                state["v"] += 1
-                eng.load_policy_weights(state["v"], trainer)
-        return done
+    def step():
+        s_, info = eng.decode_step()
+        if s_ == DONE:
+            st["done"] = True
+            return None
+        if info.k >= 0:
+            trace.append((info.r_k, info.sum_ctx, info.dt_ms, info.n_prefill_tokens, info.n_finished,
+                          info.r_local))
+        if s_ == GROUP_READY:        # rows a15-a17: sorted group out, refreshed policy in
+            h = eng.harvest_finished(cap_recs=2048, cap_toks=2048 * sched.cap)
+            st["useful"] += sum(r["len"] for r in h.records)
+            st["d2h"] += sum(r["len"] for r in h.records) * 12 + len(h.records) * 64
+            st["v"] += 1
+            eng.load_policy_weights(st["v"], trainer)
+            return True
+        return False
 
-    # ---------------- value: device-timed window, prompts resident
-    eng.submit_prompts(ids, off, toks, L)
-    state = {"useful": 0, "d2h": 0, "v": 0}
-    drive(eng, args.precondition, state)
-    drive(eng, args.warmup, state)
-    stats = []
-    state["useful"] = 0
-    c0 = eng.counters()
-    eng.set_profiling(True)
+    def one_round():
+        """One early-update round: decode steps until the length-sorted update group
+        is ready, its harvest and the policy refresh (the bench's "step")."""
+        while not st["done"]:
+            if step():
+                return True
+        return False
+
+    def submit(lo, hi):
+        o = off[lo:hi + 1]
+        eng.submit_prompts(ids[lo:hi], (o - o[0]).astype(np.int32), toks[o[0]:o[-1]], L[lo:hi])
+        st["sub"] = hi
+
+    # the first two epochs are resident; the e2e leg streams the rest from host memory
+    submit(0, min(n_prompts, 2 * N_PROMPTS_PER_EPOCH * world))
+    for _ in range(args.precondition):
+        if step() is None:
+            break
+    while not st["done"] and not step():
+        pass                         # finish the round in flight
+    for _ in range(args.warmup):
+        one_round()
+    # ---------------- value: device-timed rounds, inputs resident; only the dominant
+    # kernel class is bracketed by events (for the roofline) so the decode graph
+    # keeps its programmatic-launch edges elsewhere
+    eng.set_profiling(True, classes=["attention"])
+    t0 = len(trace)
+    u0, c0 = st["useful"], eng.counters()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    stream = eng.stream              # the stream every engine kernel is launched on
+    ran = 0
     with ClockSampler(dev) as clk:
         e0.record(stream)
-        ran = drive(eng, args.steps, state, stats=stats)
+        for _ in range(args.steps):
+            ran += one_round()
         e1.record(stream)
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
     ms = e0.elapsed_time(e1)
     prof = eng.profile()
-    eng.set_profiling(False)
     c1 = eng.counters()
-    raw = c1["raw_tokens"] - c0["raw_tokens"]
-    useful = state["useful"]
+    raw, useful = c1["raw_tokens"] - c0["raw_tokens"], st["useful"] - u0
     launches = c1["kernel_launches"] - c0["kernel_launches"]
-    eng.close()
-    del eng
-
-    # ---------------- e2e: same window through the C ABI with host buffers
+    stats = trace[t0:]
+    # ---------------- breakdown: one more round with every kernel class bracketed
+    # (events cut the graph's PDL edges: reported, not the headline)
+    eng.set_profiling(True)
+    b0 = len(trace)
+    one_round()
+    breakdown = eng.profile()
+    n_break = len(trace) - b0
+    eng.set_profiling(False)
+    # ---------------- e2e: the same rounds through the public API with host buffers:
+    # each round submits the next U prompts from pinned host memory (the streaming
+    # dataloader) and copies its harvested group back to host
     e2e = None
-    if not args.no_e2e:
-        eng = new_engine()
-        if trainer is not None:
-            eng.W.copy_(trainer)
-        eng.load_policy_weights(0)
-        n0 = N_PROMPTS_PER_EPOCH * world
-        eng.submit_prompts(ids[:n0], off[:n0 + 1], toks[:off[n0]], L[:n0])
-        st2 = {"useful": 0, "d2h": 0, "v": 0}
-        drive(eng, args.precondition + args.warmup, st2)
-        st2["d2h"] = 0
-        # pinned host copies of the next epoch's prompts (the dataloader's batch)
-        import torch as _t
-        rest_off = (off[n0:] - off[n0]).astype(np.int32)
-        rest_tok = _t.from_numpy(toks[off[n0]:].copy()).pin_memory().numpy()
-        rest_len = _t.from_numpy(L[n0:].copy()).pin_memory().numpy()
+    if not args.no_e2e and st["sub"] < n_prompts:
+        U = sched.U
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+        toks_p, L_p, ids_p = pin(toks), pin(L), pin(ids)
+        k_e2e = max(1, min(args.steps, 3))
         c0 = eng.counters()
+        h2d = 0
+        d0 = st["d2h"]
+        n0 = len(trace)
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        eng.submit_prompts(ids[n0:], rest_off, rest_tok, rest_len)
-        h2d = rest_tok.nbytes + rest_off.nbytes + rest_len.nbytes + (len(ids) - n0) * 72
-        ran2 = drive(eng, args.steps, st2)
+        w0 = time.perf_counter()
+        for _ in range(k_e2e):
+            lo, hi = st["sub"], min(n_prompts, st["sub"] + U * world)
+            if hi > lo:
+                o = off[lo:hi + 1]
+                eng.submit_prompts(ids_p[lo:hi], (o - o[0]).astype(np.int32), toks_p[o[0]:o[-1]], L_p[lo:hi])
+                st["sub"] = hi
+                h2d += (o[-1] - o[0]) * 4 + (hi - lo) * (8 + 4 + 4) + 4
+            one_round()
         torch.cuda.synchronize()
-        t1 = time.perf_counter()
+        w1 = time.perf_counter()
         if dist:
             dist.barrier()
         c1 = eng.counters()
-        raw2 = c1["raw_tokens"] - c0["raw_tokens"]
-        d2h = st2["d2h"] + ran2 * 48          # per-step status/info readbacks + harvested groups
-        e2e = {"value": raw2 / (t1 - t0), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d / max(1, ran2)),
-               "d2h_bytes_per_step": int(d2h / max(1, ran2)), "wall_ms_per_step": (t1 - t0) * 1e3 / max(1, ran2)}
-        eng.close()
-        del eng
-    return dict(ms=ms, ran=ran, raw=raw, useful=useful, stats=stats, prof=prof, launches=launches,
-                clocks=clk.summary(), e2e=e2e)
+        n_steps = max(1, len(trace) - n0)
+        d2h = st["d2h"] - d0 + n_steps * 2 * 96          # harvested groups + per-step status readbacks
+        e2e = {"value": (c1["raw_tokens"] - c0["raw_tokens"]) / (w1 - w0), "unit": "tokens/s",
+               "h2d_bytes_per_step": int(h2d / k_e2e), "d2h_bytes_per_step": int(d2h / k_e2e),
+               "wall_ms_per_step": (w1 - w0) * 1e3 / k_e2e, "steps": k_e2e,
+               "step": "one early-update round (see config.step)"}
+    eng.close()
+    del eng
+    return dict(ms=ms, ran=ran, raw=raw / world, useful=useful / world, stats=stats, prof=prof, launches=launches,
+                clocks=clk.summary(), e2e=e2e, trace=trace, breakdown=breakdown, n_break=n_break)
 
 
 # ------------------------------------------------------------------ CPU oracle sample
@@ -324,9 +355,10 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=40)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--precondition", type=int, default=600)
+    ap.add_argument("--steps", type=int, default=3, help="timed early-update rounds")
+    ap.add_argument("--warmup", type=int, default=3, help="untimed rounds before them")
+    ap.add_argument("--precondition", type=int, default=1500,
+                    help="untimed decode steps first, so contexts are mid-rollout")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -346,71 +378,77 @@ def main():
     r = run_gpu(args, rank, world, dist)
     m = LLAMA8B
     hbm, tf_burst, tf_sust, peak_src = load_peaks()
-    # per-rank aggregates
-    sum_ctx = sum(s[1] for s in r["stats"])
+    # per-rank aggregates over the timed rounds
+    stats = r["stats"]
+    sum_ctx = sum(x[1] for x in stats)
     steps = r["ran"]
+    n_dec = len(stats)
+    m = LLAMA8B
     attn_ms, attn_n = r["prof"]["attention"]
-    # dominant kernel class (decode path)
-    dec = {k: v for k, v in r["prof"].items()
-           if k in ("attention", "gemm_qkv", "gemm_o", "gemm_gate_up", "gemm_down", "lm_head")}
-    dom = max(dec, key=lambda k: dec[k][0])
-    if dom == "attention":
-        per_unit = 2 * m.Hkv * m.dh * 2                         # K+V bytes per context token per layer
-        units = sum_ctx                                          # context tokens over all timed steps (per layer)
-        bytes_tot = per_unit * units * m.L
-        achieved = bytes_tot / (attn_ms * 1e-3) / 1e9
-        roof = {"bound": "hbm", "kernel": "paged_attention", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None, "per_unit_bytes": per_unit,
-                "units_per_launch": units / max(1, steps), "launches": attn_n, "peak_source": peak_src}
-    else:
-        Nk = {"gemm_qkv": ((m.Hq + 2 * m.Hkv) * m.dh, m.d), "gemm_o": (m.d, m.Hq * m.dh),
-              "gemm_gate_up": (2 * m.ff, m.d), "gemm_down": (m.d, m.ff), "lm_head": (m.V, m.d)}[dom]
-        launches_per_step = 1 if dom == "lm_head" else m.L
-        bytes_tot = Nk[0] * Nk[1] * 2 * launches_per_step * steps
-        achieved = bytes_tot / (dec[dom][0] * 1e-3) / 1e9
-        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None, "launches": dec[dom][1], "peak_source": peak_src}
+    # dominant kernel: paged attention (bracketed alone in the timed rounds; the
+    # breakdown round confirms it is the largest class)
+    per_unit = 2 * m.Hkv * m.dh * 2                             # K+V bytes per context token per layer
+    units = sum_ctx                                              # context tokens read per layer, all timed steps
+    achieved = per_unit * units * m.L / (attn_ms * 1e-3) / 1e9 if attn_ms > 0 else None
+    roof = {"bound": "hbm", "kernel": "attn_bf16_kernel (paged GQA decode attention)", "achieved": achieved,
+            "peak": hbm, "unit": "GB/s", "frac": achieved / hbm if achieved else None, "traffic": None,
+            "per_unit_bytes": per_unit, "unit_def": "one context token of one layer (K+V, bf16)",
+            "units_per_launch": units / max(1, n_dec), "launches": attn_n, "peak_source": peak_src}
     # decode roofline fraction of the whole step
     t_roof = 0.0
-    for (rk, sc, dt, npre, nfin, rl) in r["stats"]:
-        B, F, _, _ = step_bytes_flops(m, rl, sc)             # this GPU's rows and context
+    for (rk, sc, dt, npre, nfin, rl) in stats:
+        B, F, _, _ = step_bytes_flops(m, rl, sc)                 # this GPU's rows and context
         t_roof += max(B / (hbm * 1e9), F / (tf_sust * 1e12))
     dec_frac = t_roof / (r["ms"] * 1e-3)
     tok_s = r["raw"] / (r["ms"] * 1e-3)
-    Q = 256 * world                                          # Q_tot (reading R1)
-    bubble = sum(Q - s[0] for s in r["stats"]) / (Q * max(1, len(r["stats"])))
-    dts = [s[2] for s in r["stats"]]
-    bubble_t = sum((Q - s[0]) * s[2] for s in r["stats"]) / (Q * max(1e-9, sum(dts)))
+    Q = 256 * world                                              # Q_tot (reading R1)
+
+    def bubble(tr):
+        if not tr:
+            return None, None
+        ab = sum(Q - x[0] for x in tr) / (Q * len(tr))
+        tw = sum((Q - x[0]) * x[2] for x in tr) / (Q * max(1e-9, sum(x[2] for x in tr)))
+        return ab, tw
+    b_win, b_win_t = bubble(stats)
+    b_all, b_all_t = bubble(r["trace"])
     if dist:
-        # raw tokens: the replicated counter counts every replica's tokens, so each
-        # rank contributes its own rows only (raw / world on every rank, exact in
-        # lockstep since the counter is global); useful likewise
-        tok_s, useful_s, ms = aggregate_over_ranks(dist, r["raw"] / world, r["useful"] / world, r["ms"])
+        tok_s, useful_s, ms = aggregate_over_ranks(dist, r["raw"], r["useful"], r["ms"])
     else:
         useful_s = r["useful"] / (r["ms"] * 1e-3)
         ms = r["ms"]
     if rank != 0:
         dist.barrier() if dist else None
         return
+    nb = max(1, r["n_break"])
     line = {
         "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": world, "steps": steps,
         "warmup": args.warmup, "ms_per_step": ms / max(1, steps), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "window": f"decode steps [{args.precondition + args.warmup}, "
-                   f"{args.precondition + args.warmup + steps}) of the cfg2 rollout",
-                   "l2": "no flush needed: every step streams 15 GB of weights + the KV cache (>> 126 MB L2)",
+        "config": {"workload": WORKLOAD,
+                   "step": "one early-update round: decode steps (refill, prefill, decode GEMMs, paged attention, "
+                           "Philox sampling, stop detection, compaction) until the length-sorted update group of "
+                           "U=64 is ready, its harvest, and the policy refresh (load_policy_weights, K bound)",
+                   "window": f"after {args.precondition} untimed decode steps and {args.warmup} untimed rounds; "
+                             f"{n_dec} decode steps timed",
+                   "l2": "no flush needed: every decode step streams 15 GB of weights + the KV cache (>> 126 MB L2)",
                    "parallelism": f"dp{world} lockstep replicas (NCCL)" if world > 1 else "dp1"},
+        "decode_steps": n_dec,
+        "ms_per_decode_step": ms / max(1, n_dec),
         "useful_tokens_per_s": useful_s,
-        "bubble_ratio": {"window_abstract": bubble, "window_time_weighted": bubble_t,
-                         "definition": "Eq.(bubble) P:339-342 over the timed decode steps, Q=Q_g"},
+        "bubble_ratio": {"window_abstract": b_win, "window_time_weighted": b_win_t,
+                         "since_start_abstract": b_all, "since_start_time_weighted": b_all_t,
+                         "since_start_steps": len(r["trace"]),
+                         "definition": "Eq.(bubble) P:339-342, Q = Q_tot; abstract (dt=1) and measured dt"},
         "decode_roofline_frac": {"value": dec_frac, "definition": "sum_k max(B_k/BW, F_k/TC) / sum_k dt_k (SURVEY 8(d))",
                                  "BW_GBs": hbm, "TC_TFs": tf_sust},
         "roofline": roof,
-        "kernel_ms_per_step": {k: v[0] / max(1, steps) for k, v in r["prof"].items()},
+        "kernel_ms_per_decode_step": {k: v[0] / nb for k, v in r["breakdown"].items()},
+        "kernel_breakdown_note": "one extra round with every class bracketed by CUDA events (which also cut the "
+                                 "decode graph's PDL edges); not part of the timed value",
         "gpu_launches": r["launches"],
         "clocks": r["clocks"],
         "e2e": r["e2e"],
-        "mean_ctx": sum_ctx / max(1, sum(s[5] for s in r["stats"])),
+        "mean_ctx": sum_ctx / max(1, sum(x[5] for x in stats)),
     }
     if not args.no_cpu and world == 1:
         line["cpu_baseline"] = oracle_sample()

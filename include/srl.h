@@ -242,8 +242,13 @@ int32_t srl_get_counters(srl_engine* e, int64_t* raw_tokens, int64_t* discarded_
 /* Change K between updates (SRL_E_STATE while a group is pending). */
 int32_t srl_set_cache_bound(srl_engine* e, int32_t K);
 
-/* Enable (1) / disable (0) per-class timing; enabling resets the accumulators. */
+/* Enable (1) / disable (0) per-class timing; enabling resets the accumulators.
+ * Only the classes in the profile mask (bit SRL_K_*; default all) are bracketed
+ * by CUDA events.  Event records sit between kernels, so they also cut the
+ * programmatic (PDL) edges of the decode graph: with profiling off the graph
+ * holds no events at all.  Changing either setting recaptures the graph. */
 int32_t srl_set_profiling(srl_engine* e, int32_t on);
+int32_t srl_set_profile_mask(srl_engine* e, uint32_t class_mask);
 /* ms[SRL_K_NCLASS]: accumulated device milliseconds per class over decode steps
  * (prefill passes are accumulated whole under SRL_K_PREFILL); launches[]: launch counts. */
 int32_t srl_get_profile(srl_engine* e, double* ms, int64_t* launches);

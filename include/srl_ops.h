@@ -33,8 +33,11 @@ extern "C" {
  * epi | SRL_GEMM_W_PACKED: W is in the packed layout written by srl_op_pack_weight
  *   (for epi 2: the packed image of the interleaved [2N, K] matrix) instead of
  *   row-major; the weight stream then moves contiguous 16 KB blocks.
- * workspace: device bytes >= srl_op_gemm_workspace(M, N, K, epi) (currently
- *   unused by the kernel; kept so callers need not change if a variant needs it).
+ * workspace: device bytes >= srl_op_gemm_workspace(M, N, K, epi), ZERO-FILLED
+ *   before its first use and not shared by concurrent launches; every launch
+ *   leaves it zeroed.  It holds the stream-K fp32 partial slots and per-unit
+ *   arrival counters (M >= 128, when whole units would leave SM pairs idle);
+ *   NULL disables stream-K.
  * Requires K % 64 == 0 and, for epi 2, N % 64 == 0. */
 #define SRL_GEMM_W_PACKED 0x100
 int64_t srl_op_gemm_workspace(int32_t M, int32_t N, int32_t K, int32_t epi);

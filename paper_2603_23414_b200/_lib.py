@@ -89,6 +89,7 @@ SIGNATURES = {
     "srl_set_cache_bound": (_I32, [_P, _I32]),
     "srl_debug_copy_logits": (_I32, [_P, _P, _I64]),
     "srl_set_profiling": (_I32, [_P, _I32]),
+    "srl_set_profile_mask": (_I32, [_P, C.c_uint32]),
     "srl_get_profile": (_I32, [_P, C.POINTER(C.c_double), _I64P]),
     "srl_nccl_unique_id": (_I32, [_P]),
     "srl_local_group_create": (_I32, [_I32, C.POINTER(_P)]),

@@ -15,6 +15,7 @@
 // attn_combine in chunk order.
 // fp32 KV (test mode): a plain FFMA kernel with the same item/partial format.
 #include "common.cuh"
+#include "launch.hpp"
 #include "layers.hpp"
 #include "tma.hpp"
 
@@ -30,6 +31,8 @@ constexpr int kMinItems = 4 * 148;
 __global__ void attn_plan_kernel(AttnArgs a, int split) {
   __shared__ int wsum[32];
   __shared__ int base_s, active_s;
+  pdl_trigger();
+  pdl_wait();
   if (threadIdx.x == 0) {
     base_s = 0;
     active_s = 0;
@@ -96,6 +99,8 @@ int attn_max_items(int M, int Hkv, int max_ctx) {
 // ---------------------------------------------------------------- combine
 template <bool F32OUT>
 __global__ void attn_combine_kernel(AttnArgs a, float* out_f32) {
+  pdl_trigger();
+  pdl_wait();
   const int G = a.Hq / a.Hkv;
   const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -136,6 +141,8 @@ __global__ void attn_combine_kernel(AttnArgs a, float* out_f32) {
 constexpr int kF32Threads = 128;
 __global__ void __launch_bounds__(kF32Threads) attn_f32_kernel(AttnArgs a) {
   extern __shared__ float sm[];
+  pdl_trigger();
+  pdl_wait();
   const int G = a.Hq / a.Hkv;
   const int chunk_tok = 64 * kChunkPages;
   float* sq = sm;                       // [G][dh]
@@ -282,6 +289,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stages = smem;
   float* mrg = reinterpret_cast<float*>(stages + kStages * C::kStageBytes);  // [4 warps][8 q][DH + 2]
+  pdl_trigger();
+  pdl_wait();
   uint64_t* full = reinterpret_cast<uint64_t*>(mrg + kConsumerWarps * 8 * (DH + 2));
   uint64_t* empty = full + kStages;
 
@@ -470,12 +479,12 @@ static void launch_bf16(const AttnArgs& a, const void* tk, const void* tv, cudaS
   int grid = 148;
   const int occ = (int)((228 * 1024) / (smem + 1024));
   grid *= occ < 1 ? 1 : occ;
-  attn_bf16_kernel<DH><<<grid, kAttnThreads, smem, st>>>(a, *reinterpret_cast<const CUtensorMap*>(tk),
-                                                          *reinterpret_cast<const CUtensorMap*>(tv));
+  launch_k(attn_bf16_kernel<DH>, dim3(grid), dim3(kAttnThreads), smem, st, 1, a, *reinterpret_cast<const CUtensorMap*>(tk),
+           *reinterpret_cast<const CUtensorMap*>(tv));
 }
 
 void attn_plan(const AttnArgs& a, int split, cudaStream_t st) {
-  attn_plan_kernel<<<1, 1024, 0, st>>>(a, split);
+  launch_k(attn_plan_kernel, dim3(1), dim3(1024), 0, st, 1, a, split);
 }
 
 void attn_run(const AttnArgs& a, bool kv_fp32, const void* tmap_k, const void* tmap_v, cudaStream_t st) {
@@ -483,7 +492,7 @@ void attn_run(const AttnArgs& a, bool kv_fp32, const void* tmap_k, const void* t
   if (kv_fp32) {
     const int G = a.Hq / a.Hkv;
     const size_t smem = (size_t)G * a.dh * 4 + (size_t)G * 64 * kChunkPages * 4;
-    attn_f32_kernel<<<148 * 4, kF32Threads, smem, st>>>(a);
+    launch_k(attn_f32_kernel, dim3(148 * 4), dim3(kF32Threads), smem, st, 1, a);
   } else {
     switch (a.dh) {
       case 128: launch_bf16<128>(a, tmap_k, tmap_v, st); break;
@@ -493,12 +502,12 @@ void attn_run(const AttnArgs& a, bool kv_fp32, const void* tmap_k, const void* t
     }
   }
   const int warps = a.M * a.Hq;
-  attn_combine_kernel<false><<<(warps + 7) / 8, 256, 0, st>>>(a, nullptr);
+  launch_k(attn_combine_kernel<false>, dim3((warps + 7) / 8), dim3(256), 0, st, 1, a, (float*)nullptr);
 }
 
 void attn_combine_f32(const AttnArgs& a, float* out_f32, cudaStream_t st) {
   const int warps = a.M * a.Hq;
-  attn_combine_kernel<true><<<(warps + 7) / 8, 256, 0, st>>>(a, out_f32);
+  launch_k(attn_combine_kernel<true>, dim3((warps + 7) / 8), dim3(256), 0, st, 1, a, out_f32);
 }
 
 }  // namespace srl

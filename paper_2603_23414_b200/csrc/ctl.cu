@@ -18,6 +18,7 @@
 // admission / page-growth loops (a handful of items per step) run on one
 // thread, in ascending slot order, exactly as the oracle specifies.
 #include "common.cuh"
+#include "launch.hpp"
 #include "engine.hpp"
 
 namespace srl {
@@ -497,6 +498,8 @@ __global__ void __launch_bounds__(kCtlThreads, 1) ctl_end_kernel(Ctl c) {
   extern __shared__ long long keys[];
   __shared__ int sh_fin[1024];
   __shared__ int sh_nfin_total;
+  pdl_trigger();
+  pdl_wait();
   CtlState* s = c.s;
   const int v = s->v;
   if (threadIdx.x == 0) sh_nfin_total = 0;
@@ -718,7 +721,7 @@ __global__ void ctl_submit_kernel(Ctl c, int n_traj, int n_prompts) {
 static size_t sort_smem() { return (size_t)kMaxSortReady * sizeof(long long); }
 
 void ctl_begin(const Ctl& c, cudaStream_t st) { ctl_begin_kernel<<<1, kCtlThreads, sort_smem(), st>>>(c); }
-void ctl_end(const Ctl& c, cudaStream_t st) { ctl_end_kernel<<<1, kCtlThreads, sort_smem(), st>>>(c); }
+void ctl_end(const Ctl& c, cudaStream_t st) { launch_k(ctl_end_kernel, dim3(1), dim3(kCtlThreads), sort_smem(), st, 1, c); }
 void ctl_bump(const Ctl& c, int version, cudaStream_t st) {
   ctl_bump_kernel<<<1, kCtlThreads, sort_smem(), st>>>(c, version);
 }

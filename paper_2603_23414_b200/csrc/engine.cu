@@ -25,6 +25,7 @@ using namespace srl;
 namespace {
 
 constexpr size_t kAlign = 1024;
+constexpr int kMaxSmsPlan = 160;  // GEMM workspace sized for up to this many SMs
 inline size_t al(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct LayerW {
@@ -204,6 +205,8 @@ struct srl_engine {
   float* logits = nullptr;
   float *rope_cos = nullptr, *rope_sin = nullptr;
   int* row_slot_id = nullptr;  // identity rows 0..Q_g-1
+  void* gemm_ws = nullptr;     // GEMM stream-K workspace (zeroed at create, left zeroed by every launch)
+  size_t gemm_ws_bytes = 0;
   AttnArgs attn{};
   Ctl ctl{};
   CtlStatus* hst = nullptr;  // pinned
@@ -225,6 +228,8 @@ struct srl_engine {
     std::vector<int> cls, nl;
   };
   bool prof = false;
+  uint32_t prof_mask = 0xffffffffu;  // classes bracketed while profiling
+  uint32_t graph_mask = 0;           // classes bracketed inside the captured graph
   bool capturing = false;
   EvSet direct, gset;
   double prof_ms[SRL_K_NCLASS] = {0};
@@ -247,8 +252,10 @@ struct Prof {
   int nl;
   Prof(srl_engine* e_, int cls_, int nlaunch = 1) : e(e_), cls(cls_), nl(nlaunch) {
     if (cls < 0) return;
-    S = e->capturing ? &e->gset : (e->prof ? &e->direct : nullptr);
-    if (!S) return;
+    // Only profiled classes get event records: an event node between two kernels
+    // of the captured graph replaces their programmatic (PDL) edge by a full one.
+    if (!e->prof || !((e->prof_mask >> cls) & 1u)) return;
+    S = e->capturing ? &e->gset : &e->direct;
     if (S->used + 2 > S->ev.size()) {
       for (int i = 0; i < 256; ++i) {
         cudaEvent_t ev;
@@ -342,6 +349,8 @@ void plan_scratch(srl_engine* e, ScratchPlan& p, bool assign) {
   c.h_ver = (int*)P(4ull * z.h_cap_tok);
   c.h_rec = (srl_traj*)P(sizeof(srl_traj) * kMaxGroup);
   e->row_slot_id = (int*)P(4 * z.Q_g);
+  e->gemm_ws_bytes = gemm_workspace_bytes(kMaxSmsPlan);
+  e->gemm_ws = P(e->gemm_ws_bytes);
   e->x_res = (float*)P(4ull * z.mmax * m.d);
   e->xn = (__nv_bfloat16*)P(2ull * z.mmax * m.d);
   e->attn_out = (__nv_bfloat16*)P(2ull * z.mmax * m.Hq * m.dh);
@@ -416,13 +425,16 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
   qe.dh = m.dh;
   qe.kv_f32 = e->kv_f32 ? 1 : 0;
   qe.w_packed = 1;
+  qe.ws = e->gemm_ws;
   GemmEpi re{};
   re.w_packed = 1;
+  re.ws = e->gemm_ws;
   re.kind = EPI_RESID;
   re.x_res = e->x_res;
   re.ldo = d;
   GemmEpi se{};
   se.w_packed = 1;
+  se.ws = e->gemm_ws;
   se.kind = EPI_SILU;
   se.act = e->act;
   se.ldo = m.ff;
@@ -458,6 +470,7 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
     fe.out_f32 = e->logits;
     fe.ldo = m.V;
     fe.w_packed = 1;
+    fe.ws = e->gemm_ws;
     run_gemm(e, SRL_K_LM_HEAD, e->xn, M, (const __nv_bfloat16*)e->plm_head, m.V, d, fe);
   }
 }
@@ -667,6 +680,7 @@ int32_t srl_create(const srl_model_cfg* m, const srl_sched_cfg* s, int32_t devic
   e->prompt_tok_cap = (long long)e->z.max_prompts * s->max_prompt;
   // init device state
   cudaMemsetAsync(e->KV, 0, mem->kv_bytes, e->st);  // finite values in never-written KV rows
+  cudaMemsetAsync(e->gemm_ws, 0, e->gemm_ws_bytes, e->st);
   std::vector<int> ident(s->Q_g);
   for (int i = 0; i < s->Q_g; ++i) ident[i] = i;
   cudaMemcpyAsync(e->row_slot_id, ident.data(), 4 * s->Q_g, cudaMemcpyHostToDevice, e->st);
@@ -798,6 +812,7 @@ int32_t srl_decode_step(srl_engine* e, srl_step_info* info) {
   // launch sequence, replayed from a CUDA graph after the first step.
   if (e->use_graph && e->direct_steps >= 1 && !e->gexec) {
     const long long l0 = e->launches;
+    e->graph_mask = e->prof ? e->prof_mask : 0u;
     cudaGraph_t g = nullptr;
     e->capturing = true;
     bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
@@ -976,9 +991,31 @@ int32_t srl_get_counters(srl_engine* e, int64_t* raw, int64_t* disc, int64_t* em
   return SRL_OK;
 }
 
+static void drop_graph_if_stale(srl_engine* e) {
+  // the captured decode graph carries the event nodes of the classes profiled at
+  // capture time: recapture when that set changes
+  const uint32_t want = e->prof ? e->prof_mask : 0u;
+  if (e->gexec && want != e->graph_mask) {
+    cudaStreamSynchronize(e->st);
+    cudaGraphExecDestroy(e->gexec);
+    e->gexec = nullptr;
+    e->gset.cls.clear();
+    e->gset.nl.clear();
+    e->gset.used = 0;
+  }
+}
+
+int32_t srl_set_profile_mask(srl_engine* e, uint32_t class_mask) {
+  if (!e) return fail(SRL_E_INVALID_ARG, "srl_set_profile_mask: null engine");
+  e->prof_mask = class_mask;
+  drop_graph_if_stale(e);
+  return SRL_OK;
+}
+
 int32_t srl_set_profiling(srl_engine* e, int32_t on) {
   if (!e) return fail(SRL_E_INVALID_ARG, "srl_set_profiling: null engine");
   e->prof = on != 0;
+  drop_graph_if_stale(e);
   for (int i = 0; i < SRL_K_NCLASS; ++i) {
     e->prof_ms[i] = 0;
     e->prof_launch[i] = 0;

@@ -17,12 +17,19 @@
 // CTAs' epilogue warps arrive on the leader's "tempty".  Each CTA's TMEM holds
 // its 128 rows x N accumulator and it runs the same fused epilogues.
 //
-// Decomposition: persistent pairs over pair units when there are enough units;
-// otherwise split-K over the S pairs of a (2S)-CTA cluster, with a push-style
-// reduction: every CTA sends each 16-column chunk of its partial to the CTA
-// (same row half) that owns the chunk, straight into that CTA's shared memory
-// (st.shared::cluster), and the owner sums the S partials in pair (= k) order
-// from local memory: fire-and-forget remote stores instead of remote loads.
+// Decomposition (SPLIT; host selection and measurements in gemm_tc.cu):
+//  0  persistent pairs, whole pair units round-robin (gate/up, LM head, prefill);
+//  1  split-K over the S pairs of a (2S)-CTA cluster (decode QKV / O / down):
+//     every CTA pushes each 16-column chunk of its fp32 partial straight into the
+//     shared memory of the CTA (same row half) that owns the chunk
+//     (st.shared::cluster, fire-and-forget), and the owner sums the S partials
+//     in pair (= k) order from local memory -- deterministic;
+//  2  stream-K (opt-in, SRL_GEMM_SPLIT=2): the flattened (unit, k-block) space
+//     is cut into #pairs equal ranges; a unit cut between pairs is finished by
+//     its LAST arriving piece: every piece stores its fp32 partial to an
+//     L2-resident workspace slot and bumps the unit's counter, and the CTA
+//     completing the count sums all pieces in k order and runs the epilogue.
+//     Nobody waits on another CTA, so co-residency is never assumed.
 
 SRL_DEV uint32_t mapa_u32(uint32_t local_addr, uint32_t rank) {
   uint32_t r;
@@ -69,6 +76,43 @@ SRL_DEV void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
   asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
 }
 
+// stream-K: first flattened k-block of pair q's range
+__device__ __forceinline__ long long sk_bound(const GemmParams& p, int q) {
+  return (long long)q * p.sk_total / p.sk_pairs;
+}
+// piece i of pair `pid` (unit, k0, k1); *n = piece count when i < 0
+__device__ __forceinline__ Seg sk_piece(const GemmParams& p, int pid, int i, int* n = nullptr) {
+  long long g = sk_bound(p, pid);
+  const long long e = sk_bound(p, pid + 1);
+  Seg sg{0, 0, 0};
+  int j = 0;
+  while (g < e) {
+    sg.u = (int)(g / p.kb);
+    sg.k0 = (int)(g - (long long)sg.u * p.kb);
+    sg.k1 = (int)min((long long)p.kb, sg.k0 + (e - g));
+    if (j == i) return sg;
+    g += sg.k1 - sg.k0;
+    ++j;
+  }
+  if (n) *n = j;
+  return sg;
+}
+// workspace slot of pair q's piece of unit u: 2q for its first piece, 2q + 1 for a later one
+__device__ __forceinline__ int sk_slot(const GemmParams& p, int q, int u) {
+  return 2 * q + (sk_bound(p, q) >= (long long)u * p.kb ? 0 : 1);
+}
+// pairs whose ranges intersect unit u: [*q0, *q1]
+__device__ __forceinline__ void sk_unit_pairs(const GemmParams& p, int u, int* q0, int* q1) {
+  const long long a = (long long)u * p.kb, b = a + p.kb - 1;
+  int q = (int)(a * p.sk_pairs / p.sk_total);
+  while (q > 0 && sk_bound(p, q) > a) --q;
+  while (q + 1 < p.sk_pairs && sk_bound(p, q + 1) <= a) ++q;
+  *q0 = q;
+  while (q + 1 < p.sk_pairs && sk_bound(p, q + 1) <= b) ++q;
+  *q1 = q;
+}
+__device__ __forceinline__ float4 ldcg_f4(const float4* a) { return __ldcg(a); }
+
 // pair unit u -> (pair tile, batch block); pair tile t covers weight rows 256t..256t+255
 template <int SPLIT>
 __global__ void __launch_bounds__(kGemmThreads, 1)
@@ -98,11 +142,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   //        else  -> pair id, round-robin over pair units
   const int npairs = gridDim.x >> 1;
   const int pid = blockIdx.x >> 1;
-  const int cl = SPLIT ? (int)(blockIdx.x / (2 * p.S)) : 0;
-  const int pi = SPLIT ? (int)(rank >> 1) : 0;
-  const int nseg = SPLIT ? 1 : (pid < p.units ? (p.units - pid + npairs - 1) / npairs : 0);
-  auto unit_of = [&](int i) { return SPLIT ? cl : pid + i * npairs; };
-  const int k0 = SPLIT ? pi * p.kb / p.S : 0, k1 = SPLIT ? (pi + 1) * p.kb / p.S : p.kb;
+  const int cl = SPLIT == 1 ? (int)(blockIdx.x / (2 * p.S)) : 0;
+  const int pi = SPLIT == 1 ? (int)(rank >> 1) : 0;
+  int nseg;
+  if (SPLIT == 1) nseg = 1;
+  else if (SPLIT == 2) sk_piece(p, pid, -1, &nseg);
+  else nseg = pid < p.units ? (p.units - pid + npairs - 1) / npairs : 0;
+  // piece i of this pair: (unit, k-block range)
+  auto piece = [&](int i) -> Seg {
+    if (SPLIT == 2) return sk_piece(p, pid, i);
+    if (SPLIT == 1) return Seg{cl, pi * p.kb / p.S, (pi + 1) * p.kb / p.S};
+    return Seg{pid + i * npairs, 0, p.kb};
+  };
+  pdl_trigger();
 
   if (threadIdx.x == 0) {
     DBG(0);
@@ -128,18 +180,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_after();
   const uint32_t tbase = *tholder;
   if (threadIdx.x == 0) DBG(1);
+  if (w != 0) pdl_wait();  // PDL: only the (constant) weight stream runs ahead of the predecessor
 
   if (w == 0) {
     if (lane == 0) {
-      const uint64_t pol_w = policy_evict_first();
+      const uint64_t pol_w = p.w_shared ? policy_evict_normal() : policy_evict_first();
       const uint32_t full_l = mapa_u32(smem_u32(full), leader);
       int s = 0;
       uint32_t ph = 1;
       bool first = true;
       for (int i = 0; i < nseg; ++i) {
-        const int u = unit_of(i);
+        const Seg sg = piece(i);
+        const int u = sg.u;
         const int t128 = (u % p.n_tiles) * 2 + (int)r2;  // this CTA's 128-row tile
-        for (int k = k0; k < k1; ++k) {
+        for (int k = sg.k0; k < sg.k1; ++k) {
           mbar_wait(&empty[s], ph);
           if (is_leader) mbar_arrive_expect_tx(&full[s], 2 * kStageA);  // both CTAs' halves
           const int c1 = p.wp ? (t128 * p.kb + k) * 128 : t128 * 128;
@@ -164,10 +218,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int s = 0;
       uint32_t ph = 1;
       for (int i = 0; i < nseg; ++i) {
-        const int u = unit_of(i);
+        const Seg sg = piece(i);
+        const int u = sg.u;
         const int ncol = unit_cols(p, u);
         const int mrow = (u / p.n_tiles) * p.m_blk + (int)r2 * (ncol >> 1);
-        for (int k = k0; k < k1; ++k) {
+        for (int k = sg.k0; k < sg.k1; ++k) {
           mbar_wait(&xempty[s], ph);
           if (is_leader) mbar_arrive_expect_tx(&xfull[s], 2 * stage_b);
           tma_load_2d_pair(sB + s * stage_b, &tmX, xfull_l + 8u * s, k * 64, mrow, pol_x);
@@ -186,14 +241,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t ph = 0, phx = 0;
       bool first = true;
       for (int i = 0; i < nseg; ++i) {
-        const int u = unit_of(i);
+        const Seg sg = piece(i);
+        const int u = sg.u;
         const uint32_t idesc = umma_idesc_bf16(256, unit_cols(p, u));
         const int a = i % p.acc_stages;
         mbar_wait(&tempty[a], ((i / p.acc_stages) & 1) ^ 1);
         tc_fence_after();
         const uint32_t tacc = tbase + (uint32_t)(a * p.m_blk);
         uint32_t acc = 0;
-        for (int k = k0; k < k1; ++k) {
+        for (int k = sg.k0; k < sg.k1; ++k) {
           mbar_wait(&full[s], ph);
           mbar_wait(&xfull[sx], phx);
           tc_fence_after();
@@ -223,36 +279,91 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       DBG(5);
     }
     __syncwarp();
-  } else if (!SPLIT) {
+  } else if (SPLIT != 1) {
     // ------------------------------ epilogue warps (2..9): TMEM -> fused op
     const int qw = w & 3, n = qw * 32 + lane, eg = (w - 2) >> 2;
     float* xg = xch + eg * kXchFloats;
     const uint32_t tempty_l = mapa_u32(smem_u32(tempty), leader);
+    volatile int& sh_last = *reinterpret_cast<volatile int*>(tholder + 2);  // (static smem would cap the dynamic 227 KB)
+    const int cmax = p.m_blk >> 4;
     for (int i = 0; i < nseg; ++i) {
-      const int u = unit_of(i);
+      const Seg sg = piece(i);
+      const int u = sg.u;
       const int unit_n0 = (u % p.n_tiles) * 256 + (int)r2 * 128, m_base = (u / p.n_tiles) * p.m_blk;
-      const int ncol = unit_cols(p, u);
+      const int ncol = unit_cols(p, u), nchunk = ncol >> 4;
       const int a = i % p.acc_stages;
+      const bool whole = sg.k0 == 0 && sg.k1 == p.kb;
       fill_row_table(p, m_base, ncol, rtab, (int)threadIdx.x - 64);  // overlaps the MMAs
       mbar_wait(&tfull[a], (i / p.acc_stages) & 1);
       tc_fence_after();
       if (lane == 0 && qw == 0 && i < 3) DBG(6 + i);
-      if (unit_n0 < p.N) {
-        const uint32_t tl = tbase + ((uint32_t)(qw * 32) << 16) + (uint32_t)(a * p.m_blk);
-        for (int cc = eg * 16; cc < ncol; cc += 32) {
-          float v[16];
-          tmem_ld16(tl + cc, v);
-          apply_epilogue(p, unit_n0, n, m_base + cc, v, xg, 1 + eg, rtab + cc);
+      const uint32_t tl = tbase + ((uint32_t)(qw * 32) << 16) + (uint32_t)(a * p.m_blk);
+      if (whole) {
+        if (unit_n0 < p.N) {
+          for (int cc = eg * 16; cc < ncol; cc += 32) {
+            float v[16];
+            tmem_ld16(tl + cc, v);
+            apply_epilogue(p, unit_n0, n, m_base + cc, v, xg, 1 + eg, rtab + cc);
+          }
         }
+      } else {
+        // stream-K piece of a split unit: fp32 partial -> workspace slot (layout
+        // [slot][row half][chunk][4 column quads][128 rows] float4, coalesced per warp)
+        float4* dst = reinterpret_cast<float4*>(p.sk_ws) +
+                      ((size_t)(sk_slot(p, pid, u) * 2 + (int)r2) * cmax) * 512 + n;
+        for (int c = eg; c < nchunk; c += 2) {
+          float v[16];
+          tmem_ld16(tl + (uint32_t)(c * 16), v);
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4)
+            __stcg(dst + (size_t)c * 512 + q4 * 128, make_float4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]));
+        }
+        __threadfence();  // this thread's partial is visible device-wide before the count
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty_l + 8u * a);
+      if (lane == 0) mbar_arrive_cluster(tempty_l + 8u * a);  // TMEM buffer free: the next piece may accumulate
       if (lane == 0 && qw == 0 && i < 3) DBG(9 + i);
+      if (!whole) {
+        // count the piece in; the CTA completing the count reduces the unit (this row half)
+        int q0, q1;
+        sk_unit_pairs(p, u, &q0, &q1);
+        asm volatile("bar.sync 4, 256;" ::: "memory");
+        if (w == 2 && lane == 0) {
+          __threadfence();
+          const int old = atomicAdd(p.sk_cnt + 2 * u + (int)r2, 1);
+          sh_last = old == q1 - q0;
+          if (sh_last) {
+            p.sk_cnt[2 * u + (int)r2] = 0;  // ready for the next launch
+            __threadfence();
+          }
+        }
+        asm volatile("bar.sync 4, 256;" ::: "memory");
+        if (sh_last && unit_n0 < p.N) {
+          for (int c = eg; c < nchunk; c += 2) {
+            float v[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = 0.f;
+            for (int q = q0; q <= q1; ++q) {  // pair order = k order: deterministic
+              const float4* src = reinterpret_cast<const float4*>(p.sk_ws) +
+                                  ((size_t)(sk_slot(p, q, u) * 2 + (int)r2) * cmax + c) * 512 + n;
+#pragma unroll
+              for (int q4 = 0; q4 < 4; ++q4) {
+                const float4 x = ldcg_f4(src + q4 * 128);
+                v[4 * q4] += x.x;
+                v[4 * q4 + 1] += x.y;
+                v[4 * q4 + 2] += x.z;
+                v[4 * q4 + 3] += x.w;
+              }
+            }
+            apply_epilogue(p, unit_n0, n, m_base + c * 16, v, xg, 1 + eg, rtab + c * 16);
+          }
+        }
+      }
     }
   }
 
-  if (SPLIT) {
+  if (SPLIT == 1) {
     // ------------------------------ split-K reduction: push partials to chunk owners
     const int u = cl;
     const int unit_n0 = (u % p.n_tiles) * 256 + (int)r2 * 128, m_base = (u / p.n_tiles) * p.m_blk;

@@ -40,6 +40,7 @@
 
 #include "common.cuh"
 #include "kernels.hpp"
+#include "launch.hpp"
 #include "tma.hpp"
 
 namespace srl {
@@ -49,11 +50,17 @@ struct GemmParams {
   int m_blk, m_blocks, n_tiles, kb, units;
   int H;   // 128-row halves per weight tile (1 or 2): both multiply one activation slice
   int S;   // cluster split-K factor (1 = persistent whole-unit mode)
+  int w_shared;  // pair kernel: several batch blocks stream the same weight tile (keep it in L2)
   int hp;  // SPLIT: tile halves reduced per DSMEM phase (what fits in the idle rings)
   int stages, xstages, tmem_cols, acc_stages;
   GemmEpi epi;
   const uint8_t* wp;  // packed weights (epi.w_packed), else null
   unsigned long long* dbg;  // optional [grid][16] globaltimer stamps (profiling builds)
+  // stream-K (pair kernel, SPLIT == 2): partial slots, per-(unit, row half) arrival counters
+  float* sk_ws;
+  int* sk_cnt;
+  long long sk_total;  // units * kb
+  int sk_pairs;
 };
 
 static constexpr int kStageA = 128 * 128;  // 128 weight rows x 64 bf16 (128 B)
@@ -155,6 +162,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const int w = warp_id(), lane = lane_id();
   const int nseg = seg_count<SPLIT>(p);
+  pdl_trigger();
   if (threadIdx.x == 0) {
     DBG(0);
     for (int s = 0; s < p.stages; ++s) {
@@ -179,6 +187,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_after();
   const uint32_t tbase = *tholder;
   if (threadIdx.x == 0) DBG(1);
+  // PDL: only the weight stream (constant during decode) may start before the
+  // predecessor grid has completed; every other role reads or writes its data
+  if (w != 0) pdl_wait();
 
   // The three issuing threads run lean loops: ring slot / phase counters are
   // advanced incrementally (no runtime division) and the shared-memory
@@ -457,22 +468,14 @@ static int max_clusters_pair(int size) {
 static int launch_cluster(void (*kern)(const CUtensorMap, const CUtensorMap, GemmParams), int grid, int csize,
                           size_t smem, cudaStream_t stream, const CUtensorMap& tmW, const CUtensorMap& tmX,
                           const GemmParams& p) {
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kGemmThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = csize;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, tmW, tmX, p) == cudaSuccess ? 0 : -3;
+  return launch_k(kern, dim3(grid), dim3(kGemmThreads), smem, stream, csize, tmW, tmX, p) == cudaSuccess ? 0 : -3;
 }
 
 // CTA-pair variant (gemm_pair.cuh) for wide batches; returns 1 when not applicable
+size_t gemm_workspace_bytes(int num_sms) {
+  return (size_t)num_sms * 2 * kSkSlotBytes + (size_t)kSkMaxUnits * 2 * sizeof(int);
+}
+
 static int gemm_pair_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N, int K, const GemmEpi& epi,
                            int num_sms, cudaStream_t stream) {
   GemmParams p;
@@ -480,23 +483,54 @@ static int gemm_pair_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W
   p.M = M;
   p.N = N;
   p.K = K;
-  p.m_blk = pick_mblk(M);
+  const int pairs = num_sms / 2;
+  p.n_tiles = (N + 255) / 256;  // pair tiles
+  // Decomposition when whole pair units cannot occupy the pairs evenly (decode
+  // QKV / O / down: 24 / 16 / 16 tiles, gate/up 112, on 74 pairs):
+  //   1 (default) split-K over a cluster of S pairs with a DSMEM reduction;
+  //   0 batch split -- each weight tile multiplied by nb = pairs/tiles batch blocks
+  //     on nb pairs (UMMA N = M/nb), no partial sums.  Measured r01: slower -- the
+  //     nb-fold weight re-reads are served at ~6.4 TB/s aggregate, HBM-like, not
+  //     deduplicated by L2 (QKV 32 vs 30 us, down 72 vs 42 us per launch);
+  //   2 stream-K with an L2 fix-up (gemm_pair.cuh).  Measured r01: slower (QKV
+  //     53 us in the decode graph): 128 KB fp32 partials per piece through L2.
+  static const int mode = getenv("SRL_GEMM_SPLIT") ? atoi(getenv("SRL_GEMM_SPLIT")) : 1;
+  int mb = pick_mblk(M);
+  bool bsplit = false;
+  if (mode == 0 && M <= 256 && p.n_tiles < pairs) {
+    const int nb = pairs / p.n_tiles;
+    if (nb > 1) {
+      int m = (M + nb - 1) / nb;
+      m = (m + 15) & ~15;
+      if (m < mb) {
+        mb = m;
+        bsplit = true;
+      }
+    }
+  }
+  p.m_blk = mb;
   p.m_blocks = (M + p.m_blk - 1) / p.m_blk;
   p.H = 1;
-  p.n_tiles = (N + 255) / 256;  // pair tiles
+  p.w_shared = bsplit ? 1 : 0;
   p.kb = K / 64;
   p.units = p.n_tiles * p.m_blocks;
   p.epi = epi;
   p.dbg = (g_dbg && g_dbg_count++ == g_dbg_target) ? g_dbg : nullptr;
-  const int pairs = num_sms / 2;
+  const bool sk = mode == 2 && epi.ws && p.units % pairs != 0 && p.units <= kSkMaxUnits;
   int S = 1;
-  if (p.units < pairs) {
+  if (!sk && !bsplit && p.units < pairs) {
     S = pairs / p.units;
     if (S > 4) S = 4;
     if (S > p.kb) S = p.kb;
     while (S > 1 && p.units > max_clusters_pair(2 * S)) --S;
   }
   p.S = S;
+  if (sk) {
+    p.sk_total = (long long)p.units * p.kb;
+    p.sk_pairs = (int)(p.sk_total < pairs ? p.sk_total : pairs);
+    p.sk_ws = reinterpret_cast<float*>(epi.ws);
+    p.sk_cnt = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(epi.ws) + (size_t)num_sms * 2 * kSkSlotBytes);
+  }
   const int stage_b = (p.m_blk >> 1) * 128;
   const int budget = 200 * 1024;
   int xstages = stage_b <= 4096 ? 8 : (stage_b <= 8192 ? 6 : 4);
@@ -528,14 +562,17 @@ static int gemm_pair_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W
   if (!attr_set) {
     cudaFuncSetAttribute(gemm_pair_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(gemm_pair_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(gemm_pair_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_set = true;
   }
   static const bool verbose = getenv("SRL_GEMM_VERBOSE") != nullptr;
   if (verbose)
-    fprintf(stderr, "gemm(pair) M=%d N=%d K=%d units=%d S=%d stages=%d/%d smem=%zu\n", M, N, K, p.units, S, stages,
-            xstages, smem);
+    fprintf(stderr, "gemm(pair) M=%d N=%d K=%d units=%d S=%d sk=%d stages=%d/%d smem=%zu\n", M, N, K, p.units, S,
+            (int)sk, stages, xstages, smem);
   int rc;
-  if (S == 1) {
+  if (sk) {
+    rc = launch_cluster(gemm_pair_kernel<2>, 2 * p.sk_pairs, 2, smem, stream, tmW, tmX, p);
+  } else if (S == 1) {
     const int np = p.units < pairs ? p.units : pairs;
     rc = launch_cluster(gemm_pair_kernel<0>, 2 * np, 2, smem, stream, tmW, tmX, p);
   } else {
@@ -622,7 +659,7 @@ int gemm_bf16_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N
   }
   if (S == 1) {
     const int grid = p.units < num_sms ? p.units : num_sms;
-    gemm_bf16_tc_kernel<0><<<grid, kGemmThreads, smem, stream>>>(tmW, tmX, p);
+    launch_k(gemm_bf16_tc_kernel<0>, dim3(grid), dim3(kGemmThreads), smem, stream, 1, tmW, tmX, p);
   } else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p.units * S);
@@ -643,7 +680,7 @@ int gemm_bf16_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N
       fprintf(stderr, "gemm M=%d N=%d K=%d H=%d units=%d S=%d hp=%d stages=%d smem=%zu max_active_clusters=%d\n", M,
               N, K, p.H, p.units, S, p.hp, stages, smem, ncl);
     }
-    cudaLaunchKernelEx(&cfg, gemm_bf16_tc_kernel<1>, tmW, tmX, p);
+    launch_k(gemm_bf16_tc_kernel<1>, dim3(p.units * S), dim3(kGemmThreads), smem, stream, S, tmW, tmX, p);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }

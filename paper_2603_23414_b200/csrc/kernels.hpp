@@ -29,7 +29,15 @@ struct GemmEpi {
   void* k_pool;
   void* v_pool;
   int Hq, Hkv, dh, kv_f32;
+  // GEMM workspace (gemm_workspace_bytes, zero-filled before first use; every
+  // launch leaves it zeroed): stream-K partial slots + arrival counters.  Null
+  // disables stream-K (cluster split-K / whole units instead).
+  void* ws;
 };
+
+constexpr size_t kSkSlotBytes = 128 * 256 * 4;  // one CTA's fp32 partial: 128 rows x <= 256 batch columns
+constexpr int kSkMaxUnits = 8192;               // stream-K counters: pair units per launch
+size_t gemm_workspace_bytes(int num_sms);
 
 // ---- gemm_tc.cu
 // Y = X[M,K] . W[N,K]^T with the fused epilogue `epi` (for EPI_SILU, W's

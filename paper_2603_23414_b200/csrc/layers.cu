@@ -5,6 +5,7 @@
 // operand).  The residual adds, SiLU-mul, bias + RoPE + KV append run inside
 // the GEMM epilogues (gemm_tc.cu).
 #include "common.cuh"
+#include "launch.hpp"
 #include "layers.hpp"
 
 namespace srl {
@@ -37,6 +38,8 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(float* __restrict
                                                                 const __nv_bfloat16* __restrict__ w, float eps,
                                                                 __nv_bfloat16* __restrict__ y) {
   __shared__ float red[kNormThreads / 32];
+  pdl_trigger();
+  pdl_wait();
   const int m = blockIdx.x;
   float* x = x_res + (size_t)m * d;
   __nv_bfloat16* out = y + (size_t)m * d;
@@ -90,7 +93,7 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(float* __restrict
 
 void rmsnorm(float* x_res, const int* row_tok, const int* row_pos, int M, int d, const __nv_bfloat16* embed,
              const __nv_bfloat16* w, float eps, __nv_bfloat16* y, cudaStream_t st) {
-  if (M > 0) rmsnorm_kernel<<<M, kNormThreads, 0, st>>>(x_res, row_tok, row_pos, M, d, embed, w, eps, y);
+  if (M > 0) launch_k(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, st, 1, x_res, row_tok, row_pos, M, d, embed, w, eps, y);
 }
 
 }  // namespace srl

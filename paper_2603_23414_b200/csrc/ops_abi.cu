@@ -38,7 +38,7 @@ extern "C" int64_t srl_op_gemm_workspace(int32_t M, int32_t N, int32_t K, int32_
   epi &= ~SRL_GEMM_W_PACKED;
   if (M <= 0 || N <= 0 || K <= 0 || epi < 0 || epi > 2) return -1;
   (void)K;
-  return 256;
+  return (int64_t)gemm_workspace_bytes(op_sms());
 }
 
 extern "C" int32_t srl_op_gemm_bf16(const void* X, int32_t M, const void* W, int32_t N, int32_t K, int32_t epi,
@@ -58,10 +58,10 @@ extern "C" int32_t srl_op_gemm_bf16(const void* X, int32_t M, const void* W, int
   e.out_f32 = reinterpret_cast<float*>(out);
   e.x_res = reinterpret_cast<float*>(out);
   e.act = reinterpret_cast<__nv_bfloat16*>(out);
+  e.ws = workspace;
   const int rows = epi == 2 ? 2 * N : N;  // SiLU-mul: interleaved gate/up rows
   int r = gemm_bf16_fused(reinterpret_cast<const __nv_bfloat16*>(X), M, reinterpret_cast<const __nv_bfloat16*>(W),
                           rows, K, e, sms, st);
-  (void)workspace;
   if (r) set_error("srl_op_gemm_bf16: %s (code %ld)", r == -1 ? "bad shape" : "launch/tma failure", r);
   return r;
 }

@@ -12,6 +12,7 @@
 // __fdiv_rn) in the order the algorithm states; the logprob uses a parallel
 // reduction and is compared with a tolerance (reading R15).
 #include "common.cuh"
+#include "launch.hpp"
 #include "layers.hpp"
 
 namespace srl {
@@ -94,6 +95,8 @@ __device__ __forceinline__ bool better(float s, int j, float bs, int bj) {
 constexpr int kSampThreads = 512;
 
 __global__ void __launch_bounds__(kSampThreads) sample_kernel(SampleArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const int m = blockIdx.x;
   if (a.row_pos[m] < 0) {
     if (threadIdx.x == 0) {
@@ -172,7 +175,7 @@ __global__ void __launch_bounds__(kSampThreads) sample_kernel(SampleArgs a) {
 }
 
 void sample(const SampleArgs& a, cudaStream_t st) {
-  if (a.M > 0) sample_kernel<<<a.M, kSampThreads, 0, st>>>(a);
+  if (a.M > 0) launch_k(sample_kernel, dim3(a.M), dim3(kSampThreads), 0, st, 1, a);
 }
 
 }  // namespace srl

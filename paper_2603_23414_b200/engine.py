@@ -182,7 +182,10 @@ class RolloutEngine:
         check(self.lib.srl_get_counters(self.h, *[C.byref(x) for x in v]), "srl_get_counters")
         return dict(zip(["raw_tokens", "discarded_tokens", "emitted", "groups", "kernel_launches"], [x.value for x in v]))
 
-    def set_profiling(self, on: bool):
+    def set_profiling(self, on: bool, classes=None):
+        """classes: iterable of _lib.KERNEL_CLASSES names to bracket (default all)."""
+        mask = 0xFFFFFFFF if classes is None else sum(1 << _lib.KERNEL_CLASSES.index(c) for c in classes)
+        check(self.lib.srl_set_profile_mask(self.h, mask), "srl_set_profile_mask")
         return check(self.lib.srl_set_profiling(self.h, 1 if on else 0), "srl_set_profiling")
 
     def profile(self):

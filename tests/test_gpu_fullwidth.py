@@ -1,0 +1,141 @@
+"""Full-width parity: LLaMA-3.1-8B- and Qwen-2.5-32B-shaped policies (2-layer
+slices at full width, SURVEY §8(c) "shape-faithful shallow slices"), at the
+per-GPU batch the benchmark runs (Q_g = 256 for 8B / cfg2, Q_g = 64 for 32B /
+cfg4), through the C ABI with the same GEMM / attention / sampler launch
+configurations bench.py times (the GEMM picks its split from M, N, K only).
+
+Per sampled row and generated index n (teacher forcing on the GPU's own
+tokens, oracle.model.Model.full_forward in fp64 -- pinned against incremental
+decode in test_oracle_model.py):
+* logits: per-(row, n) relative L2 -- mean over the checked rows <= 1e-2 (the
+  BASELINE.json north-star bar), every one <= 1.5e-2.  DESIGN.md reading R29:
+  at full width the bf16 rounding points of the path (GEMM activation operands,
+  q, KV cache, P, attention output, SiLU product, LM-head input) alone give
+  0.0083 mean / 0.0097 max rel-L2 at 2 layers (numpy fp64 model with exactly
+  those roundings, tools/precision_budget.py), so the per-element bar is the
+  mean, the max carries the derived headroom;
+* the sampler's id on the GPU logits equals oracle.sampler.sample_row's
+  (bit-exact Gumbel-max on identical logits) and the harvested token;
+* the oracle's own sample on its own logits equals the GPU's token unless the
+  top-2 perturbed-score gap is below 4x the observed logits error (at V >= 128k
+  that band holds ~20% of positions; >= 60% must be decided);
+* logprobs within 4x the max-abs logits error + 1e-4.
+
+Weights: the workload generator's torch implementation (bit-identical to its
+numpy one, pinned in test_oracle_model.py) evaluated on the GPU and copied to
+host -- generating 1e9 elements with numpy would take minutes; the embedding
+table is never materialised (rows on demand).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle.model import Model  # noqa: E402
+from oracle.sampler import sample_row  # noqa: E402
+from workload.configs import K_INF, KV_BF16, LLAMA8B, QWEN32B, SchedConfig  # noqa: E402
+from workload.prompts import make_prompts  # noqa: E402
+from workload.weights import bf16_bits_to_f32, gen_weight_np, gen_weight_torch, weight_names  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+
+
+class _EmbedRows:
+    """W["embed"] stand-in: row `tok` generated on demand (fp64)."""
+
+    def __init__(self, m):
+        self.m = m
+
+    def __getitem__(self, tok):
+        return bf16_bits_to_f32(gen_weight_np(self.m, "embed", rows=[int(tok)]))[0].astype(np.float64)
+
+
+def _oracle_weights(m):
+    W = {"embed": _EmbedRows(m)}
+    for name in weight_names(m):
+        if name == "embed":
+            continue
+        t = gen_weight_torch(m, name, device="cuda")
+        W[name] = t.float().cpu().numpy().astype(np.float64)
+        del t
+    return W
+
+
+STEPS = 6
+
+
+@pytest.mark.parametrize("shape,Q_g", [(LLAMA8B, 256), (QWEN32B, 64)], ids=["llama8b-L2-Q256", "qwen32b-L2-Q64"])
+def test_fullwidth_teacher_forced(shape, Q_g):
+    from paper_2603_23414_b200.engine import RolloutEngine
+    from workload.weights import fill_engine_weights
+    m = shape.with_layers(2)
+    cap = STEPS + 2
+    cfg = SchedConfig(Q_g=Q_g, U=Q_g // 4, K=K_INF, pool_prompts=Q_g, cap=cap, kv_pages=4 * Q_g, kv_dtype=KV_BF16)
+    off, toks = make_prompts(1, Q_g, m.V, 4, 12)
+    L = np.full(Q_g, cap, dtype=np.int32)              # nobody finishes inside the checked window
+    eng = RolloutEngine(m, cfg, max_traj=Q_g, max_prompt=16, prefill_chunk=4096)
+    fill_engine_weights(eng, m, 0)
+    eng.load_policy_weights(0)
+    eng.submit_prompts(np.arange(Q_g, dtype=np.uint64) + 1, off, toks, L)
+    rows = sorted({0, 1, Q_g // 3, Q_g // 2 + 1, Q_g - 2, Q_g - 1})
+    zs = []                                            # [step][row] fp32 logits
+    for k in range(STEPS):
+        st, info = eng.decode_step()
+        assert info.k == k and info.r_k == Q_g          # pool = Q_g: slot s holds trajectory s
+        z = eng.debug_logits()
+        zs.append(z[rows].copy())
+        del z
+    # run to the end; every trajectory's tokens + behaviour logprobs come back in the groups
+    gpu_tok, gpu_lp, v = {}, {}, 0
+    while True:
+        st, _ = eng.decode_step()
+        if st == 2:
+            break
+        if st == 1:
+            h = eng.harvest_finished(cap_recs=Q_g)
+            for r in h.records:
+                seg = slice(r["tok_offset"], r["tok_offset"] + r["len"])
+                gpu_tok[r["traj_id"]], gpu_lp[r["traj_id"]] = h.tokens[seg].tolist(), h.logprobs[seg].tolist()
+            v += 1
+            eng.load_policy_weights(v)
+    eng.close()
+    torch.cuda.empty_cache()
+    assert sorted(gpu_tok) == list(range(Q_g)) and all(len(t) == cap for t in gpu_tok.values())
+    W = _oracle_weights(m)
+    mdl = Model(m, W)
+    invT = np.float32(1.0)
+    rels = []
+    excluded = checked = 0
+    for j, s in enumerate(rows):
+        prompt = [int(t) for t in toks[off[s]:off[s + 1]]]
+        gen = gpu_tok[s]
+        for n in range(STEPS):    # bit-exact sampler: the oracle's Gumbel-max on the GPU's logits
+            assert sample_row(zs[n][j], invT, cfg.sample_seed, n, s, 0)[0] == gen[n], (s, n)
+        seq = prompt + gen[:STEPS - 1]
+        zo_all = mdl.full_forward(seq)                     # logits at every position
+        for n in range(STEPS):
+            zo = zo_all[len(prompt) - 1 + n]
+            zg = zs[n][j].astype(np.float64)
+            rel = np.linalg.norm(zg - zo) / np.linalg.norm(zo)
+            rels.append(rel)
+            err = float(np.abs(zg - zo).max())
+            tok_o, lp_o, sc = sample_row(zo.astype(np.float32), invT, cfg.sample_seed, n, s, 0)
+            ss = np.sort(sc.astype(np.float64))
+            if ss[-1] - ss[-2] < 4 * err:
+                excluded += 1
+            else:
+                checked += 1
+                assert tok_o == gen[n], (s, n)
+            assert abs(gpu_lp[s][n] - lp_o) <= 4 * err + 1e-4, (s, n)
+    rels = np.array(rels)
+    print(f"{m.name}: logits rel-L2 mean {rels.mean():.2e} max {rels.max():.2e}; ids checked {checked}, "
+          f"near-tie excluded {excluded}")
+    assert rels.mean() <= 1e-2 and rels.max() <= 1.5e-2, rels
+    # near ties: with V >= 128k the top-2 Gumbel-perturbed score gap is ~Exp(1), so a
+    # 4x max-abs-error band of ~0.2 excludes ~20% of positions; most must still decide
+    assert checked >= 0.6 * (checked + excluded)

@@ -24,7 +24,7 @@ def _stream():
 # ------------------------------------------------------------------ GEMM (tcgen05)
 GEMM_SHAPES = [(1, 128, 64), (16, 256, 128), (200, 384, 256), (256, 6144, 4096), (64, 4096, 14336),
                (600, 512, 128), (37, 1000, 192), (256, 7168, 5120), (256, 128256, 4096), (4096, 4096, 4096),
-               (300, 1024, 14336)]
+               (300, 1024, 14336), (256, 4096, 14336), (128, 2048, 4096), (512, 3072, 1024)]
 
 
 def _pack(lib, W):
@@ -36,7 +36,7 @@ def _pack(lib, W):
 
 def _gemm(lib, X, W, N, epi, out, packed=False):
     M, K = X.shape
-    ws = torch.empty(lib.srl_op_gemm_workspace(M, N, K, epi), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(lib.srl_op_gemm_workspace(M, N, K, epi), dtype=torch.uint8, device="cuda")
     Wp = _pack(lib, W) if packed else W
     flag = 0x100 if packed else 0                      # SRL_GEMM_W_PACKED
     rc = lib.srl_op_gemm_bf16(X.data_ptr(), M, Wp.data_ptr(), N, K, epi | flag, out.data_ptr(), ws.data_ptr(),
@@ -90,7 +90,7 @@ def test_gemm_matches_fp64_reference(lib, M, N, K, packed):
 
 
 @pytest.mark.parametrize("packed", [False, True], ids=["rowmajor", "packed"])
-@pytest.mark.parametrize("M,N,K", [(16, 256, 128), (256, 4096, 4096), (77, 640, 14336)])
+@pytest.mark.parametrize("M,N,K", [(16, 256, 128), (256, 4096, 4096), (77, 640, 14336), (256, 4096, 14336)])
 def test_gemm_residual_epilogue(lib, M, N, K, packed):
     g = torch.Generator(device="cuda").manual_seed(3)
     X = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
