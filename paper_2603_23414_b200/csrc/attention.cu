@@ -88,7 +88,45 @@ __global__ void attn_plan_kernel(AttnArgs a, int split) {
     if (threadIdx.x == 0) base_s += wsum[31];
     __syncthreads();
   }
-  if (threadIdx.x == 0) *a.n_items = min(base_s, a.max_items);
+  const int n = min(base_s, a.max_items);
+  if (threadIdx.x == 0) *a.n_items = n;
+  for (int i = threadIdx.x; i < a.n_ctr; i += blockDim.x) a.work_ctr[i] = 0;
+  // processing order: counting sort by descending page count (longest first:
+  // the persistent CTAs then pull items LPT-style from a counter)
+  __shared__ int hist[1024];
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  auto bucket = [&](int it) {
+    const int m = a.items[it * 3], c = a.items[it * 3 + 2];
+    const int npages = (a.row_pos[m] + 1 + 63) / 64;
+    const int pg = a.row_nchunk[m] == 1 ? npages : min(npages - c * kChunkPages, kChunkPages);
+    return 1023 - min(pg, 1023);
+  };
+  for (int it = threadIdx.x; it < n; it += blockDim.x) atomicAdd(&hist[bucket(it)], 1);
+  __syncthreads();
+  {  // exclusive scan of the 1024 buckets, one per thread
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int v = threadIdx.x < 1024 ? hist[threadIdx.x] : 0;
+    int x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int s = wsum[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= o) s += y;
+      }
+      wsum[lane] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < 1024) hist[threadIdx.x] = (w ? wsum[w - 1] : 0) + x - v;
+    __syncthreads();
+  }
+  for (int it = threadIdx.x; it < n; it += blockDim.x) a.order[atomicAdd(&hist[bucket(it)], 1)] = it;
 }
 
 int attn_max_items(int M, int Hkv, int max_ctx) {
@@ -293,6 +331,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   pdl_wait();
   uint64_t* full = reinterpret_cast<uint64_t*>(mrg + kConsumerWarps * 8 * (DH + 2));
   uint64_t* empty = full + kStages;
+  volatile int* hdr = reinterpret_cast<volatile int*>(empty + kStages);  // [kStages] item of each staged page
 
   const int G = a.Hq / a.Hkv;
   const int w = warp_id(), lane = lane_id();
@@ -313,7 +352,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       tma_prefetch(&tmV);
       const uint64_t pol = policy_evict_first();
       int q = 0;
-      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      for (;;) {
+        // longest remaining item first, pulled dynamically (balances the tail)
+        const int j = atomicAdd(a.work_ctr, 1);
+        if (j >= n_items) break;
+        const int it = a.order[j];
         const ItemInfo ii = item_info(a, it);
         for (int p = ii.p0; p < ii.p1; ++p, ++q) {
           const int s = q % kStages;
@@ -323,6 +366,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           const int row = (page * a.Hkv + ii.kvh) * 64;
           uint8_t* kb = stages + s * C::kStageBytes;
           uint8_t* vb = kb + C::kBlockBytes;
+          hdr[s] = it;  // published by the arrive below (release), read after the consumers' wait
           mbar_arrive_expect_tx(&full[s], C::kStageBytes);
 #pragma unroll
           for (int b = 0; b < C::kBoxes; ++b) {
@@ -331,6 +375,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           }
         }
       }
+      // end of work: a stage with no data and item -1
+      const int s = q % kStages;
+      mbar_wait(&empty[s], ((q / kStages) & 1) ^ 1);
+      hdr[s] = -1;
+      mbar_arrive(&full[s]);
     }
     return;
   }
@@ -338,7 +387,13 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   // ---------------- consumer warps
   const float scale2 = a.scale * kLog2e;
   int q = 0;
-  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+  for (;;) {
+    {  // the next item is announced in the header of its first staged page
+      const int s = q % kStages;
+      mbar_wait(&full[s], (q / kStages) & 1);
+    }
+    const int it = hdr[q % kStages];
+    if (it < 0) break;
     const ItemInfo ii = item_info(a, it);
     // Q^T fragments (B operand): n = query index lane/4 (< G), k = dims
     uint32_t bq[MT][2];

@@ -361,6 +361,9 @@ void plan_scratch(srl_engine* e, ScratchPlan& p, bool assign) {
   e->rope_sin = (float*)P(4ull * z.max_ctx * (m.dh / 2));
   AttnArgs& a = e->attn;
   a.items = (int*)P(12ull * z.max_items);
+  a.order = (int*)P(4ull * z.max_items);
+  a.work_ctr = (int*)P(4ull * m.L);
+  a.n_ctr = m.L;
   a.n_items = (int*)P(64);
   a.row_item0 = (int*)P(4ull * z.mmax);
   a.row_nchunk = (int*)P(4ull * z.mmax);
@@ -446,6 +449,7 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
     run_gemm(e, D + SRL_K_GEMM_QKV, e->xn, M, (const __nv_bfloat16*)w.pqkv, Nqkv, d, qe);
     a.k_pool = e->kpool[l];
     a.v_pool = e->vpool[l];
+    a.work_ctr = e->attn.work_ctr + l;  // one counter per layer, all zeroed by attn_plan
     {
       Prof p(e, D + SRL_K_ATTN, 2);
       attn_run(a, e->kv_f32, &e->tmK[l], &e->tmV[l], st);

@@ -34,6 +34,11 @@ struct AttnArgs {
   float* out_f32;        // optional fp32 copy of out (op-level tests)
   int max_items;
   float scale;
+  // bf16 kernel scheduling: items are taken longest-first (order, built by the
+  // plan kernel) from a dynamic counter -- LPT over the persistent CTAs
+  int* order;            // [max_items] item ids by descending page count
+  int* work_ctr;         // this launch's counter; the plan kernel zeroes work_ctr[0..n_ctr)
+  int n_ctr;
 };
 void attn_plan(const AttnArgs& a, int split, cudaStream_t st);
 void attn_run(const AttnArgs& a, bool kv_fp32, const void* tmap_k, const void* tmap_v, cudaStream_t st);
