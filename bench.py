@@ -44,7 +44,7 @@ from workload.prompts import make_prompts  # noqa: E402
 
 METRIC = "rollout tokens/s + bubble ratio @1/2/4/8 B200; decode %HBM roofline"
 WORKLOAD = ("cfg2: LLaMA-3.1-8B-shaped random-init bf16 policy, rollout batch Q_g=256 per GPU, "
-            "max 8192 new tokens, update group U=64, K=inf (partial), pool 1024 prompts per GPU x 2 epochs, "
+            "max 8192 new tokens, update group U=64, K=inf (partial), pool 1024 prompts per GPU per epoch, "
             "256-token prompts, FORCED lognormal(1600,0.55)+3%-at-cap lengths, TRAINED barrier, KEEP_KV; "
             "N>1: lockstep replicas (global slots g=s*N+r, per-step all-gather of sampled rows, "
             "weight broadcast after every update group)")
@@ -390,10 +390,21 @@ def main():
     per_unit = 2 * m.Hkv * m.dh * 2                             # K+V bytes per context token per layer
     units = sum_ctx                                              # context tokens read per layer, all timed steps
     achieved = per_unit * units * m.L / (attn_ms * 1e-3) / 1e9 if attn_ms > 0 else None
+    alg_per_launch = per_unit * units / max(1, n_dec)          # bytes one attention launch must read
+    traffic, traffic_src = None, None
+    tp = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+    if os.path.exists(tp):                                       # committed ncu --set full capture
+        with open(tp) as fh:
+            traffic_src = json.load(fh)
+        traffic = traffic_src["traffic_over_algorithmic"] * alg_per_launch
     roof = {"bound": "hbm", "kernel": "attn_bf16_kernel (paged GQA decode attention)", "achieved": achieved,
-            "peak": hbm, "unit": "GB/s", "frac": achieved / hbm if achieved else None, "traffic": None,
+            "peak": hbm, "unit": "GB/s", "frac": achieved / hbm if achieved else None, "traffic": traffic,
+            "traffic_note": "DRAM bytes per launch = this run's algorithmic bytes per launch x the measured "
+                            "dram/algorithmic ratio of the committed ncu capture (traffic_capture)",
+            "traffic_capture": traffic_src,
             "per_unit_bytes": per_unit, "unit_def": "one context token of one layer (K+V, bf16)",
-            "units_per_launch": units / max(1, n_dec), "launches": attn_n, "peak_source": peak_src}
+            "units_per_launch": units / max(1, n_dec), "launches": attn_n,
+            "peak_source": peak_src + " (MEASURED_PEAKS.json copy bandwidth; a read-only stream may exceed it)"}
     # decode roofline fraction of the whole step
     t_roof = 0.0
     for (rk, sc, dt, npre, nfin, rl) in stats:
