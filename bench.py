@@ -37,7 +37,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from workload.configs import (BARRIER_TRAINED, K_INF, KV_BF16, LLAMA8B, MODE_SORTED, RESUME_KEEP_KV,  # noqa: E402
+from workload.configs import (BARRIER_TRAINED, K_INF, KV_BF16, LLAMA8B, MODE_SORTED, QWEN32B, RESUME_KEEP_KV,  # noqa: E402
                               STOP_FORCED, SchedConfig)
 from workload.lengths import LengthModel, sample_lengths  # noqa: E402
 from workload.prompts import make_prompts  # noqa: E402
@@ -50,22 +50,30 @@ WORKLOAD = ("cfg2: LLaMA-3.1-8B-shaped random-init bf16 policy, rollout batch Q_
             "weight broadcast after every update group)")
 N_PROMPTS_PER_EPOCH = 1024
 PROMPT_LEN = 256
+WORKLOAD_32B = ("cfg4 per GPU: Qwen-2.5-32B-shaped random-init bf16 policy (qkv bias, compact packed-only weights "
+                "65.5 GB), rollout batch Q_g=64 per GPU, max 16384 new tokens, update group U=64, K=inf (partial), "
+                "pool 256 prompts per GPU per epoch, 256-token prompts, FORCED lognormal(1600,0.55)+3%-at-cap lengths, "
+                "TRAINED barrier, KEEP_KV; policy refresh = version bump (no trainer copy fits beside the engine)")
+# model -> (shape, Q_g, cap, kv_pages, prompts per GPU per epoch, compact weights, trainer copy, workload text)
+MODELS = {"llama8b": (LLAMA8B, 256, 8192, 11000, 1024, False, True, None),
+          "qwen32b": (QWEN32B, 64, 16384, 5000, 256, True, False, WORKLOAD_32B)}
 EPOCHS = 4          # prompt stream long enough for precondition + warmup + timed + e2e rounds
+U_MAX = 2048        # harvest buffer capacity (records)
 
 
-def cfg2_sched(world=1):
-    return SchedConfig(Q_g=256, R=world, U=64, K=K_INF, pool_prompts=N_PROMPTS_PER_EPOCH * world, G=1, cap=8192,
+def cfg2_sched(world=1, Q_g=256, cap=8192, pool=N_PROMPTS_PER_EPOCH, kv_pages=11000):
+    return SchedConfig(Q_g=Q_g, R=world, U=64, K=K_INF, pool_prompts=pool * world, G=1, cap=cap,
                        page_tokens=64,
-                       kv_pages=11000, mode=MODE_SORTED, resume=RESUME_KEEP_KV, barrier=BARRIER_TRAINED,
+                       kv_pages=kv_pages, mode=MODE_SORTED, resume=RESUME_KEEP_KV, barrier=BARRIER_TRAINED,
                        stop=STOP_FORCED, kv_dtype=KV_BF16, temperature=1.0, sample_seed=3)
 
 
-def workload_inputs(world=1, epochs=2):
+def workload_inputs(world=1, epochs=2, pool=N_PROMPTS_PER_EPOCH, V=LLAMA8B.V, cap=8192):
     """The prompt stream every replica submits (identical on all ranks; the replicated
     pending queue shards it over the global slots)."""
-    n = N_PROMPTS_PER_EPOCH * world * epochs
-    off, toks = make_prompts(1, n, LLAMA8B.V, PROMPT_LEN)
-    L = sample_lengths(LengthModel(median=1600, sigma=0.55, tail=0.03, floor=1, cap=8192), 0, n)
+    n = pool * world * epochs
+    off, toks = make_prompts(1, n, V, PROMPT_LEN)
+    L = sample_lengths(LengthModel(median=1600, sigma=0.55, tail=0.03, floor=1, cap=cap), 0, n)
     return off, toks, L
 
 
@@ -154,20 +162,21 @@ def run_gpu(args, rank, world, dist):
     torch.cuda.set_device(rank % max(1, torch.cuda.device_count()))
     dev = torch.cuda.current_device()
     from paper_2603_23414_b200.engine import share_nccl_unique_id
-    model, sched = LLAMA8B, cfg2_sched(world)
-    off, toks, L = workload_inputs(world, epochs=EPOCHS)
+    model, Q_g, cap, kv_pages, pool, compact, keep_trainer, _ = MODELS[args.model]
+    sched = cfg2_sched(world, Q_g=Q_g, cap=cap, pool=pool, kv_pages=kv_pages)
+    off, toks, L = workload_inputs(world, epochs=EPOCHS, pool=pool, V=model.V, cap=cap)
     ids = np.arange(len(off) - 1, dtype=np.uint64) + 1
     n_prompts = len(ids)
-    max_traj = EPOCHS * N_PROMPTS_PER_EPOCH * world
+    max_traj = EPOCHS * pool * world
     rep = {}
     if world > 1:
         rep = dict(rank=rank, world=world, nccl_id=share_nccl_unique_id(dist, rank))
     eng = RolloutEngine(model, sched, max_traj=max_traj, max_prompt=PROMPT_LEN, prefill_chunk=4096, device=dev,
-                        **rep)
+                        compact_weights=compact, **rep)
     fill_engine_weights(eng, model, 0)
     # the trainer's copy of the refreshed policy on rank 0 (K13: the same bytes are
     # re-emitted); the other replicas receive it through the engine's broadcast
-    trainer = eng.W.clone() if rank == 0 else None
+    trainer = eng.W.clone() if rank == 0 and keep_trainer else None
     eng.load_policy_weights(0)
     torch.cuda.synchronize()
     stream = eng.stream              # the stream every engine kernel is launched on
@@ -183,7 +192,7 @@ def run_gpu(args, rank, world, dist):
             trace.append((info.r_k, info.sum_ctx, info.dt_ms, info.n_prefill_tokens, info.n_finished,
                           info.r_local))
         if s_ == GROUP_READY:        # rows a15-a17: sorted group out, refreshed policy in
-            h = eng.harvest_finished(cap_recs=2048, cap_toks=2048 * sched.cap)
+            h = eng.harvest_finished(cap_recs=U_MAX, cap_toks=U_MAX * sched.cap)
             st["useful"] += sum(r["len"] for r in h.records)
             st["d2h"] += sum(r["len"] for r in h.records) * 12 + len(h.records) * 64
             st["v"] += 1
@@ -205,7 +214,7 @@ def run_gpu(args, rank, world, dist):
         st["sub"] = hi
 
     # the first two epochs are resident; the e2e leg streams the rest from host memory
-    submit(0, min(n_prompts, 2 * N_PROMPTS_PER_EPOCH * world))
+    submit(0, min(n_prompts, 2 * pool * world))
     for _ in range(args.precondition):
         if step() is None:
             break
@@ -360,6 +369,8 @@ def main():
     ap.add_argument("--precondition", type=int, default=1500,
                     help="untimed decode steps first, so contexts are mid-rollout")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="llama8b", choices=sorted(MODELS),
+                    help="llama8b = BASELINE configs[1] (default); qwen32b = the per-GPU slice of configs[3]")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -376,14 +387,13 @@ def main():
         td.init_process_group("nccl")
         dist = td
     r = run_gpu(args, rank, world, dist)
-    m = LLAMA8B
+    m = MODELS[args.model][0]
     hbm, tf_burst, tf_sust, peak_src = load_peaks()
     # per-rank aggregates over the timed rounds
     stats = r["stats"]
     sum_ctx = sum(x[1] for x in stats)
     steps = r["ran"]
     n_dec = len(stats)
-    m = LLAMA8B
     attn_ms, attn_n = r["prof"]["attention"]
     # dominant kernel: paged attention (bracketed alone in the timed rounds; the
     # breakdown round confirms it is the largest class)
@@ -412,7 +422,7 @@ def main():
         t_roof += max(B / (hbm * 1e9), F / (tf_sust * 1e12))
     dec_frac = t_roof / (r["ms"] * 1e-3)
     tok_s = r["raw"] / (r["ms"] * 1e-3)
-    Q = 256 * world                                              # Q_tot (reading R1)
+    Q = MODELS[args.model][1] * world                           # Q_tot (reading R1)
 
     def bubble(tr):
         if not tr:
@@ -435,7 +445,7 @@ def main():
         "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": world, "steps": steps,
         "warmup": args.warmup, "ms_per_step": ms / max(1, steps), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": WORKLOAD,
+        "config": {"workload": MODELS[args.model][7] or WORKLOAD,
                    "step": "one early-update round: decode steps (refill, prefill, decode GEMMs, paged attention, "
                            "Philox sampling, stop detection, compaction) until the length-sorted update group of "
                            "U=64 is ready, its harvest, and the policy refresh (load_policy_weights, K bound)",
@@ -461,7 +471,7 @@ def main():
         "e2e": r["e2e"],
         "mean_ctx": sum_ctx / max(1, sum(x[5] for x in stats)),
     }
-    if not args.no_cpu and world == 1:
+    if not args.no_cpu and world == 1 and args.model == "llama8b":
         line["cpu_baseline"] = oracle_sample()
     elif not args.no_cpu:
         line["cpu_baseline"] = None

@@ -62,6 +62,12 @@ typedef struct srl_model_cfg {
   int32_t L, d, Hq, Hkv, dh, ff, V;
   float rope_theta, rms_eps;
   int32_t qkv_bias; /* Qwen-2.5 has q/k/v biases */
+  /* 1: the weight region holds the projection matrices ONLY in the GEMM's packed
+   * layout (no row-major staging copy: about half the bytes, what lets a
+   * 65 GB Qwen-2.5-32B policy and its KV cache share one GPU).  Those tensors
+   * are then installed with srl_load_policy_tensor and srl_weight_layout /
+   * srl_weight_offset do not address them.  Needs Hq*dh, Hkv*dh % 128 == 0. */
+  int32_t weights_compact;
 } srl_model_cfg;
 
 /* Scheduler.  Q_g slots per GPU, Q_tot = R * Q_g ("Q").
@@ -228,6 +234,19 @@ int32_t srl_harvest_finished(srl_engine* e, int32_t cap_recs, srl_traj* recs, in
  * re-queued (tokens dropped); under REPREFILL running ones are scavenged.
  * SRL_E_STATE if a group is ready but not harvested or version <= current. */
 int32_t srl_load_policy_weights(srl_engine* e, const void* flat_w, int64_t version);
+
+/* Install ONE tensor of the next policy from a caller device buffer holding it
+ * row-major [rows, cols] bf16 (the srl_weight_layout shape; wg / wu plain, not
+ * interleaved): projection matrices are packed straight into the GEMM's weight
+ * stream (for wq / wk / wv into their tile range of the fused QKV matrix, for
+ * wg / wu into their 64-row interleave), the others are copied.  The source is
+ * read on the engine stream; the caller keeps it alive until the next
+ * synchronising call.  Then srl_load_policy_weights(e, NULL, version) makes the
+ * installed tensors the new policy (and broadcasts them from rank 0).  Works
+ * with and without weights_compact (without it the staging copy is updated
+ * too).  Errors: SRL_E_INVALID_ARG (unknown name), SRL_E_STATE (a group awaits
+ * harvest), SRL_E_CUDA. */
+int32_t srl_load_policy_tensor(srl_engine* e, const char* name, const void* src);
 
 /* Trace / event log since record index `from` (see srl_trace_rec).  *n_out
  * receives the number copied; *n_total the total recorded. */

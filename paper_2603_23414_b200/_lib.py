@@ -19,7 +19,7 @@ _F32P = C.POINTER(C.c_float)
 
 class ModelCfg(C.Structure):
     _fields_ = [("L", _I32), ("d", _I32), ("Hq", _I32), ("Hkv", _I32), ("dh", _I32), ("ff", _I32), ("V", _I32),
-                ("rope_theta", C.c_float), ("rms_eps", C.c_float), ("qkv_bias", _I32)]
+                ("rope_theta", C.c_float), ("rms_eps", C.c_float), ("qkv_bias", _I32), ("weights_compact", _I32)]
 
 
 class SchedCfg(C.Structure):
@@ -92,6 +92,7 @@ SIGNATURES = {
     "srl_set_profile_mask": (_I32, [_P, C.c_uint32]),
     "srl_get_profile": (_I32, [_P, C.POINTER(C.c_double), _I64P]),
     "srl_nccl_unique_id": (_I32, [_P]),
+    "srl_load_policy_tensor": (_I32, [_P, C.c_char_p, _P]),
     "srl_local_group_create": (_I32, [_I32, C.POINTER(_P)]),
     "srl_local_group_destroy": (_I32, [_P]),
 }

@@ -33,6 +33,9 @@ struct LayerW {
   uint8_t *pqkv, *po, *pgu, *pd;                                     // packed GEMM copies (pack_weight)
 };
 
+bool is_packed_tensor(const std::string& n);
+constexpr size_t kNoOff = ~size_t(0);  // compact weights: tensor held only in packed form
+
 // ------------------------------------------------------------------ weight layout
 struct WeightLayout {
   // row i of a tensor lives at byte off + ((i / row_block) * block_stride + i % row_block) * cols * 2
@@ -43,12 +46,21 @@ struct WeightLayout {
   };
   std::vector<Ent> ents;
   size_t total = 0;
+  bool compact = false;  // projection matrices get no staging storage
   void add(const std::string& n, size_t rows, size_t cols) {
+    if (compact && is_packed_tensor(n)) {
+      ents.push_back({n, kNoOff, rows * cols, rows, cols, rows, rows});
+      return;
+    }
     ents.push_back({n, total, rows * cols, rows, cols, rows, rows});
     total += al(rows * cols * 2);
   }
   // q/k/v (and their biases) must be contiguous: add them unaligned in one run
   void add_run(const std::vector<std::pair<std::string, size_t>>& run, size_t cols) {
+    if (compact && is_packed_tensor(run[0].first)) {
+      for (auto& e : run) ents.push_back({e.first, kNoOff, e.second * cols, e.second, cols, e.second, e.second});
+      return;
+    }
     size_t off = total;
     for (auto& e : run) {
       ents.push_back({e.first, off, e.second * cols, e.second, cols, e.second, e.second});
@@ -59,9 +71,10 @@ struct WeightLayout {
   // gate / up rows interleaved in 64-row blocks: one 128-row GEMM tile holds the
   // gate and up rows of the same 64 outputs (fused SiLU-mul epilogue)
   void add_gate_up(const std::string& g, const std::string& u, size_t ff, size_t cols) {
-    ents.push_back({g, total, ff * cols, ff, cols, 64, 128});
-    ents.push_back({u, total + 64 * cols * 2, ff * cols, ff, cols, 64, 128});
-    total += al(2 * ff * cols * 2);
+    const size_t o = compact ? kNoOff : total;
+    ents.push_back({g, o, ff * cols, ff, cols, 64, 128});
+    ents.push_back({u, compact ? kNoOff : total + 64 * cols * 2, ff * cols, ff, cols, 64, 128});
+    if (!compact) total += al(2 * ff * cols * 2);
   }
   const Ent* find(const std::string& n) const {
     for (auto& e : ents)
@@ -72,6 +85,7 @@ struct WeightLayout {
 
 WeightLayout make_layout(const srl_model_cfg& m) {
   WeightLayout w;
+  w.compact = m.weights_compact != 0;
   const size_t d = m.d, qd = (size_t)m.Hq * m.dh, kd = (size_t)m.Hkv * m.dh, ff = m.ff;
   w.add("embed", m.V, d);
   for (int l = 0; l < m.L; ++l) {
@@ -107,6 +121,9 @@ PackedLayout make_packed(const srl_model_cfg& m, size_t staging_total) {
   p.total = p.base + p.lm + al(packed_weight_bytes(m.V, d));
   return p;
 }
+// compact weights pack q / k / v separately: each must cover whole 128-row tiles
+bool compact_ok(const srl_model_cfg& m) { return (m.Hq * m.dh) % 128 == 0 && (m.Hkv * m.dh) % 128 == 0; }
+
 bool is_packed_tensor(const std::string& n) {
   static const char* kSuffix[] = {".wq", ".wk", ".wv", ".wo", ".wg", ".wu", ".wd"};
   if (n == "lm_head") return true;
@@ -142,6 +159,7 @@ int validate(const srl_model_cfg* m, const srl_sched_cfg* s, int world, std::str
   if (m->dh != 32 && m->dh != 64 && m->dh != 128) return why = "dh must be 32, 64 or 128", -1;
   if (m->d % 128 || (m->Hq * m->dh) % 64 || m->ff % 128) return why = "d, ff must be multiples of 128 and Hq*dh of 64", -1;
   if (m->d > 8192) return why = "d must be <= 8192", -1;
+  if (m->weights_compact && !compact_ok(*m)) return why = "compact weights need Hq*dh and Hkv*dh multiples of 128", -1;
   if (s->Q_g <= 0 || s->U <= 0 || s->G <= 0 || s->cap <= 0 || s->pool_prompts <= 0 || s->kv_pages <= 0)
     return why = "Q_g, U, G, cap, pool_prompts, kv_pages must be positive", -1;
   if (s->page_tokens != kPage) return why = "page_tokens must be 64", -1;
@@ -558,7 +576,7 @@ int64_t srl_weight_offset(const srl_model_cfg* m, const char* name, int64_t* num
   if (!m || !name) return -1;
   WeightLayout w = make_layout(*m);
   const WeightLayout::Ent* e = w.find(name);
-  if (!e) return -1;
+  if (!e || e->off == kNoOff) return -1;
   if (numel) *numel = (int64_t)e->numel;
   return (int64_t)e->off;
 }
@@ -569,6 +587,9 @@ int32_t srl_weight_layout(const srl_model_cfg* m, const char* name, int64_t* off
   WeightLayout w = make_layout(*m);
   const WeightLayout::Ent* e = w.find(name);
   if (!e) return fail(SRL_E_INVALID_ARG, std::string("srl_weight_layout: unknown tensor ") + name);
+  if (e->off == kNoOff)
+    return fail(SRL_E_INVALID_ARG, std::string("srl_weight_layout: ") + name +
+                                       " is held only in packed form (compact weights): use srl_load_policy_tensor");
   if (offset) *offset = (int64_t)e->off;
   if (rows) *rows = (int64_t)e->rows;
   if (cols) *cols = (int64_t)e->cols;
@@ -616,7 +637,7 @@ int32_t srl_create(const srl_model_cfg* m, const srl_sched_cfg* s, int32_t devic
   e->wl = make_layout(*m);
   auto wp = [&](const std::string& n) -> __nv_bfloat16* {
     const WeightLayout::Ent* en = e->wl.find(n);
-    return en ? (__nv_bfloat16*)(e->W + en->off) : nullptr;
+    return en && en->off != kNoOff ? (__nv_bfloat16*)(e->W + en->off) : nullptr;
   };
   e->embed = wp("embed");
   e->final_norm = wp("final_norm");
@@ -907,8 +928,12 @@ int32_t srl_load_policy_weights(srl_engine* e, const void* flat_w, int64_t versi
   // Pack the projection matrices from the staging-layout source straight into the
   // GEMM weight stream's layout; the remaining tensors (embedding, norms, biases)
   // are read in place, so copy those when the source is the caller's buffer.
+  if (e->m.weights_compact && flat_w)
+    return fail(SRL_E_INVALID_ARG, "srl_load_policy_weights: compact weights are loaded with srl_load_policy_tensor");
   const uint8_t* src = flat_w ? (const uint8_t*)flat_w : e->W;
-  const bool root = e->rank == 0;  // with replicas only rank 0 reads a source; the rest receive
+  // with replicas only rank 0 reads a source (the rest receive); compact weights
+  // were already installed tensor by tensor
+  const bool root = e->rank == 0 && !e->m.weights_compact;
   if (root && src != e->W) {
     for (const auto& en : e->wl.ents)
       if (!is_packed_tensor(en.name))
@@ -940,7 +965,7 @@ int32_t srl_load_policy_weights(srl_engine* e, const void* flat_w, int64_t versi
     // norms, biases).  Packed staging matrices are not decoded from, so not sent.
     std::vector<Range> rr;
     for (const auto& en : e->wl.ents)
-      if (!is_packed_tensor(en.name)) rr.push_back({e->W + en.off, en.numel * 2});
+      if (!is_packed_tensor(en.name) && en.off != kNoOff) rr.push_back({e->W + en.off, en.numel * 2});
     rr.push_back({e->W + e->pk.base, e->pk.total - e->pk.base});
     std::string err;
     Prof p(e, SRL_K_COMM);
@@ -1076,5 +1101,41 @@ extern "C" int32_t srl_local_group_create(int32_t world, void** out) {
 
 extern "C" int32_t srl_local_group_destroy(void* group) {
   local_group_destroy(group);
+  return SRL_OK;
+}
+
+// ------------------------------------------------------------------ compact weights: one tensor at a time
+extern "C" int32_t srl_load_policy_tensor(srl_engine* e, const char* name, const void* src) {
+  if (!e || !name || !src) return fail(SRL_E_INVALID_ARG, "srl_load_policy_tensor: null argument");
+  if (e->group_state == 1) return fail(SRL_E_STATE, "srl_load_policy_tensor: harvest the ready group first");
+  const std::string n(name);
+  const WeightLayout::Ent* en = e->wl.find(n);
+  if (!en) return fail(SRL_E_INVALID_ARG, "srl_load_policy_tensor: unknown tensor " + n);
+  const __nv_bfloat16* s = (const __nv_bfloat16*)src;
+  const srl_model_cfg& m = e->m;
+  int rc = 0;
+  if (!is_packed_tensor(n)) {
+    if (cudaMemcpyAsync(e->W + en->off, src, en->numel * 2, cudaMemcpyDeviceToDevice, e->st) != cudaSuccess) rc = -3;
+  } else if (n == "lm_head") {
+    rc = pack_weight(s, m.V, m.d, e->plm_head, e->st);
+  } else {
+    const int l = atoi(n.c_str() + 1);
+    const std::string t = n.substr(n.find('.') + 1);
+    const LayerW& w = e->lw[l];
+    const size_t kbq = (size_t)m.d / 64, tile = 128ull * 128;  // one packed 128-row x 64-col block, bytes
+    const int qd = m.Hq * m.dh, kd = m.Hkv * m.dh;
+    if (t == "wq") rc = pack_weight(s, qd, m.d, w.pqkv, e->st);
+    else if (t == "wk") rc = pack_weight(s, kd, m.d, w.pqkv + (size_t)(qd / 128) * kbq * tile, e->st);
+    else if (t == "wv") rc = pack_weight(s, kd, m.d, w.pqkv + (size_t)((qd + kd) / 128) * kbq * tile, e->st);
+    else if (t == "wo") rc = pack_weight(s, m.d, qd, w.po, e->st);
+    else if (t == "wd") rc = pack_weight(s, m.d, m.ff, w.pd, e->st);
+    else if (t == "wg") rc = pack_weight_rows(s, m.ff, m.d, w.pgu, 64, 128, 0, e->st);
+    else if (t == "wu") rc = pack_weight_rows(s, m.ff, m.d, w.pgu, 64, 128, 64, e->st);
+    else return fail(SRL_E_INVALID_ARG, "srl_load_policy_tensor: not loadable: " + n);
+    if (!e->m.weights_compact && en->off != kNoOff)  // keep the staging image consistent too
+      cudaMemcpyAsync(e->W + en->off, src, en->numel * 2, cudaMemcpyDeviceToDevice, e->st);
+  }
+  e->launches++;
+  if (rc || cudaGetLastError() != cudaSuccess) return cuda_fail("srl_load_policy_tensor");
   return SRL_OK;
 }

@@ -705,6 +705,33 @@ __global__ void pack_weight_kernel(const __nv_bfloat16* __restrict__ src, int N,
 
 size_t packed_weight_bytes(int N, int K) { return (size_t)((N + 127) / 128) * 128 * (size_t)K * 2; }
 
+// source row i -> packed row (i / rb) * bs + off + i % rb (the gate / up interleave)
+__global__ void pack_weight_rows_kernel(const __nv_bfloat16* __restrict__ src, int n, int K, uint4* __restrict__ dst,
+                                        int rb, int bs, int off, long long nchunks) {
+  const int kb = K / 64;
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < nchunks;
+       g += (long long)gridDim.x * blockDim.x) {
+    const long long cpr = (long long)K / 8;  // 16-byte chunks per source row
+    const int i = (int)(g / cpr);
+    const int cc = (int)(g % cpr);
+    const int k = cc >> 3, c = cc & 7;
+    const int row = (i / rb) * bs + off + i % rb;
+    const int t = row >> 7, r = row & 127;
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + (size_t)i * K) + cc);
+    dst[((long long)t * kb + k) * 1024 + r * 8 + (c ^ (r & 7))] = v;
+  }
+}
+
+int pack_weight_rows(const __nv_bfloat16* src, int n, int K, void* dst, int rb, int bs, int off, cudaStream_t stream) {
+  if (n <= 0 || K <= 0 || K % 64 || rb <= 0) return -1;
+  const long long nchunks = (long long)n * K / 8;
+  long long blocks = (nchunks + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  pack_weight_rows_kernel<<<(int)blocks, 256, 0, stream>>>(src, n, K, reinterpret_cast<uint4*>(dst), rb, bs, off,
+                                                           nchunks);
+  return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
+
 int pack_weight(const __nv_bfloat16* src, int N, int K, void* dst, cudaStream_t stream) {
   if (N <= 0 || K <= 0 || K % 64) return -1;
   const long long nchunks = (long long)packed_weight_bytes(N, K) / 16;

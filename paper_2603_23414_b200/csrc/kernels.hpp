@@ -55,5 +55,8 @@ void gemm_set_debug(unsigned long long* buf, int target);
 // chunk c ^ (r % 8)); rows past N are zero.  One block = one contiguous bulk copy.
 size_t packed_weight_bytes(int N, int K);
 int pack_weight(const __nv_bfloat16* src, int N, int K, void* dst, cudaStream_t stream);
+// pack n source rows into the packed image, source row i landing on row
+// (i / rb) * bs + off + i % rb (rows of the other rb-blocks are left as they are)
+int pack_weight_rows(const __nv_bfloat16* src, int n, int K, void* dst, int rb, int bs, int off, cudaStream_t stream);
 
 }  // namespace srl

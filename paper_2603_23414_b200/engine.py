@@ -67,7 +67,7 @@ class RolloutEngine:
 
     def __init__(self, model, sched, *, max_traj: int, max_prompt: int, prefill_chunk: int = 2048,
                  device: int = 0, stream=None, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
-                 local_group: LocalGroup | None = None):
+                 local_group: LocalGroup | None = None, compact_weights: bool = False):
         """world > 1 (or an explicit nccl_id / local_group) makes this engine rank
         `rank` of a lockstep replica group: NCCL when `nccl_id` is given (one process
         per GPU), in-process when `local_group` is."""
@@ -76,8 +76,9 @@ class RolloutEngine:
         self.lib = _lib.load()
         self.model, self.sched = model, sched
         self.dev = torch.device("cuda", device)
+        self.compact = bool(compact_weights)
         self.m = ModelCfg(model.L, model.d, model.Hq, model.Hkv, model.dh, model.ff, model.V,
-                          float(model.rope_theta), float(model.rms_eps), int(model.qkv_bias))
+                          float(model.rope_theta), float(model.rms_eps), int(model.qkv_bias), int(self.compact))
         self.s = SchedCfg(sched.Q_g, sched.U, sched.K, sched.pool_prompts, sched.G, sched.cap, sched.page_tokens,
                           sched.kv_pages, sched.mode, sched.resume, sched.barrier, sched.stop, sched.eos_id,
                           sched.kv_dtype, float(sched.temperature), int(sched.sample_seed), max_traj, max_prompt,
@@ -124,6 +125,12 @@ class RolloutEngine:
         if rb == r:
             return W16[o:o + r * c].view(r, c) if c > 1 else W16[o:o + r]
         return W16.as_strided((r // rb, rb, c), (bs * c, c, 1), o)
+
+    def load_policy_tensor(self, name: str, src):
+        """Install one tensor of the next policy (row-major bf16 device tensor)."""
+        self._sync_in()
+        return check(self.lib.srl_load_policy_tensor(self.h, name.encode(), C.c_void_p(src.data_ptr())),
+                     "srl_load_policy_tensor")
 
     def _sync_in(self):
         """Order the engine stream after work torch queued on the current stream."""

@@ -81,3 +81,26 @@ def test_arena_sizes_and_validation_on_cpu(lib):
     mats = LLAMA8B.L * ((LLAMA8B.Hq + 2 * LLAMA8B.Hkv) * LLAMA8B.dh * 4096 + 4096 * 4096 + 2 * 14336 * 4096
                         + 4096 * 14336) + LLAMA8B.V * 4096
     assert abs(w.value - (16.06e9 + 2 * mats)) / 16.06e9 < 0.01
+
+
+def test_compact_weights_sizing_on_cpu(lib):
+    """weights_compact: no staging copy of the projections (about half the bytes);
+    packed-only tensors are not addressable; q/k/v must tile by 128 rows."""
+    from paper_2603_23414_b200 import _lib
+    from workload.configs import QWEN32B, TINY
+    L = _lib.load()
+    s = _lib.SchedCfg(64, 64, -1, 256, 1, 16384, 64, 5000, 0, 0, 0, 0, -1, 0, 1.0, 3, 1024, 256, 4096)
+    sizes = []
+    for compact in (0, 1):
+        m = _lib.ModelCfg(QWEN32B.L, QWEN32B.d, QWEN32B.Hq, QWEN32B.Hkv, QWEN32B.dh, QWEN32B.ff, QWEN32B.V, 1e6,
+                          1e-5, 1, compact)
+        w = ctypes.c_uint64()
+        assert L.srl_arena_sizes(ctypes.byref(m), ctypes.byref(s), 1, ctypes.byref(w), None, None) == 0
+        sizes.append(w.value)
+        off = L.srl_weight_offset(ctypes.byref(m), b"L3.wg", None)
+        assert (off >= 0) == (compact == 0)
+        assert L.srl_weight_offset(ctypes.byref(m), b"L3.bq", None) >= 0
+    assert abs(sizes[1] - 65.5e9) / 65.5e9 < 0.02 and sizes[0] > 1.9 * sizes[1]
+    mt = _lib.ModelCfg(TINY.L, TINY.d, TINY.Hq, TINY.Hkv, TINY.dh, TINY.ff, TINY.V, 1e4, 1e-5, 0, 1)
+    s.U = 4
+    assert L.srl_arena_sizes(ctypes.byref(mt), ctypes.byref(s), 1, None, None, None) < 0

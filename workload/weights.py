@@ -124,6 +124,14 @@ def fill_engine_weights(eng, m: ModelShape, version: int = 0, seed: int = 2, fla
     (`eng.weight_view(name)` gives each tensor), or into `flat`, a uint8 tensor
     with the same layout."""
     import torch
+    if getattr(eng, "compact", False) and flat is None:
+        # compact engines hold projections only packed: install tensor by tensor
+        for name in weight_names(m):
+            t = gen_weight_torch(m, name, seed=seed, version=version, device=eng.W.device)
+            eng.load_policy_tensor(name, t)
+            eng.stream.synchronize()
+            del t
+        return
     for name in weight_names(m):
         view = eng.weight_view(name)
         if flat is not None:   # same layout inside `flat`
