@@ -91,6 +91,13 @@ __global__ void attn_plan_kernel(AttnArgs a, int split) {
   const int n = min(base_s, a.max_items);
   if (threadIdx.x == 0) *a.n_items = n;
   for (int i = threadIdx.x; i < a.n_ctr; i += blockDim.x) a.work_ctr[i] = 0;
+  if (a.merge_ctr)
+    for (int i = threadIdx.x; i < a.M * a.Hkv; i += blockDim.x) a.merge_ctr[i] = 0;
+  // rows without context get no item: their (bf16) output is zeroed here, once per
+  // forward, so the O projection never reads stale values for them
+  for (int m = 0; m < a.M; ++m)
+    if (a.row_pos[m] < 0)
+      for (int i = threadIdx.x; i < a.Hq * a.dh; i += blockDim.x) a.out[(size_t)m * a.Hq * a.dh + i] = __float2bfloat16(0.f);
   // processing order: counting sort by descending page count (longest first:
   // the persistent CTAs then pull items LPT-style from a counter)
   __shared__ int hist[1024];
@@ -332,6 +339,7 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(mrg + kConsumerWarps * 8 * (DH + 2));
   uint64_t* empty = full + kStages;
   volatile int* hdr = reinterpret_cast<volatile int*>(empty + kStages);  // [kStages] item of each staged page
+  volatile int* merge_flag = hdr + kStages;
 
   const int G = a.Hq / a.Hkv;
   const int w = warp_id(), lane = lane_id();
@@ -518,6 +526,40 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         }
       }
     }
+    if (!single && a.merge_ctr) {
+      // split-KV: the CTA completing the last chunk of (row, kv head) merges all
+      // chunks in chunk order (deterministic whoever arrives last; no second kernel)
+      __threadfence();
+      asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32));
+      const int nch = a.row_nchunk[ii.m];
+      int* ctr = a.merge_ctr + ii.m * a.Hkv + ii.kvh;
+      if (threadIdx.x == 0) {
+        const int last = atomicAdd(ctr, 1) == nch - 1;
+        if (last) *ctr = 0;
+        __threadfence();
+        *merge_flag = last;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32));
+      if (*merge_flag) {
+        const int it0 = a.row_item0[ii.m] + ii.kvh * nch;
+        for (int i = threadIdx.x; i < G * DH; i += kConsumerWarps * 32) {
+          const int g = i / DH, d = i % DH;
+          float mx = -INFINITY;
+          for (int c = 0; c < nch; ++c) mx = fmaxf(mx, __ldcg(a.part_ml + ((size_t)(it0 + c) * G + g) * 2));
+          float acc = 0.f, l = 0.f;
+          for (int c = 0; c < nch; ++c) {
+            const float mc = __ldcg(a.part_ml + ((size_t)(it0 + c) * G + g) * 2);
+            const float f = mc == -INFINITY ? 0.f : exp2f(mc - mx);
+            acc += __ldcg(a.part_o + ((size_t)(it0 + c) * G + g) * DH + d) * f;
+            l += __ldcg(a.part_ml + ((size_t)(it0 + c) * G + g) * 2 + 1) * f;
+          }
+          const float o = acc / l;
+          const size_t oi = ((size_t)ii.m * a.Hq + ii.kvh * G + g) * DH + d;
+          a.out[oi] = __float2bfloat16(o);
+          if (a.out_f32) a.out_f32[oi] = o;
+        }
+      }
+    }
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32));
   }
 }
@@ -556,8 +598,10 @@ void attn_run(const AttnArgs& a, bool kv_fp32, const void* tmap_k, const void* t
       default: return;
     }
   }
-  const int warps = a.M * a.Hq;
-  launch_k(attn_combine_kernel<false>, dim3((warps + 7) / 8), dim3(256), 0, st, 1, a, (float*)nullptr);
+  if (kv_fp32 || !a.merge_ctr) {  // the bf16 kernel merges split-KV chunks itself
+    const int warps = a.M * a.Hq;
+    launch_k(attn_combine_kernel<false>, dim3((warps + 7) / 8), dim3(256), 0, st, 1, a, (float*)nullptr);
+  }
 }
 
 void attn_combine_f32(const AttnArgs& a, float* out_f32, cudaStream_t st) {

@@ -382,6 +382,7 @@ void plan_scratch(srl_engine* e, ScratchPlan& p, bool assign) {
   a.order = (int*)P(4ull * z.max_items);
   a.work_ctr = (int*)P(4ull * m.L);
   a.n_ctr = m.L;
+  a.merge_ctr = (int*)P(4ull * z.mmax * m.Hkv);
   a.n_items = (int*)P(64);
   a.row_item0 = (int*)P(4ull * z.mmax);
   a.row_nchunk = (int*)P(4ull * z.mmax);

@@ -39,6 +39,7 @@ struct AttnArgs {
   int* order;            // [max_items] item ids by descending page count
   int* work_ctr;         // this launch's counter; the plan kernel zeroes work_ctr[0..n_ctr)
   int n_ctr;
+  int* merge_ctr;        // [M * Hkv] split-KV chunk arrivals (zeroed by the plan kernel, reset by the merger)
 };
 void attn_plan(const AttnArgs& a, int split, cudaStream_t st);
 void attn_run(const AttnArgs& a, bool kv_fp32, const void* tmap_k, const void* tmap_v, cudaStream_t st);

@@ -9,8 +9,9 @@
 //   lp   = z_tok*invT - (m + log sum_j exp(z_j*invT - m))
 // The token decision is bit-reproducible against the CPU oracle because every
 // operation on its path is a correctly rounded fp32 op (__fmul_rn/__fadd_rn/
-// __fdiv_rn) in the order the algorithm states; the logprob uses a parallel
-// reduction and is compared with a tolerance (reading R15).
+// __fdiv_rn) in the order the algorithm states; candidates that provably lose
+// (a cheap logf-based bound) skip the exact evaluation.  The logprob uses a
+// parallel reduction and is compared with a tolerance (reading R15).
 #include "common.cuh"
 #include "launch.hpp"
 #include "layers.hpp"
@@ -88,6 +89,13 @@ __device__ __forceinline__ float gumbel_from_bits(uint32_t x) {
   return -log_rn(-log_rn(u));
 }
 
+// pruning bound (see sample_kernel): generous against the <= 1e-5 deviation
+constexpr float kPrune = 1e-3f;
+__device__ __forceinline__ float gumbel_fast(uint32_t x) {
+  const float u = ((float)(x >> 9) * 2.0f + 1.0f) * 5.9604644775390625e-08f;  // exact (24-bit integer * 2^-24)
+  return -logf(-logf(u));
+}
+
 __device__ __forceinline__ bool better(float s, int j, float bs, int bj) {
   return s > bs || (s == bs && j < bj);
 }
@@ -120,10 +128,16 @@ __global__ void __launch_bounds__(kSampThreads) sample_kernel(SampleArgs a) {
       const int j = j4 + q;
       if (j < a.V) {
         const float zs = __fmul_rn(z[j], invT);
-        const float s = __fadd_rn(zs, gumbel_from_bits(ws[q]));
-        if (better(s, j, bs, bj)) {
-          bs = s;
-          bj = j;
+        // Exact score only where it could win: g_fast (CUDA logf, <= 1 ulp each)
+        // is within 1e-5 of the RN msun value for u in [2^-24, 1 - 2^-24] (|g| <= 16.6),
+        // so zs + g_fast + kPrune < bs proves exact(s) < bs.  The decision is
+        // unchanged; most of the V - 1 losers skip the two RN-only logs.
+        if (__fadd_rn(zs, gumbel_fast(ws[q])) + kPrune + 1e-6f * fabsf(bs) >= bs) {
+          const float s = __fadd_rn(zs, gumbel_from_bits(ws[q]));
+          if (better(s, j, bs, bj)) {
+            bs = s;
+            bj = j;
+          }
         }
         if (zs > mx) {
           sum = sum * expf(mx - zs) + 1.f;
