@@ -213,6 +213,29 @@ def run_gpu(args, rank, world, dist):
         eng.submit_prompts(ids[lo:hi], (o - o[0]).astype(np.int32), toks[o[0]:o[-1]], L[lo:hi])
         st["sub"] = hi
 
+    if args.full:
+        # the whole job: both epochs from the first admission to the last emitted
+        # group, device-timed end to end (includes the epoch-start prefill bursts and
+        # the TRAINED-barrier drains that carry the bubble)
+        submit(0, min(n_prompts, 2 * pool * world))
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0 = eng.counters()
+        with ClockSampler(dev) as clk:
+            e0.record(stream)
+            rounds = 0
+            while one_round():
+                rounds += 1
+            e1.record(stream)
+            torch.cuda.synchronize()
+        c1 = eng.counters()
+        ms = e0.elapsed_time(e1)
+        eng.close()
+        return dict(ms=ms, ran=rounds, raw=(c1["raw_tokens"] - c0["raw_tokens"]) / world, useful=st["useful"] / world,
+                    stats=trace, prof={"attention": (0.0, 0)}, launches=c1["kernel_launches"] - c0["kernel_launches"],
+                    clocks=clk.summary(), e2e=None, trace=trace, breakdown={}, n_break=0)
     # the first two epochs are resident; the e2e leg streams the rest from host memory
     submit(0, min(n_prompts, 2 * pool * world))
     for _ in range(args.precondition):
@@ -372,6 +395,8 @@ def main():
     ap.add_argument("--model", default="llama8b", choices=sorted(MODELS),
                     help="llama8b = BASELINE configs[1] (default); qwen32b = the per-GPU slice of configs[3]")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--full", action="store_true",
+                    help="time the whole 2-epoch rollout (every round, incl. epoch starts and drains) instead")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
@@ -449,8 +474,9 @@ def main():
                    "step": "one early-update round: decode steps (refill, prefill, decode GEMMs, paged attention, "
                            "Philox sampling, stop detection, compaction) until the length-sorted update group of "
                            "U=64 is ready, its harvest, and the policy refresh (load_policy_weights, K bound)",
-                   "window": f"after {args.precondition} untimed decode steps and {args.warmup} untimed rounds; "
-                             f"{n_dec} decode steps timed",
+                   "window": (f"the whole 2-epoch rollout: {steps} rounds, {n_dec} decode steps" if args.full else
+                              f"after {args.precondition} untimed decode steps and {args.warmup} untimed rounds; "
+                              f"{n_dec} decode steps timed"),
                    "l2": "no flush needed: every decode step streams 15 GB of weights + the KV cache (>> 126 MB L2)",
                    "parallelism": f"dp{world} lockstep replicas (NCCL)" if world > 1 else "dp1"},
         "decode_steps": n_dec,

@@ -28,22 +28,32 @@ constexpr float kLog2e = 1.4426950408889634f;
 // drain phase of a rollout: few long sequences); otherwise one item per pair
 // and the attention kernel writes the normalised output itself.
 constexpr int kMinItems = 4 * 148;
+constexpr int kTargetItems = 6 * 148;
 __global__ void attn_plan_kernel(AttnArgs a, int split) {
   __shared__ int wsum[32];
-  __shared__ int base_s, active_s;
+  __shared__ int base_s, active_s, pages_s;
   pdl_trigger();
   pdl_wait();
   if (threadIdx.x == 0) {
     base_s = 0;
     active_s = 0;
+    pages_s = 0;
   }
   __syncthreads();
-  int my_active = 0;
-  for (int m = threadIdx.x; m < a.M; m += blockDim.x) my_active += a.row_pos[m] >= 0;
+  int my_active = 0, my_pages = 0;
+  for (int m = threadIdx.x; m < a.M; m += blockDim.x) {
+    my_active += a.row_pos[m] >= 0;
+    my_pages += (a.row_pos[m] + 1 + 63) / 64;
+  }
   atomicAdd(&active_s, my_active);
+  atomicAdd(&pages_s, my_pages);
   __syncthreads();
   if (active_s * a.Hkv >= kMinItems) split = 0;
-  const int chunk_tok = 64 * kChunkPages;
+  // split-KV chunk: about kTargetItems items over all (row, head) pairs, never
+  // below kChunkPages pages (per-item overhead: q load, 4-warp merge, partials)
+  const int cp = max(kChunkPages, min(256, (pages_s * a.Hkv + kTargetItems - 1) / kTargetItems));
+  if (threadIdx.x == 0) *a.chunk_pages = cp;
+  const int chunk_tok = 64 * cp;
   for (int b0 = 0; b0 < a.M; b0 += blockDim.x) {
     const int m = b0 + threadIdx.x;
     int nch = 0;
@@ -106,7 +116,7 @@ __global__ void attn_plan_kernel(AttnArgs a, int split) {
   auto bucket = [&](int it) {
     const int m = a.items[it * 3], c = a.items[it * 3 + 2];
     const int npages = (a.row_pos[m] + 1 + 63) / 64;
-    const int pg = a.row_nchunk[m] == 1 ? npages : min(npages - c * kChunkPages, kChunkPages);
+    const int pg = a.row_nchunk[m] == 1 ? npages : min(npages - c * cp, cp);
     return 1023 - min(pg, 1023);
   };
   for (int it = threadIdx.x; it < n; it += blockDim.x) atomicAdd(&hist[bucket(it)], 1);
@@ -189,7 +199,8 @@ __global__ void __launch_bounds__(kF32Threads) attn_f32_kernel(AttnArgs a) {
   pdl_trigger();
   pdl_wait();
   const int G = a.Hq / a.Hkv;
-  const int chunk_tok = 64 * kChunkPages;
+  const int chunk_tok = 64 * kChunkPages;  // scores staged per block (smem); a chunk spans several
+  const int item_tok = 64 * *a.chunk_pages;
   float* sq = sm;                       // [G][dh]
   float* ss = sq + G * a.dh;            // [G][chunk_tok]
   const int n_items = *a.n_items;
@@ -197,8 +208,8 @@ __global__ void __launch_bounds__(kF32Threads) attn_f32_kernel(AttnArgs a) {
     const int m = a.items[it * 3], kvh = a.items[it * 3 + 1], c = a.items[it * 3 + 2];
     const int ctx = a.row_pos[m] + 1;
     const int nch = a.row_nchunk[m];
-    const int t0 = nch == 1 ? 0 : c * chunk_tok;
-    const int t1 = nch == 1 ? ctx : min(ctx, t0 + chunk_tok);
+    const int t0 = nch == 1 ? 0 : c * item_tok;
+    const int t1 = nch == 1 ? ctx : min(ctx, t0 + item_tok);
     const int slot = a.row_slot[m];
     const float* qrow = reinterpret_cast<const float*>(a.q) + ((size_t)m * a.Hq + kvh * G) * a.dh;
     const float* kp = reinterpret_cast<const float*>(a.k_pool);
@@ -318,8 +329,9 @@ __device__ __forceinline__ ItemInfo item_info(const AttnArgs& a, int it) {
     r.p0 = 0;
     r.p1 = npages;
   } else {
-    r.p0 = c * kChunkPages;
-    r.p1 = min(npages, r.p0 + kChunkPages);
+    const int cp = *a.chunk_pages;
+    r.p0 = c * cp;
+    r.p1 = min(npages, r.p0 + cp);
   }
   r.slot = a.row_slot[r.m];
   return r;
@@ -529,11 +541,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     if (!single && a.merge_ctr) {
       // split-KV: the CTA completing the last chunk of (row, kv head) merges all
       // chunks in chunk order (deterministic whoever arrives last; no second kernel)
-      __threadfence();
+      // CTA barrier, then one fenced atomic by one thread (CUTLASS semaphore pattern)
       asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32));
       const int nch = a.row_nchunk[ii.m];
       int* ctr = a.merge_ctr + ii.m * a.Hkv + ii.kvh;
       if (threadIdx.x == 0) {
+        __threadfence();  // release: the CTA's partials (ordered by the barrier) before the count
         const int last = atomicAdd(ctr, 1) == nch - 1;
         if (last) *ctr = 0;
         __threadfence();

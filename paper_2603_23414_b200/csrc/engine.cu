@@ -383,6 +383,7 @@ void plan_scratch(srl_engine* e, ScratchPlan& p, bool assign) {
   a.work_ctr = (int*)P(4ull * m.L);
   a.n_ctr = m.L;
   a.merge_ctr = (int*)P(4ull * z.mmax * m.Hkv);
+  a.chunk_pages = (int*)P(64);
   a.n_items = (int*)P(64);
   a.row_item0 = (int*)P(4ull * z.mmax);
   a.row_nchunk = (int*)P(4ull * z.mmax);
@@ -395,10 +396,19 @@ size_t kv_bytes_for(const srl_model_cfg& m, const srl_sched_cfg& s) {
   return al((size_t)s.kv_pages * m.Hkv * kPage * m.dh * el) * 2 * m.L;
 }
 
+// Timing ablation (never for results): SRL_DEBUG_SKIP=<hex mask of SRL_K_* classes>
+// drops those launches from the DECODE path, to measure what each class really
+// costs inside the PDL-linked graph (per-class events would cut those links).
+bool debug_skip(int cls) {
+  static const unsigned mask = getenv("SRL_DEBUG_SKIP") ? (unsigned)strtoul(getenv("SRL_DEBUG_SKIP"), nullptr, 16) : 0u;
+  return cls >= 0 && ((mask >> cls) & 1u);
+}
+
 // ---- fused GEMM helper
 // one fused GEMM launch, profiled under `cls`
 void run_gemm(srl_engine* e, int cls, const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N, int K,
               const GemmEpi& epi) {
+  if (debug_skip(cls)) return;
   Prof p(e, cls);
   gemm_bf16_fused(X, M, W, N, K, epi, e->num_sms, e->st);
   e->launches++;
@@ -428,7 +438,7 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
     Prof p1(e, D + SRL_K_ATTN);
     attn_plan(a, decode ? 1 : 0, st);
   }
-  {
+  if (!debug_skip(D + SRL_K_ELEMWISE)) {
     Prof p2(e, D + SRL_K_ELEMWISE);
     rmsnorm(e->x_res, row_tok, row_pos, M, d, e->embed, e->lw[0].attn_norm, m.rms_eps, e->xn, st);
   }
@@ -469,18 +479,18 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
     a.k_pool = e->kpool[l];
     a.v_pool = e->vpool[l];
     a.work_ctr = e->attn.work_ctr + l;  // one counter per layer, all zeroed by attn_plan
-    {
+    if (!debug_skip(D + SRL_K_ATTN)) {
       Prof p(e, D + SRL_K_ATTN, 2);
       attn_run(a, e->kv_f32, &e->tmK[l], &e->tmV[l], st);
     }
     run_gemm(e, D + SRL_K_GEMM_O, e->attn_out, M, (const __nv_bfloat16*)w.po, d, qd, re);
-    {
+    if (!debug_skip(D + SRL_K_ELEMWISE)) {
       Prof p(e, D + SRL_K_ELEMWISE);
       rmsnorm(e->x_res, row_tok, row_pos, M, d, nullptr, w.mlp_norm, m.rms_eps, e->xn, st);
     }
     run_gemm(e, D + SRL_K_GEMM_GU, e->xn, M, (const __nv_bfloat16*)w.pgu, 2 * m.ff, d, se);  // interleaved gate/up
     run_gemm(e, D + SRL_K_GEMM_DOWN, e->act, M, (const __nv_bfloat16*)w.pd, d, m.ff, re);
-    {
+    if (!debug_skip(D + SRL_K_ELEMWISE)) {
       Prof p(e, D + SRL_K_ELEMWISE);
       const __nv_bfloat16* next = l + 1 < m.L ? e->lw[l + 1].attn_norm : e->final_norm;
       rmsnorm(e->x_res, row_tok, row_pos, M, d, nullptr, next, m.rms_eps, e->xn, st);
@@ -516,7 +526,7 @@ void decode_tail(srl_engine* e, bool with_end) {
   sa.seed = e->s.sample_seed;
   sa.tok_out = c.samp + (size_t)e->rank * 2 * e->s.Q_g;
   sa.lp_out = (float*)(c.samp + (size_t)e->rank * 2 * e->s.Q_g + e->s.Q_g);
-  {
+  if (!debug_skip(SRL_K_SAMPLE)) {
     Prof p(e, SRL_K_SAMPLE);
     sample(sa, st);
   }

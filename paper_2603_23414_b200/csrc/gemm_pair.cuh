@@ -311,14 +311,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         // [slot][row half][chunk][4 column quads][128 rows] float4, coalesced per warp)
         float4* dst = reinterpret_cast<float4*>(p.sk_ws) +
                       ((size_t)(sk_slot(p, pid, u) * 2 + (int)r2) * cmax) * 512 + n;
-        for (int c = eg; c < nchunk; c += 2) {
+        int c = eg;
+        for (; c + 2 < nchunk; c += 4) {  // two TMEM loads in flight per wait
+          float va[16], vb[16];
+          tmem_ld16x2(tl + (uint32_t)(c * 16), tl + (uint32_t)((c + 2) * 16), va, vb);
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            __stcg(dst + (size_t)c * 512 + q4 * 128, make_float4(va[4 * q4], va[4 * q4 + 1], va[4 * q4 + 2], va[4 * q4 + 3]));
+            __stcg(dst + (size_t)(c + 2) * 512 + q4 * 128,
+                   make_float4(vb[4 * q4], vb[4 * q4 + 1], vb[4 * q4 + 2], vb[4 * q4 + 3]));
+          }
+        }
+        for (; c < nchunk; c += 2) {
           float v[16];
           tmem_ld16(tl + (uint32_t)(c * 16), v);
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4)
             __stcg(dst + (size_t)c * 512 + q4 * 128, make_float4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]));
         }
-        __threadfence();  // this thread's partial is visible device-wide before the count
       }
       tc_fence_before();
       __syncwarp();
@@ -328,6 +338,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         // count the piece in; the CTA completing the count reduces the unit (this row half)
         int q0, q1;
         sk_unit_pairs(p, u, &q0, &q1);
+        // CTA barrier, then one release by one thread (the CUTLASS semaphore pattern):
+        // every epilogue thread's partial stores happen before the count
         asm volatile("bar.sync 4, 256;" ::: "memory");
         if (w == 2 && lane == 0) {
           __threadfence();
@@ -344,23 +356,36 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             float v[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) v[j] = 0.f;
-            for (int q = q0; q <= q1; ++q) {  // pair order = k order: deterministic
-              const float4* src = reinterpret_cast<const float4*>(p.sk_ws) +
-                                  ((size_t)(sk_slot(p, q, u) * 2 + (int)r2) * cmax + c) * 512 + n;
+            // pair order = k order: deterministic.  Loads are issued in batches of
+            // four pieces before the first add, so L2 latency is paid once per batch.
+            for (int qb = q0; qb <= q1; qb += 4) {
+              float4 x[4][4];
 #pragma unroll
-              for (int q4 = 0; q4 < 4; ++q4) {
-                const float4 x = ldcg_f4(src + q4 * 128);
-                v[4 * q4] += x.x;
-                v[4 * q4 + 1] += x.y;
-                v[4 * q4 + 2] += x.z;
-                v[4 * q4 + 3] += x.w;
-              }
+              for (int qq = 0; qq < 4; ++qq)
+                if (qb + qq <= q1) {
+                  const float4* src = reinterpret_cast<const float4*>(p.sk_ws) +
+                                      ((size_t)(sk_slot(p, qb + qq, u) * 2 + (int)r2) * cmax + c) * 512 + n;
+#pragma unroll
+                  for (int q4 = 0; q4 < 4; ++q4) x[qq][q4] = ldcg_f4(src + q4 * 128);
+                }
+#pragma unroll
+              for (int qq = 0; qq < 4; ++qq)
+                if (qb + qq <= q1)
+#pragma unroll
+                  for (int q4 = 0; q4 < 4; ++q4) {
+                    v[4 * q4] += x[qq][q4].x;
+                    v[4 * q4 + 1] += x[qq][q4].y;
+                    v[4 * q4 + 2] += x[qq][q4].z;
+                    v[4 * q4 + 3] += x[qq][q4].w;
+                  }
             }
             apply_epilogue(p, unit_n0, n, m_base + c * 16, v, xg, 1 + eg, rtab + c * 16);
           }
+          if (w == 2 && lane == 0) DBG(15);
         }
       }
     }
+    if (w == 2 && lane == 0) DBG(14);
   }
 
   if (SPLIT == 1) {

@@ -15,7 +15,7 @@ void rmsnorm(float* x_res, const int* row_tok, const int* row_pos, int M, int d,
 // ---- attention.cu
 // Work item = (row, kv head, chunk of kChunkPages pages).  The plan kernel
 // builds the item list from row_pos (ctx = pos + 1).
-constexpr int kChunkPages = 4;  // 256 tokens per work item
+constexpr int kChunkPages = 4;  // smallest split-KV chunk (pages); the plan kernel picks >= this
 struct AttnArgs {
   const void* q;         // [M][Hq][dh] bf16 or fp32
   const void* k_pool;    // [pages][Hkv][64][dh]
@@ -40,6 +40,7 @@ struct AttnArgs {
   int* work_ctr;         // this launch's counter; the plan kernel zeroes work_ctr[0..n_ctr)
   int n_ctr;
   int* merge_ctr;        // [M * Hkv] split-KV chunk arrivals (zeroed by the plan kernel, reset by the merger)
+  int* chunk_pages;      // device int: split-KV chunk size in pages, chosen by the plan kernel
 };
 void attn_plan(const AttnArgs& a, int split, cudaStream_t st);
 void attn_run(const AttnArgs& a, bool kv_fp32, const void* tmap_k, const void* tmap_v, cudaStream_t st);

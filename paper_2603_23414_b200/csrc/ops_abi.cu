@@ -102,11 +102,12 @@ static size_t attn_ws_layout(int M, int Hq, int Hkv, int dh, int max_ctx, size_t
   offs[8] = o; o += al256(4ull * items);              // order
   offs[9] = o; o += al256(64);                        // work counter
   offs[10] = o; o += al256(4ull * M * Hkv);           // split-KV merge counters
+  offs[11] = o; o += al256(64);                       // chunk size
   return o;
 }
 
 extern "C" int64_t srl_op_attention_workspace(int32_t M, int32_t Hq, int32_t Hkv, int32_t dh, int32_t max_ctx) {
-  size_t offs[11];
+  size_t offs[12];
   if (M <= 0 || Hq <= 0 || Hkv <= 0 || Hq % Hkv || dh <= 0 || max_ctx <= 0) return -1;
   return (int64_t)attn_ws_layout(M, Hq, Hkv, dh, max_ctx, offs);
 }
@@ -125,7 +126,7 @@ extern "C" int32_t srl_op_attention(const void* q, const void* k_pool, const voi
     return -1;
   }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  size_t offs[11];
+  size_t offs[12];
   attn_ws_layout(M, Hq, Hkv, dh, max_ctx, offs);
   uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
   AttnArgs a{};
@@ -154,6 +155,7 @@ extern "C" int32_t srl_op_attention(const void* q, const void* k_pool, const voi
   a.work_ctr = reinterpret_cast<int*>(ws + offs[9]);
   a.n_ctr = 1;
   a.merge_ctr = reinterpret_cast<int*>(ws + offs[10]);
+  a.chunk_pages = reinterpret_cast<int*>(ws + offs[11]);
   iota_kernel<<<(M + 255) / 256, 256, 0, st>>>(const_cast<int*>(a.row_slot), M);
   CUtensorMap tk, tv;
   if (!kv_fp32) {
