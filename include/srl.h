@@ -51,7 +51,12 @@ extern "C" {
 #define SRL_E_NCCL (-7)
 
 /* ---- enums */
-enum { SRL_MODE_SORTED = 0, SRL_MODE_SYNC = 1 };
+/* SORTED: SortedRL.  SYNC: the synchronous baseline -- batches of
+ * Q_tot admitted together, groups of U in completion order.  POSTHOC:
+ * the paper's post-hoc sorting ablation -- a pool of pool_prompts*G
+ * trajectories generated with refill, then, once ALL of it has finished, sorted
+ * groups of U (the last group is |pool|/U - 1 versions stale). */
+enum { SRL_MODE_SORTED = 0, SRL_MODE_SYNC = 1, SRL_MODE_POSTHOC = 2 };
 enum { SRL_RESUME_KEEP_KV = 0, SRL_RESUME_REPREFILL = 1 };   /* reading R10 */
 enum { SRL_BARRIER_TRAINED = 0, SRL_BARRIER_ADMITTED = 1 };  /* reading R8 */
 enum { SRL_STOP_FORCED = 0, SRL_STOP_EOS = 1 };              /* reading R16 */

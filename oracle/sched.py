@@ -27,7 +27,7 @@ import bisect
 from dataclasses import dataclass, field
 from typing import List, Optional
 
-from workload.configs import (BARRIER_ADMITTED, BARRIER_TRAINED, MODE_SORTED, MODE_SYNC,
+from workload.configs import (BARRIER_ADMITTED, BARRIER_TRAINED, MODE_POSTHOC, MODE_SORTED, MODE_SYNC,
                               RESUME_REPREFILL, STOP_EOS, STOP_FORCED, SchedConfig)
 
 # status codes (match include/srl.h)
@@ -81,7 +81,7 @@ class Controller:
             raise SchedError("INVALID_ARG", "Q_g, R, U, G, cap, pool_prompts must be positive")
         if cfg.page_tokens <= 0 or cfg.kv_pages <= 0:
             raise SchedError("INVALID_ARG", "page_tokens and kv_pages must be positive")
-        if cfg.mode == MODE_SORTED and cfg.U > cfg.pool_prompts * cfg.G:
+        if cfg.mode in (MODE_SORTED, MODE_POSTHOC) and cfg.U > cfg.pool_prompts * cfg.G:
             raise SchedError("INVALID_ARG", "U larger than the prompt pool (S:252)")
         if cfg.stop == STOP_EOS and cfg.eos_id < 0:
             raise SchedError("INVALID_ARG", "EOS stop needs eos_id")
@@ -190,7 +190,7 @@ class Controller:
             return False
         if self.loaded == 0:
             return True
-        if cfg.mode == MODE_SYNC or cfg.barrier == BARRIER_TRAINED:
+        if cfg.mode in (MODE_SYNC, MODE_POSTHOC) or cfg.barrier == BARRIER_TRAINED:
             return self.emitted == self.loaded
         # ADMITTED: no trajectory of the latest epoch still pending
         for e in self.resumed:
@@ -276,6 +276,10 @@ class Controller:
                     t.pages += 1
                     continue
                 cands = [h for h in range(r, cfg.Q_tot, cfg.R) if self.slots[h] is not None]
+                if cands == [g]:
+                    # alone on its replica and still short of pages: preempting itself
+                    # cannot help (with K = 0 it would restart forever) -- reading R25
+                    raise SchedError("CAPACITY", "a trajectory outgrows its replica's KV pool")
                 victim = max(cands, key=lambda h: (self.slots[h].admit_step, h))
                 self._preempt(victim)
 
@@ -289,6 +293,10 @@ class Controller:
             self.ready = self.ready[cfg.U:]
             final = not self.ready
         else:
+            # post-hoc sorting (ablation): nothing is emitted before the whole
+            # loaded batch has finished; then sorted groups of U as in SortedRL
+            if cfg.mode == MODE_POSTHOC and (occupied or not self._pending_empty()):
+                return False
             drain = self._pending_empty() and not occupied and not self._load_possible()
             if len(self.ready) >= cfg.U:
                 group = sorted(self.ready, key=lambda t: (len(t.tokens), t.tid))[:cfg.U]

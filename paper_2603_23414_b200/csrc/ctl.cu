@@ -168,7 +168,8 @@ __device__ bool load_possible(const Ctl& c) {
   const CtlState* s = c.s;
   if (s->next_stream >= s->n_stream) return false;
   if (s->loaded == 0) return true;
-  if (c.mode == SRL_MODE_SYNC || c.barrier == SRL_BARRIER_TRAINED) return s->emitted == s->loaded;
+  if (c.mode == SRL_MODE_SYNC || c.mode == SRL_MODE_POSTHOC || c.barrier == SRL_BARRIER_TRAINED)
+    return s->emitted == s->loaded;
   if (s->fresh_head < s->next_stream) return false;  // the tail of the fresh range is the latest epoch
   for (int i = 0; i < s->n_resumed; ++i)
     if (c.traj[c.resumed[i]].epoch == s->epoch_of_latest) return false;
@@ -208,7 +209,8 @@ __device__ bool emission_check(const Ctl& c, long long* keys) {
         sh_n = min(c.U, s->n_ready);
         sh_final = s->n_ready == sh_n;
       }
-    } else {
+    } else if (c.mode != SRL_MODE_POSTHOC || (pe && occ == 0)) {
+      // (POSTHOC: the sorted groups only once the whole loaded batch has finished)
       const bool drain = pe && occ == 0 && !load_possible(c);
       if (s->n_ready >= c.U) {
         sh_flag = 2;
@@ -286,10 +288,11 @@ __device__ void fill_status(const Ctl& c, int status) {
 __global__ void __launch_bounds__(kCtlThreads, 1) ctl_begin_kernel(Ctl c) {
   extern __shared__ long long keys[];
   __shared__ int sh_free[1024];
-  __shared__ int sh_nfree, sh_ngrow, sh_stop;
+  __shared__ int sh_nfree, sh_ngrow, sh_stop, sh_cap;
   CtlState* s = c.s;
   if (threadIdx.x == 0) {
     sh_stop = 0;
+    sh_cap = 0;
     s->st.n_admit = s->st.n_admit_local = s->st.m_pre = s->st.r_k = s->st.n_fin = 0;
     if (s->group_state != 0 || !s->v_valid) {
       fill_status(c, SRL_E_STATE);
@@ -371,7 +374,7 @@ __global__ void __launch_bounds__(kCtlThreads, 1) ctl_begin_kernel(Ctl c) {
     if (threadIdx.x == 0) sh_ngrow = tot;
     __syncthreads();
     if (threadIdx.x == 0) {
-      for (int i = 0; i < sh_ngrow; ++i) {
+      for (int i = 0; i < sh_ngrow && !sh_cap; ++i) {
         const int gg = sh_free[i];
         const int tid = c.slot_traj[gg];
         if (tid < 0) continue;  // preempted earlier in this loop
@@ -386,15 +389,20 @@ __global__ void __launch_bounds__(kCtlThreads, 1) ctl_begin_kernel(Ctl c) {
             continue;
           }
           // victim: occupied slot of replica r with max (admit_step, slot)
-          int victim = -1, vstep = -1;
+          int victim = -1, vstep = -1, n_occ = 0;
           for (int h = r; h < c.Q_tot; h += c.R) {
             const int vt = c.slot_traj[h];
             if (vt < 0) continue;
+            ++n_occ;
             const int as = c.traj[vt].admit_step;
             if (as > vstep || (as == vstep && h > victim)) {
               vstep = as;
               victim = h;
             }
+          }
+          if (n_occ == 1) {  // alone and still short of pages: it can never fit (reading R25)
+            sh_cap = 1;
+            break;
           }
           const int vt = c.slot_traj[victim];
           DevTraj& v = c.traj[vt];
@@ -409,6 +417,10 @@ __global__ void __launch_bounds__(kCtlThreads, 1) ctl_begin_kernel(Ctl c) {
       }
     }
     __syncthreads();
+  }
+  if (sh_cap) {
+    if (threadIdx.x == 0) fill_status(c, SRL_E_CAPACITY);
+    return;
   }
   // running set
   int occ = 0;

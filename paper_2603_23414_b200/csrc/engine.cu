@@ -165,7 +165,8 @@ int validate(const srl_model_cfg* m, const srl_sched_cfg* s, int world, std::str
   if (s->page_tokens != kPage) return why = "page_tokens must be 64", -1;
   if (world < 1 || world > kMaxR) return why = "world out of range", -1;
   if ((long long)s->Q_g * world > 4096) return why = "Q_tot must be <= 4096", -1;
-  if (s->mode == SRL_MODE_SORTED && s->U > s->pool_prompts * s->G) return why = "U larger than the prompt pool (S:252)", -1;
+  if (s->mode < SRL_MODE_SORTED || s->mode > SRL_MODE_POSTHOC) return why = "mode", -1;
+  if (s->mode != SRL_MODE_SYNC && s->U > s->pool_prompts * s->G) return why = "U larger than the prompt pool (S:252)", -1;
   if (s->U > kMaxGroup) return why = "U too large", -1;
   if (s->stop == SRL_STOP_EOS && s->eos_id < 0) return why = "EOS stop needs eos_id", -1;
   if (s->temperature <= 0.f) return why = "temperature must be > 0", -1;

@@ -19,8 +19,8 @@ from engine_harness import make_engine, run_engine, tiny_workload  # noqa: E402
 from oracle.model import ModelRunner, load_weights  # noqa: E402
 from oracle.sampler import sample_row  # noqa: E402
 from oracle.sched import Controller  # noqa: E402
-from workload.configs import (BARRIER_ADMITTED, BARRIER_TRAINED, K_INF, KV_BF16, KV_FP32, MODE_SORTED,  # noqa: E402
-                              MODE_SYNC, RESUME_KEEP_KV, RESUME_REPREFILL, TINY, SchedConfig)
+from workload.configs import (BARRIER_ADMITTED, BARRIER_TRAINED, K_INF, KV_BF16, KV_FP32, MODE_POSTHOC,  # noqa: E402
+                              MODE_SORTED, MODE_SYNC, RESUME_KEEP_KV, RESUME_REPREFILL, TINY, SchedConfig)
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -66,6 +66,7 @@ SCHED_CASES = [
     ("partial_reprefill", dict(K=K_INF, resume=RESUME_REPREFILL)),
     ("admitted_barrier", dict(K=K_INF, barrier=BARRIER_ADMITTED, pool_prompts=6)),
     ("sync", dict(mode=MODE_SYNC, Q_g=8)),
+    ("posthoc", dict(mode=MODE_POSTHOC, Q_g=6, pool_prompts=8, U=3)),
     ("small_pool_preempt", dict(K=1, kv_pages=6, Q_g=8, pool_prompts=8)),
     ("small_pool_onpolicy", dict(K=0, kv_pages=5, Q_g=8, pool_prompts=8, U=2)),
     ("G2", dict(G=2, pool_prompts=4, U=3)),
@@ -85,6 +86,26 @@ def test_schedule_bit_exact(name, over, kv):
     res = run_engine(eng, TINY, off, toks, L)
     eng.close()
     c, og = _oracle(cfg, off, toks, L)
+    _compare_schedule(res, c, og)
+
+
+PREEMPT_CASES = [("K1_kv4", dict(K=1, kv_pages=4)), ("K0_kv5", dict(K=0, kv_pages=5)),
+                 ("Kinf_kv4", dict(K=K_INF, kv_pages=4)), ("K1_kv4_reprefill", dict(K=1, kv_pages=4, resume=RESUME_REPREFILL))]
+
+
+@pytest.mark.parametrize("name,over", PREEMPT_CASES, ids=[c[0] for c in PREEMPT_CASES])
+def test_preemption_bit_exact(name, over):
+    """KV exhaustion (reading R25): page growth preempts the latest-admitted slot;
+    tokens kept (K != 0) or dropped (K = 0).  Lengths up to 128 so slots cross
+    64-token page boundaries while the pool is full (each case preempts 8-19 times)."""
+    from workload.lengths import LengthModel
+    cfg = SchedConfig(Q_g=8, U=2, pool_prompts=16, G=1, cap=128, kv_dtype=KV_BF16, **over)
+    off, toks, L = tiny_workload(n_prompts=16, cap=128, lm=LengthModel(median=40, sigma=0.6, tail=0.3, floor=1, cap=128))
+    eng = make_engine(TINY, cfg, max_traj=64, max_prompt=16)
+    res = run_engine(eng, TINY, off, toks, L)
+    eng.close()
+    c, og = _oracle(cfg, off, toks, L)
+    assert sum(1 for e in c.events if e[0] == "PREEMPT") > 0
     _compare_schedule(res, c, og)
 
 

@@ -137,6 +137,20 @@ def test_replicas_schedule_bit_exact(name, over):
     _compare(outs[0], c, og)
 
 
+@pytest.mark.parametrize("K", [1, 0], ids=["K1", "K0"])
+def test_replicas_preemption_bit_exact(K):
+    """Per-replica KV exhaustion: every rank tracks every replica's free-page count
+    and runs the same victim choice; only the owner moves its page ids."""
+    from workload.lengths import LengthModel
+    cfg = SchedConfig(R=2, Q_g=4, U=2, K=K, pool_prompts=16, cap=128, kv_pages=4, kv_dtype=KV_BF16)
+    off, toks, L = tiny_workload(n_prompts=16, cap=128, lm=LengthModel(median=40, sigma=0.6, tail=0.3, floor=1, cap=128))
+    outs = _run_replicas(cfg, off, toks, L)
+    _same_across_ranks(outs)
+    c, og = _oracle(cfg, off, toks, L)
+    assert sum(1 for e in c.events if e[0] == "PREEMPT") > 0
+    _compare(outs[0], c, og)
+
+
 def test_replicas_qtot_above_one_ctl_block():
     """Q_tot = 2 x 600 slots > the controller CTA's 1024 threads: chunked scans."""
     cfg = SchedConfig(R=2, Q_g=600, U=64, K=K_INF, pool_prompts=1300, cap=8, kv_pages=700, kv_dtype=KV_BF16)

@@ -16,7 +16,7 @@ import pytest
 
 from oracle.metrics import bubble_ratio
 from oracle.sched import DONE, GROUP_READY, Controller, SchedError
-from workload.configs import (BARRIER_ADMITTED, BARRIER_TRAINED, K_INF, MODE_SORTED, MODE_SYNC,
+from workload.configs import (BARRIER_ADMITTED, BARRIER_TRAINED, K_INF, MODE_POSTHOC, MODE_SORTED, MODE_SYNC,
                               RESUME_KEEP_KV, RESUME_REPREFILL, SchedConfig)
 from workload.lengths import LengthModel, sample_lengths
 
@@ -138,6 +138,43 @@ def test_closed_form_on_policy_mode_p3(seed):
             assert set(r["vers"]) == {j} and r["v_first"] == j
 
 
+@pytest.mark.parametrize("seed", range(30))
+def test_posthoc_sorting_definition(seed):
+    """P:349 post-hoc sorting: each loaded pool is generated to completion (with
+    refill when Q < pool) before anything is emitted; then its trajectories go out
+    as the U-slices of sort(len, traj_id), one per policy version -- group j of a
+    pool is j versions stale, and every token of the pool is from the version it
+    started under.  With Q >= pool each pool takes exactly max(len) steps."""
+    rng = random.Random(3000 + seed)
+    P = rng.randint(1, 12)
+    n_pools = rng.randint(1, 3)
+    N = P * n_pools
+    U = rng.randint(1, P)
+    Q = rng.randint(max(1, P // 2), P + 3)
+    L = [rng.randint(1, 15) for _ in range(N)]
+    c, groups = run(L, Q_g=Q, U=U, pool_prompts=P, cap=15, K=K_INF, mode=MODE_POSTHOC)
+    want, v = [], 0
+    for e in range(n_pools):
+        ids = sorted(range(e * P, (e + 1) * P), key=lambda t: (L[t], t))
+        want += [ids[i:i + U] for i in range(0, P, U)]
+    assert [[r["traj_id"] for r in g] for g in groups] == want
+    ev = c.events
+    for e in range(n_pools):                     # no emission of a pool before its last finish
+        pool = set(range(e * P, (e + 1) * P))
+        last_fin = max(i for i, x in enumerate(ev) if x[0] == "FINISH" and x[3] in pool)
+        first_emit = min(i for i, x in enumerate(ev) if x[0] == "EMIT" and set(x[3]) <= pool)
+        assert first_emit > last_fin
+    v = 0
+    for e in range(n_pools):
+        ng = (P + U - 1) // U
+        for j in range(ng):
+            for r in groups[v + j]:
+                assert set(r["vers"]) == {v} and r["v_first"] == v      # generated before any update
+        v += ng
+    if Q >= P:
+        assert len(c.trace) == sum(max(L[e * P:(e + 1) * P]) for e in range(n_pools))
+
+
 @pytest.mark.parametrize("seed", range(20))
 def test_sync_closed_form(seed):
     """SYNC: B = 1 - sum L / (Q * sum_batches max L) with batches of Q in traj order."""
@@ -212,7 +249,7 @@ def _random_cfg(rng):
                 page_tokens=rng.choice([2, 4, 64]), kv_pages=rng.choice([4, 8, 16, 1 << 20]),
                 resume=rng.choice([RESUME_KEEP_KV, RESUME_REPREFILL]),
                 barrier=rng.choice([BARRIER_TRAINED, BARRIER_ADMITTED]),
-                mode=rng.choice([MODE_SORTED, MODE_SORTED, MODE_SYNC]))
+                mode=rng.choice([MODE_SORTED, MODE_SORTED, MODE_SYNC, MODE_POSTHOC]))
 
 
 @pytest.mark.parametrize("seed", range(500))
@@ -224,7 +261,7 @@ def test_invariants_random_runs(seed):
     N = n_prompts * cfg.G
     L = [rng.randint(1, cfg.cap) for _ in range(N)]
     plen = [rng.randint(1, 6) for _ in range(n_prompts)]
-    if cfg.mode == MODE_SORTED and cfg.U > cfg.pool_prompts * cfg.G:
+    if cfg.mode in (MODE_SORTED, MODE_POSTHOC) and cfg.U > cfg.pool_prompts * cfg.G:
         with pytest.raises(SchedError):
             Controller(cfg)
         return
@@ -251,7 +288,7 @@ def test_invariants_random_runs(seed):
     emitted = [r["traj_id"] for recs, _, _ in groups_v for r in recs]
     assert sorted(emitted) == list(range(N))                      # each exactly once
     for recs, v_emit, final in groups_v:
-        if cfg.mode == MODE_SORTED:
+        if cfg.mode in (MODE_SORTED, MODE_POSTHOC):
             keys = [(r["len"], r["traj_id"]) for r in recs]
             assert keys == sorted(keys)                           # sorted within group
             assert len(recs) == cfg.U or final                    # batch exactness
@@ -276,7 +313,7 @@ def test_invariants_random_runs(seed):
         for r in recs:
             assert r["lifecycle"] == inter.get(r["traj_id"], 0)
     # TRAINED barrier: no admission of epoch e+1 before epoch e fully emitted
-    if cfg.barrier == BARRIER_TRAINED or cfg.mode == MODE_SYNC:
+    if cfg.barrier == BARRIER_TRAINED or cfg.mode in (MODE_SYNC, MODE_POSTHOC):
         loads = [e for e in c.events if e[0] == "LOAD"]
         emit_idx = {}
         for i, e in enumerate(c.events):

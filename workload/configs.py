@@ -49,7 +49,7 @@ def model_by_name(name: str) -> ModelShape:
 
 
 # Scheduler enums (values match include/srl.h)
-MODE_SORTED, MODE_SYNC = 0, 1
+MODE_SORTED, MODE_SYNC, MODE_POSTHOC = 0, 1, 2
 RESUME_KEEP_KV, RESUME_REPREFILL = 0, 1
 BARRIER_TRAINED, BARRIER_ADMITTED = 0, 1
 STOP_FORCED, STOP_EOS = 0, 1
