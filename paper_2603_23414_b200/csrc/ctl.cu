@@ -436,30 +436,44 @@ __global__ void __launch_bounds__(kCtlThreads, 1) ctl_begin_kernel(Ctl c) {
     }
     return;
   }
-  // decode rows for the local slots
+  // decode rows: this rank's running slots compacted in ascending slot order (row i
+  // -> slot row_slot[i]), so the decode forward runs over the first r_local rows only
+  // (the host picks a graph whose M covers them); rows past them are inactive
   long long my_ctx = 0;
   int my_rows = 0;
-  for (int sl = threadIdx.x; sl < c.Q_g; sl += blockDim.x) {
-    const int g = sl * c.R + c.rank;
-    const int tid = c.slot_traj[g];
+  __shared__ int sh_rbase;
+  if (threadIdx.x == 0) sh_rbase = 0;
+  __syncthreads();
+  for (int base = 0; base < c.Q_g; base += blockDim.x) {
+    const int sl = base + threadIdx.x;
+    const int tid = sl < c.Q_g ? c.slot_traj[sl * c.R + c.rank] : -1;
+    int tot;
+    const int rank_in = block_scan(tid >= 0 ? 1 : 0, &tot);
     if (tid >= 0) {
+      const int i = sh_rbase + rank_in;
       const DevTraj& t = c.traj[tid];
       const int n = t.n_tok;
-      c.row_tok[sl] = n > 0 ? c.tokens[(size_t)tid * c.cap + n - 1]
-                            : c.prompt_tok[c.prompt_off[t.prompt_idx] + t.prompt_len - 1];
-      c.row_pos[sl] = t.prompt_len + n - 1;
+      c.row_tok[i] = n > 0 ? c.tokens[(size_t)tid * c.cap + n - 1]
+                           : c.prompt_tok[c.prompt_off[t.prompt_idx] + t.prompt_len - 1];
+      c.row_pos[i] = t.prompt_len + n - 1;
       my_ctx += t.prompt_len + n;
       my_rows++;
-      c.row_n[sl] = n;
-      c.row_traj[sl] = tid;
-      c.row_restarts[sl] = t.restarts;
-    } else {
-      c.row_tok[sl] = 0;
-      c.row_pos[sl] = -1;
-      c.row_n[sl] = 0;
-      c.row_traj[sl] = -1;
-      c.row_restarts[sl] = 0;
+      c.row_n[i] = n;
+      c.row_traj[i] = tid;
+      c.row_restarts[i] = t.restarts;
+      c.row_slot[i] = sl;
     }
+    __syncthreads();
+    if (threadIdx.x == 0) sh_rbase += tot;
+    __syncthreads();
+  }
+  for (int i = sh_rbase + threadIdx.x; i < c.Q_g; i += blockDim.x) {
+    c.row_tok[i] = 0;
+    c.row_pos[i] = -1;
+    c.row_n[i] = 0;
+    c.row_traj[i] = -1;
+    c.row_restarts[i] = 0;
+    c.row_slot[i] = -1;
   }
   // prefill rows of local admissions still running (prompt ++ kept[:-1])
   __shared__ int sh_off;

@@ -5,6 +5,7 @@
 // of host-side counters.
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <string>
 #include <unordered_set>
 #include <vector>
@@ -223,7 +224,6 @@ struct srl_engine {
   void* qbuf = nullptr;
   float* logits = nullptr;
   float *rope_cos = nullptr, *rope_sin = nullptr;
-  int* row_slot_id = nullptr;  // identity rows 0..Q_g-1
   void* gemm_ws = nullptr;     // GEMM stream-K workspace (zeroed at create, left zeroed by every launch)
   size_t gemm_ws_bytes = 0;
   AttnArgs attn{};
@@ -250,14 +250,22 @@ struct srl_engine {
   uint32_t prof_mask = 0xffffffffu;  // classes bracketed while profiling
   uint32_t graph_mask = 0;           // classes bracketed inside the captured graph
   bool capturing = false;
-  EvSet direct, gset;
+  EvSet direct;
+  EvSet* gset = nullptr;  // event set of the graph being captured / replayed
   double prof_ms[SRL_K_NCLASS] = {0};
   long long prof_launch[SRL_K_NCLASS] = {0};
   // CUDA graph of the static decode tail (forward + sampler + ctl_end)
   bool use_graph = true;
-  int direct_steps = 0;
-  cudaGraphExec_t gexec = nullptr;
-  long long g_launches = 0;
+  // one graph per decode-row bucket M (rows = the running slots, compacted):
+  // at low occupancy (epoch drains) the GEMMs stream the weights for M rows, not Q_g
+  struct Graph {
+    cudaGraphExec_t exec = nullptr;
+    long long launches = 0;
+    int direct = 0;  // direct runs of this bucket (the first step of a bucket runs uncaptured)
+    EvSet gset;
+  };
+  std::map<int, Graph> graphs;
+  int last_m = 0;  // decode rows of the last step
 };
 
 namespace {
@@ -274,7 +282,7 @@ struct Prof {
     // Only profiled classes get event records: an event node between two kernels
     // of the captured graph replaces their programmatic (PDL) edge by a full one.
     if (!e->prof || !((e->prof_mask >> cls) & 1u)) return;
-    S = e->capturing ? &e->gset : &e->direct;
+    S = e->capturing ? e->gset : &e->direct;
     if (S->used + 2 > S->ev.size()) {
       for (int i = 0; i < 256; ++i) {
         cudaEvent_t ev;
@@ -358,6 +366,7 @@ void plan_scratch(srl_engine* e, ScratchPlan& p, bool assign) {
   c.row_n = (int*)P(4 * z.Q_g);
   c.row_traj = (int*)P(4 * z.Q_g);
   c.row_restarts = (int*)P(4 * z.Q_g);
+  c.row_slot = (int*)P(4 * z.Q_g);
   c.pre_tok = (int*)P(4ull * z.prefill_rows_max);
   c.pre_pos = (int*)P(4ull * z.prefill_rows_max);
   c.pre_slot = (int*)P(4ull * z.prefill_rows_max);
@@ -367,7 +376,6 @@ void plan_scratch(srl_engine* e, ScratchPlan& p, bool assign) {
   c.h_lp = (float*)P(4ull * z.h_cap_tok);
   c.h_ver = (int*)P(4ull * z.h_cap_tok);
   c.h_rec = (srl_traj*)P(sizeof(srl_traj) * kMaxGroup);
-  e->row_slot_id = (int*)P(4 * z.Q_g);
   e->gemm_ws_bytes = gemm_workspace_bytes(kMaxSmsPlan);
   e->gemm_ws = P(e->gemm_ws_bytes);
   e->x_res = (float*)P(4ull * z.mmax * m.d);
@@ -509,15 +517,29 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
   }
 }
 
+// Decode-row bucket for r running local rows: the GEMM batch M.  Fine steps where
+// the weight stream dominates (few rows), coarser ones near full occupancy;
+// always a multiple of 16 (the UMMA N granularity) up to Q_g.
+int decode_rows(const srl_engine* e, int r) {
+  const int Q = e->s.Q_g;
+  int m;
+  if (r <= 64) m = (r + 15) / 16 * 16;
+  else if (r <= 256) m = (r + 31) / 32 * 32;
+  else m = (r + 63) / 64 * 64;
+  if (m < 16) m = 16;
+  return m < Q ? m : Q;
+}
+
 // decode forward over the local slots, sampler and (alone) controller END --
 // static shapes.  With a replica exchange the END runs after the all-gather.
-void decode_tail(srl_engine* e, bool with_end) {
+void decode_tail(srl_engine* e, bool with_end, int M) {
   const Ctl& c = e->ctl;
   cudaStream_t st = e->st;
-  forward(e, e->s.Q_g, c.row_tok, c.row_pos, e->row_slot_id, true);
+  forward(e, M, c.row_tok, c.row_pos, c.row_slot, true);
   SampleArgs sa{};
   sa.logits = e->logits;
-  sa.M = e->s.Q_g;
+  sa.M = M;
+  sa.row_slot = c.row_slot;
   sa.V = e->m.V;
   sa.row_pos = c.row_pos;
   sa.row_n = c.row_n;
@@ -718,9 +740,6 @@ int32_t srl_create(const srl_model_cfg* m, const srl_sched_cfg* s, int32_t devic
   // init device state
   cudaMemsetAsync(e->KV, 0, mem->kv_bytes, e->st);  // finite values in never-written KV rows
   cudaMemsetAsync(e->gemm_ws, 0, e->gemm_ws_bytes, e->st);
-  std::vector<int> ident(s->Q_g);
-  for (int i = 0; i < s->Q_g; ++i) ident[i] = i;
-  cudaMemcpyAsync(e->row_slot_id, ident.data(), 4 * s->Q_g, cudaMemcpyHostToDevice, e->st);
   int zero = 0;
   cudaMemcpyAsync(c.prompt_off, &zero, 4, cudaMemcpyHostToDevice, e->st);
   ctl_init(c, s->K, e->st);
@@ -745,8 +764,10 @@ int32_t srl_destroy(srl_engine* e) {
   if (e->ev0) cudaEventDestroy(e->ev0);
   if (e->ev1) cudaEventDestroy(e->ev1);
   for (cudaEvent_t ev : e->direct.ev) cudaEventDestroy(ev);
-  for (cudaEvent_t ev : e->gset.ev) cudaEventDestroy(ev);
-  if (e->gexec) cudaGraphExecDestroy(e->gexec);
+  for (auto& kv : e->graphs) {
+    for (cudaEvent_t ev : kv.second.gset.ev) cudaEventDestroy(ev);
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  }
   delete e->comm;
   delete e;
   return SRL_OK;
@@ -845,38 +866,43 @@ int32_t srl_decode_step(srl_engine* e, srl_step_info* info) {
     Prof p(e, SRL_K_PREFILL, 2 + 8 * e->m.L);
     forward(e, mc, c.pre_tok + r0, c.pre_pos + r0, c.pre_slot + r0, false);
   }
-  // decode of every local slot + sampling + stop/compaction/emission: a static
-  // launch sequence, replayed from a CUDA graph after the first step.
-  if (e->use_graph && e->direct_steps >= 1 && !e->gexec) {
+  // decode of the running local slots (compacted rows) + sampling + stop /
+  // compaction / emission: a static launch sequence per row bucket, replayed from
+  // a CUDA graph from the bucket's second step on
+  const int M = decode_rows(e, b.r_local);
+  e->last_m = M;
+  srl_engine::Graph& G = e->graphs[M];
+  e->gset = &G.gset;
+  if (e->use_graph && G.direct >= 1 && !G.exec) {
     const long long l0 = e->launches;
     e->graph_mask = e->prof ? e->prof_mask : 0u;
     cudaGraph_t g = nullptr;
     e->capturing = true;
     bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
     if (ok) {
-      decode_tail(e, e->comm == nullptr);
+      decode_tail(e, e->comm == nullptr, M);
       ok = cudaStreamEndCapture(st, &g) == cudaSuccess && g;
     }
     e->capturing = false;
-    if (ok) ok = cudaGraphInstantiate(&e->gexec, g, 0) == cudaSuccess;
+    if (ok) ok = cudaGraphInstantiate(&G.exec, g, 0) == cudaSuccess;
     if (g) cudaGraphDestroy(g);
     cudaGetLastError();
-    e->g_launches = e->launches - l0;
+    G.launches = e->launches - l0;
     e->launches = l0;
     if (!ok) {  // fall back to direct launches for good
-      e->gexec = nullptr;
+      G.exec = nullptr;
       e->use_graph = false;
-      e->gset.cls.clear();
-      e->gset.nl.clear();
-      e->gset.used = 0;
+      G.gset.cls.clear();
+      G.gset.nl.clear();
+      G.gset.used = 0;
     }
   }
-  if (e->gexec) {
-    cudaGraphLaunch(e->gexec, st);
-    e->launches += e->g_launches;
+  if (G.exec) {
+    cudaGraphLaunch(G.exec, st);
+    e->launches += G.launches;
   } else {
-    decode_tail(e, e->comm == nullptr);
-    e->direct_steps++;
+    decode_tail(e, e->comm == nullptr, M);
+    G.direct++;
   }
   if (e->comm)
     if (int rc = exchange_and_end(e)) return rc;
@@ -884,7 +910,7 @@ int32_t srl_decode_step(srl_engine* e, srl_step_info* info) {
   read_status(e);
   if (cudaError_t ce = cudaGetLastError()) return cuda_fail("decode step", ce);
   prof_collect(e, e->direct, false);
-  if (e->gexec) prof_collect(e, e->gset, true);
+  if (G.exec) prof_collect(e, G.gset, true);
   const CtlStatus& en = *e->hst;
   if (info) {
     info->k = en.k - 1;
@@ -1036,14 +1062,17 @@ static void drop_graph_if_stale(srl_engine* e) {
   // the captured decode graph carries the event nodes of the classes profiled at
   // capture time: recapture when that set changes
   const uint32_t want = e->prof ? e->prof_mask : 0u;
-  if (e->gexec && want != e->graph_mask) {
-    cudaStreamSynchronize(e->st);
-    cudaGraphExecDestroy(e->gexec);
-    e->gexec = nullptr;
-    e->gset.cls.clear();
-    e->gset.nl.clear();
-    e->gset.used = 0;
+  if (want == e->graph_mask) return;
+  cudaStreamSynchronize(e->st);
+  for (auto& kv : e->graphs) {
+    srl_engine::Graph& G = kv.second;
+    if (G.exec) cudaGraphExecDestroy(G.exec);
+    G.exec = nullptr;
+    G.gset.cls.clear();
+    G.gset.nl.clear();
+    G.gset.used = 0;
   }
+  e->graph_mask = want;
 }
 
 int32_t srl_set_profile_mask(srl_engine* e, uint32_t class_mask) {
@@ -1092,7 +1121,14 @@ extern "C" int32_t srl_debug_copy_logits(srl_engine* e, float* out_host, int64_t
   if (!e || !out_host) return fail(SRL_E_INVALID_ARG, "srl_debug_copy_logits: bad arguments");
   const long long n = (long long)e->s.Q_g * e->m.V;
   if (cap_floats < n) return fail(SRL_E_CAPACITY, "srl_debug_copy_logits: buffer too small");
-  cudaMemcpyAsync(out_host, e->logits, 4 * n, cudaMemcpyDeviceToHost, e->st);
+  // decode rows are compacted running slots: put row i back at its slot
+  std::vector<int> rs(e->s.Q_g);
+  cudaMemcpyAsync(rs.data(), e->ctl.row_slot, 4 * e->s.Q_g, cudaMemcpyDeviceToHost, e->st);
+  if (cudaStreamSynchronize(e->st) != cudaSuccess) return cuda_fail("srl_debug_copy_logits");
+  for (int i = 0; i < e->last_m && i < e->s.Q_g; ++i)
+    if (rs[i] >= 0)
+      cudaMemcpyAsync(out_host + (size_t)rs[i] * e->m.V, e->logits + (size_t)i * e->m.V, 4ull * e->m.V,
+                      cudaMemcpyDeviceToHost, e->st);
   if (cudaStreamSynchronize(e->st) != cudaSuccess) return cuda_fail("srl_debug_copy_logits");
   return SRL_OK;
 }

@@ -88,6 +88,8 @@ struct Ctl {
   int* row_n;          // [Q_g]  generated index of the token being sampled
   int* row_traj;       // [Q_g]
   int* row_restarts;   // [Q_g]
+  int* row_slot;       // [Q_g]  local slot of decode row i (-1: inactive row); rows are the running
+                       //        local slots compacted in ascending slot order (BEGIN)
   int* pre_tok;        // [prefill_rows_max]
   int* pre_pos;
   int* pre_slot;       // local slot of the prefill row

@@ -55,6 +55,7 @@ struct SampleArgs {
   const int* row_n;      // [M] generated-token index
   const int* row_traj;   // [M]
   const int* row_restarts;
+  const int* row_slot;   // [M] output index of row m (null: m itself; < 0: inactive, nothing written)
   float invT;
   uint64_t seed;
   int* tok_out;          // [M]

@@ -106,10 +106,11 @@ __global__ void __launch_bounds__(kSampThreads) sample_kernel(SampleArgs a) {
   pdl_trigger();
   pdl_wait();
   const int m = blockIdx.x;
-  if (a.row_pos[m] < 0) {
-    if (threadIdx.x == 0) {
-      a.tok_out[m] = -1;
-      a.lp_out[m] = 0.f;
+  const int om = a.row_slot ? a.row_slot[m] : m;  // where this row's sample goes
+  if (a.row_pos[m] < 0 || om < 0) {
+    if (threadIdx.x == 0 && om >= 0) {
+      a.tok_out[om] = -1;
+      a.lp_out[om] = 0.f;
     }
     return;
   }
@@ -183,8 +184,8 @@ __global__ void __launch_bounds__(kSampThreads) sample_kernel(SampleArgs a) {
       sum = (mx == -INFINITY ? 0.f : sum * expf(mx - nm)) + (r_mx[i] == -INFINITY ? 0.f : r_sum[i] * expf(r_mx[i] - nm));
       mx = nm;
     }
-    a.tok_out[m] = bj;
-    a.lp_out[m] = __fmul_rn(z[bj], invT) - (mx + logf(sum));
+    a.tok_out[om] = bj;
+    a.lp_out[om] = __fmul_rn(z[bj], invT) - (mx + logf(sum));
   }
 }
 

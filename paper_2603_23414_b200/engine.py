@@ -203,7 +203,7 @@ class RolloutEngine:
         return {k: (ms[i], nl[i]) for i, k in enumerate(_lib.KERNEL_CLASSES)}
 
     def debug_logits(self) -> np.ndarray:
-        out = np.empty((self.Q_g, self.V), dtype=np.float32)
+        out = np.full((self.Q_g, self.V), np.nan, dtype=np.float32)   # rows of idle slots stay NaN
         check(self.lib.srl_debug_copy_logits(self.h, _i32p(out), out.size), "srl_debug_copy_logits")
         return out
 
