@@ -109,6 +109,30 @@ def test_preemption_bit_exact(name, over):
     _compare_schedule(res, c, og)
 
 
+EDGE_CASES = [
+    # (name, sched overrides, n_prompts, prompt length range, cap)
+    ("one_slot_U1", dict(Q_g=1, U=1, pool_prompts=3), 3, (1, 1), 8),          # one-token prompts, serial decode
+    ("cap1", dict(Q_g=4, U=2, pool_prompts=6), 6, (4, 16), 1),                 # every trajectory is one token
+    ("U_eq_pool", dict(Q_g=4, U=6, pool_prompts=6), 6, (2, 9), 16),            # one group per epoch
+    ("max_prompt", dict(Q_g=3, U=2, pool_prompts=4), 4, (16, 16), 24),         # prompts at max_prompt
+    ("Q_gt_pool", dict(Q_g=32, U=3, pool_prompts=5), 10, (3, 12), 32),         # more slots than trajectories
+]
+
+
+@pytest.mark.parametrize("name,over,n,plen,cap", EDGE_CASES, ids=[c[0] for c in EDGE_CASES])
+def test_edge_cases_bit_exact(name, over, n, plen, cap):
+    from workload.lengths import LengthModel
+    cfg = SchedConfig(K=K_INF, G=1, cap=cap, kv_pages=256, kv_dtype=KV_BF16, **over)
+    off, toks, L = tiny_workload(n_prompts=n, cap=cap, plen=plen,
+                                 lm=LengthModel(median=max(1, cap // 3), sigma=0.8, tail=0.2, floor=1, cap=cap))
+    eng = make_engine(TINY, cfg, max_traj=64, max_prompt=16)
+    res = run_engine(eng, TINY, off, toks, L)
+    eng.close()
+    c, og = _oracle(cfg, off, toks, L)
+    _compare_schedule(res, c, og)
+    assert sum(len(h.records) for h, _ in res["groups"]) == n
+
+
 def test_two_epochs_and_counters():
     cfg = SchedConfig(Q_g=8, U=4, K=K_INF, pool_prompts=8, cap=64, kv_pages=128, kv_dtype=KV_BF16)
     off, toks, L = tiny_workload(n_prompts=24)
@@ -127,6 +151,8 @@ def test_api_state_errors():
     cfg = SchedConfig(Q_g=4, U=2, pool_prompts=4, cap=8, kv_pages=32)
     off, toks, L = tiny_workload(n_prompts=4, cap=8)
     eng = make_engine(TINY, cfg, max_traj=16, max_prompt=16)
+    with pytest.raises(SRLError, match="nothing submitted"):
+        eng.decode_step()                                          # empty stream
     with pytest.raises(SRLError):
         eng.submit_prompts([1, 1], off[:3], toks, L[:2])          # duplicate id
     with pytest.raises(SRLError):
