@@ -26,6 +26,7 @@ host memory each round and groups copied back, wall-clock.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import sys
@@ -37,7 +38,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from workload.configs import (BARRIER_TRAINED, K_INF, KV_BF16, LLAMA8B, MODE_SORTED, QWEN32B, RESUME_KEEP_KV,  # noqa: E402
+from workload.configs import (BARRIER_ADMITTED, BARRIER_TRAINED, K_INF, KV_BF16, LLAMA8B, MODE_POSTHOC,  # noqa: E402
+                              MODE_SORTED, MODE_SYNC, QWEN32B, RESUME_KEEP_KV,
                               STOP_FORCED, SchedConfig)
 from workload.lengths import LengthModel, sample_lengths  # noqa: E402
 from workload.prompts import make_prompts  # noqa: E402
@@ -164,6 +166,10 @@ def run_gpu(args, rank, world, dist):
     from paper_2603_23414_b200.engine import share_nccl_unique_id
     model, Q_g, cap, kv_pages, pool, compact, keep_trainer, _ = MODELS[args.model]
     sched = cfg2_sched(world, Q_g=Q_g, cap=cap, pool=pool, kv_pages=kv_pages)
+    # scheduler variants (the paper's comparisons; defaults = SortedRL partial mode)
+    sched = dataclasses.replace(sched, mode={"sorted": MODE_SORTED, "sync": MODE_SYNC, "posthoc": MODE_POSTHOC}[args.mode],
+                                K=args.K, U=args.U,
+                                barrier={"trained": BARRIER_TRAINED, "admitted": BARRIER_ADMITTED}[args.barrier])
     off, toks, L = workload_inputs(world, epochs=EPOCHS, pool=pool, V=model.V, cap=cap)
     ids = np.arange(len(off) - 1, dtype=np.uint64) + 1
     n_prompts = len(ids)
@@ -395,6 +401,13 @@ def main():
     ap.add_argument("--model", default="llama8b", choices=sorted(MODELS),
                     help="llama8b = BASELINE configs[1] (default); qwen32b = the per-GPU slice of configs[3]")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="sorted", choices=["sorted", "sync", "posthoc"],
+                    help="scheduler: SortedRL (default), the synchronous baseline, post-hoc sorting (P:349)")
+    ap.add_argument("--K", type=int, default=K_INF, help="cache bound in policy versions (-1 = inf, 0 = on-policy)")
+    ap.add_argument("--U", type=int, default=64, help="update group size")
+    ap.add_argument("--barrier", default="trained", choices=["trained", "admitted"], help="cache-aware loading barrier")
+    ap.add_argument("--trace-out", default=None, help="write every decode step's (r_k, sum_ctx, dt_ms, prefill "
+                    "tokens, finished, r_local) as .npy")
     ap.add_argument("--full", action="store_true",
                     help="time the whole 2-epoch rollout (every round, incl. epoch starts and drains) instead")
     ap.add_argument("--no-cpu", action="store_true")
@@ -412,6 +425,8 @@ def main():
         td.init_process_group("nccl")
         dist = td
     r = run_gpu(args, rank, world, dist)
+    if args.trace_out and rank == 0:
+        np.save(args.trace_out, np.array(r["trace"], dtype=np.float64))
     m = MODELS[args.model][0]
     hbm, tf_burst, tf_sust, peak_src = load_peaks()
     # per-rank aggregates over the timed rounds
@@ -471,6 +486,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms / max(1, steps), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": MODELS[args.model][7] or WORKLOAD,
+                   "scheduler": {"mode": args.mode, "K": args.K, "U": args.U, "barrier": args.barrier},
                    "step": "one early-update round: decode steps (refill, prefill, decode GEMMs, paged attention, "
                            "Philox sampling, stop detection, compaction) until the length-sorted update group of "
                            "U=64 is ready, its harvest, and the policy refresh (load_policy_weights, K bound)",
