@@ -185,10 +185,10 @@ Sizes compute_sizes(const srl_model_cfg* m, const srl_sched_cfg* s, int world) {
   z.max_pages = (z.max_ctx + kPage - 1) / kPage;
   z.max_prompts = (s->max_traj + s->G - 1) / s->G + 1;
   z.prefill_rows_max = s->Q_g * (z.max_ctx);
-  z.mmax = s->Q_g > s->prefill_chunk ? s->Q_g : s->prefill_chunk;
+  z.mmax = s->Q_g + s->prefill_chunk;  // a mixed pass: Q_g decode rows + up to prefill_chunk prompt rows
   z.G = m->Hq / m->Hkv;
   const int a1 = attn_max_items(s->Q_g, m->Hkv, z.max_ctx);
-  const int a2 = s->prefill_chunk * m->Hkv;
+  const int a2 = (s->Q_g + s->prefill_chunk) * m->Hkv;  // mixed / prefill passes never split the KV
   z.max_items = a1 > a2 ? a1 : a2;
   z.ev_cap = 1LL << 20;
   const int gmax = s->max_traj < kMaxGroup ? s->max_traj : kMaxGroup;
@@ -361,15 +361,17 @@ void plan_scratch(srl_engine* e, ScratchPlan& p, bool assign) {
   c.prompt_off = (int*)P(4ull * (z.max_prompts + 1));
   c.prompt_tok = (int*)P(4ull * z.max_prompts * s.max_prompt);
   c.events = (int*)P(24ull * z.ev_cap);
-  c.row_tok = (int*)P(4 * z.Q_g);
-  c.row_pos = (int*)P(4 * z.Q_g);
+  // decode rows [0, Q_g) and prefill rows [Q_g, ...) are one array each, so one
+  // forward can run both (the mixed pass of a step with admissions)
+  c.row_tok = (int*)P(4ull * (z.Q_g + z.prefill_rows_max));
+  c.row_pos = (int*)P(4ull * (z.Q_g + z.prefill_rows_max));
   c.row_n = (int*)P(4 * z.Q_g);
   c.row_traj = (int*)P(4 * z.Q_g);
   c.row_restarts = (int*)P(4 * z.Q_g);
-  c.row_slot = (int*)P(4 * z.Q_g);
-  c.pre_tok = (int*)P(4ull * z.prefill_rows_max);
-  c.pre_pos = (int*)P(4ull * z.prefill_rows_max);
-  c.pre_slot = (int*)P(4ull * z.prefill_rows_max);
+  c.row_slot = (int*)P(4ull * (z.Q_g + z.prefill_rows_max));
+  c.pre_tok = c.row_tok + z.Q_g;
+  c.pre_pos = c.row_pos + z.Q_g;
+  c.pre_slot = c.row_slot + z.Q_g;
   c.admit_local = (int*)P(4 * z.Q_g);
   c.samp = (int*)P(8 * z.Q_tot);
   c.h_tok = (int*)P(4ull * z.h_cap_tok);
@@ -424,7 +426,10 @@ void run_gemm(srl_engine* e, int cls, const __nv_bfloat16* X, int M, const __nv_
 }
 
 // One forward pass over M rows (decode: rows = local slots; prefill: rows = prompt tokens).
-void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const int* row_slot, bool decode) {
+// m_lm: rows that get logits (the decode rows, first in the batch); -1 = M.
+// split: allow split-KV attention (decode passes; never with prompt rows).
+void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const int* row_slot, bool decode,
+             int m_lm = -1, int split = -1) {
   const srl_model_cfg& m = e->m;
   cudaStream_t st = e->st;
   const int d = m.d, qd = m.Hq * m.dh;
@@ -445,7 +450,7 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
   const int D = decode ? 0 : -1000;  // profiling class offset (prefill is timed as a whole)
   {
     Prof p1(e, D + SRL_K_ATTN);
-    attn_plan(a, decode ? 1 : 0, st);
+    attn_plan(a, split >= 0 ? split : (decode ? 1 : 0), st);
   }
   if (!debug_skip(D + SRL_K_ELEMWISE)) {
     Prof p2(e, D + SRL_K_ELEMWISE);
@@ -513,7 +518,7 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
     fe.ldo = m.V;
     fe.w_packed = 1;
     fe.ws = e->gemm_ws;
-    run_gemm(e, SRL_K_LM_HEAD, e->xn, M, (const __nv_bfloat16*)e->plm_head, m.V, d, fe);
+    run_gemm(e, SRL_K_LM_HEAD, e->xn, m_lm >= 0 ? m_lm : M, (const __nv_bfloat16*)e->plm_head, m.V, d, fe);
   }
 }
 
@@ -532,10 +537,17 @@ int decode_rows(const srl_engine* e, int r) {
 
 // decode forward over the local slots, sampler and (alone) controller END --
 // static shapes.  With a replica exchange the END runs after the all-gather.
-void decode_tail(srl_engine* e, bool with_end, int M) {
+// M_pre > 0: the mixed pass of a step with admissions -- the decode rows [0, M) are
+// followed (from row Q_g) by the admitted prompts' rows, all in one forward, so
+// the prompts ride on the step's weight stream instead of a pass of their own
+// (chunked prefill); logits and sampling cover the decode rows only.
+void decode_tail(srl_engine* e, bool with_end, int M, int M_pre = 0) {
   const Ctl& c = e->ctl;
   cudaStream_t st = e->st;
-  forward(e, M, c.row_tok, c.row_pos, c.row_slot, true);
+  if (M_pre > 0)
+    forward(e, e->s.Q_g + M_pre, c.row_tok, c.row_pos, c.row_slot, true, M, 0);
+  else
+    forward(e, M, c.row_tok, c.row_pos, c.row_slot, true);
   SampleArgs sa{};
   sa.logits = e->logits;
   sa.M = M;
@@ -587,6 +599,34 @@ void read_status(srl_engine* e) {
 }  // namespace
 
 // ================================================================== C ABI
+
+// end of a decode step: status read-back, profiling, step info
+static int32_t finish_step(srl_engine* e, const CtlStatus& b, srl_step_info* info, srl_engine::EvSet* gset) {
+  cudaStream_t st = e->st;
+  cudaEventRecord(e->ev1, st);
+  read_status(e);
+  if (cudaError_t ce = cudaGetLastError()) return cuda_fail("decode step", ce);
+  prof_collect(e, e->direct, false);
+  if (gset) prof_collect(e, *gset, true);
+  const CtlStatus& en = *e->hst;
+  if (info) {
+    info->k = en.k - 1;
+    info->r_k = en.r_k;
+    info->n_finished = en.n_fin;
+    info->n_ready = en.n_ready;
+    info->n_admitted = b.n_admit;
+    info->n_prefill_tokens = b.m_pre;
+    info->sum_ctx = b.sum_ctx;
+    info->r_local = b.r_local;
+    info->v = en.v;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e->ev0, e->ev1);
+    info->dt_ms = ms;
+  }
+  if (en.status == SRL_GROUP_READY) e->group_state = 1;
+  return en.status;
+}
+
 extern "C" {
 
 int32_t srl_arena_sizes(const srl_model_cfg* m, const srl_sched_cfg* s, int32_t world, uint64_t* wb, uint64_t* kb,
@@ -860,6 +900,16 @@ int32_t srl_decode_step(srl_engine* e, srl_step_info* info) {
     return b.status;
   }
   const Ctl& c = e->ctl;
+  static const bool mixed_ok = getenv("SRL_NO_MIXED") == nullptr;
+  if (mixed_ok && b.m_pre > 0 && b.m_pre <= e->s.prefill_chunk) {
+    // steady state: the few admitted prompts join the decode pass (direct launches:
+    // the row count varies)
+    e->last_m = e->s.Q_g;
+    decode_tail(e, e->comm == nullptr, e->s.Q_g, b.m_pre);
+    if (e->comm)
+      if (int rc = exchange_and_end(e)) return rc;
+    return finish_step(e, b, info, nullptr);
+  }
   // prefill of newly admitted sequences (prompt ++ kept tokens), in chunks
   for (int r0 = 0; r0 < b.m_pre; r0 += e->s.prefill_chunk) {
     const int mc = b.m_pre - r0 < e->s.prefill_chunk ? b.m_pre - r0 : e->s.prefill_chunk;
@@ -906,28 +956,7 @@ int32_t srl_decode_step(srl_engine* e, srl_step_info* info) {
   }
   if (e->comm)
     if (int rc = exchange_and_end(e)) return rc;
-  cudaEventRecord(e->ev1, st);
-  read_status(e);
-  if (cudaError_t ce = cudaGetLastError()) return cuda_fail("decode step", ce);
-  prof_collect(e, e->direct, false);
-  if (G.exec) prof_collect(e, G.gset, true);
-  const CtlStatus& en = *e->hst;
-  if (info) {
-    info->k = en.k - 1;
-    info->r_k = en.r_k;
-    info->n_finished = en.n_fin;
-    info->n_ready = en.n_ready;
-    info->n_admitted = b.n_admit;
-    info->n_prefill_tokens = b.m_pre;
-    info->sum_ctx = b.sum_ctx;
-    info->r_local = b.r_local;
-    info->v = en.v;
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, e->ev0, e->ev1);
-    info->dt_ms = ms;
-  }
-  if (en.status == SRL_GROUP_READY) e->group_state = 1;
-  return en.status;
+  return finish_step(e, b, info, G.exec ? &G.gset : nullptr);
 }
 
 int32_t srl_harvest_finished(srl_engine* e, int32_t cap_recs, srl_traj* recs, int32_t* n_out, int32_t* toks,
