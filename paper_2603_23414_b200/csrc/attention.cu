@@ -14,6 +14,8 @@
 // and a cross-warp merge.  Per-chunk partials (o, m, l) are merged by
 // attn_combine in chunk order.
 // fp32 KV (test mode): a plain FFMA kernel with the same item/partial format.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "launch.hpp"
 #include "layers.hpp"
@@ -27,9 +29,13 @@ constexpr float kLog2e = 1.4426950408889634f;
 // Split-KV only when the (row, kv head) pairs alone cannot fill the GPU (the
 // drain phase of a rollout: few long sequences); otherwise one item per pair
 // and the attention kernel writes the normalised output itself.
-constexpr int kMinItems = 4 * 148;
-constexpr int kTargetItems = 6 * 148;
-__global__ void attn_plan_kernel(AttnArgs a, int split) {
+// Split-KV only when the (row, kv head) pairs alone leave SMs idle, into ~2 items
+// per SM (measured r01, tools/bench_attn.py: every split item costs a partial
+// write and a merge, so more, smaller items are slower; at 256-512 pairs the
+// longest-first dynamic schedule balances whole rows better than any split)
+constexpr int kMinItems = 148;
+constexpr int kTargetItems = 2 * 148;
+__global__ void attn_plan_kernel(AttnArgs a, int split, int min_items, int target_items) {
   __shared__ int wsum[32];
   __shared__ int base_s, active_s, pages_s;
   pdl_trigger();
@@ -48,10 +54,10 @@ __global__ void attn_plan_kernel(AttnArgs a, int split) {
   atomicAdd(&active_s, my_active);
   atomicAdd(&pages_s, my_pages);
   __syncthreads();
-  if (active_s * a.Hkv >= kMinItems) split = 0;
+  if (active_s * a.Hkv >= min_items) split = 0;
   // split-KV chunk: about kTargetItems items over all (row, head) pairs, never
   // below kChunkPages pages (per-item overhead: q load, 4-warp merge, partials)
-  const int cp = max(kChunkPages, min(256, (pages_s * a.Hkv + kTargetItems - 1) / kTargetItems));
+  const int cp = max(kChunkPages, min(256, (pages_s * a.Hkv + target_items - 1) / target_items));
   if (threadIdx.x == 0) *a.chunk_pages = cp;
   const int chunk_tok = 64 * cp;
   for (int b0 = 0; b0 < a.M; b0 += blockDim.x) {
@@ -555,18 +561,47 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32));
       if (*merge_flag) {
         const int it0 = a.row_item0[ii.m] + ii.kvh * nch;
-        for (int i = threadIdx.x; i < G * DH; i += kConsumerWarps * 32) {
-          const int g = i / DH, d = i % DH;
+        constexpr int kT = kConsumerWarps * 32;
+        // the chunks' (max, sum) go to shared memory once (the 4-warp merge buffer is
+        // free here); per-(chunk, head) scale factors and 1/l are computed there, then
+        // every output element sums its chunks' partials with the loads of four chunks
+        // in flight -- the merge is L2-latency-bound otherwise (chunk order kept:
+        // deterministic)
+        float* sm_m = mrg;
+        float* sm_l = sm_m + nch * G;
+        float* sm_inv = sm_l + nch * G;
+        for (int j = threadIdx.x; j < nch * G; j += kT) {
+          const int cc = j / G, g = j % G;
+          sm_m[j] = __ldcg(a.part_ml + ((size_t)(it0 + cc) * G + g) * 2);
+          sm_l[j] = __ldcg(a.part_ml + ((size_t)(it0 + cc) * G + g) * 2 + 1);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kT));
+        for (int g = threadIdx.x; g < G; g += kT) {
           float mx = -INFINITY;
-          for (int c = 0; c < nch; ++c) mx = fmaxf(mx, __ldcg(a.part_ml + ((size_t)(it0 + c) * G + g) * 2));
-          float acc = 0.f, l = 0.f;
-          for (int c = 0; c < nch; ++c) {
-            const float mc = __ldcg(a.part_ml + ((size_t)(it0 + c) * G + g) * 2);
+          for (int cc = 0; cc < nch; ++cc) mx = fmaxf(mx, sm_m[cc * G + g]);
+          float l = 0.f;
+          for (int cc = 0; cc < nch; ++cc) {
+            const float mc = sm_m[cc * G + g];
             const float f = mc == -INFINITY ? 0.f : exp2f(mc - mx);
-            acc += __ldcg(a.part_o + ((size_t)(it0 + c) * G + g) * DH + d) * f;
-            l += __ldcg(a.part_ml + ((size_t)(it0 + c) * G + g) * 2 + 1) * f;
+            sm_m[cc * G + g] = f;  // from here on: the chunk's scale factor
+            l += sm_l[cc * G + g] * f;
           }
-          const float o = acc / l;
+          sm_inv[g] = 1.f / l;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kT));
+        for (int i = threadIdx.x; i < G * DH; i += kT) {
+          const int g = i / DH, d = i % DH;
+          float acc = 0.f;
+          for (int c0 = 0; c0 < nch; c0 += 4) {
+            float p[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              p[j] = c0 + j < nch ? __ldcg(a.part_o + ((size_t)(it0 + c0 + j) * G + g) * DH + d) : 0.f;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (c0 + j < nch) acc += p[j] * sm_m[(c0 + j) * G + g];
+          }
+          const float o = acc * sm_inv[g];
           const size_t oi = ((size_t)ii.m * a.Hq + ii.kvh * G + g) * DH + d;
           a.out[oi] = __float2bfloat16(o);
           if (a.out_f32) a.out_f32[oi] = o;
@@ -594,7 +629,10 @@ static void launch_bf16(const AttnArgs& a, const void* tk, const void* tv, cudaS
 }
 
 void attn_plan(const AttnArgs& a, int split, cudaStream_t st) {
-  launch_k(attn_plan_kernel, dim3(1), dim3(1024), 0, st, 1, a, split);
+  // experiment knobs (timing only): SRL_ATTN_MIN_ITEMS, SRL_ATTN_TARGET_ITEMS
+  static const int mi = getenv("SRL_ATTN_MIN_ITEMS") ? atoi(getenv("SRL_ATTN_MIN_ITEMS")) : kMinItems;
+  static const int ti = getenv("SRL_ATTN_TARGET_ITEMS") ? atoi(getenv("SRL_ATTN_TARGET_ITEMS")) : kTargetItems;
+  launch_k(attn_plan_kernel, dim3(1), dim3(1024), 0, st, 1, a, split, mi, ti);
 }
 
 void attn_run(const AttnArgs& a, bool kv_fp32, const void* tmap_k, const void* tmap_v, cudaStream_t st) {
