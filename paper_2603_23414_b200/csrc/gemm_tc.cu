@@ -600,25 +600,37 @@ int gemm_bf16_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N
   p.K = K;
   p.m_blk = pick_mblk(M);
   p.m_blocks = (M + p.m_blk - 1) / p.m_blk;
-  static const int h_env = getenv("SRL_GEMM_H") ? atoi(getenv("SRL_GEMM_H")) : 0;
-  p.H = h_env ? h_env : 1;
-  // packed weights pad rows to 128 only: H = 2 needs an even number of 128-row tiles
-  if (epi.w_packed && ((N + 127) / 128) % 2) p.H = 1;
-  p.n_tiles = (N + 128 * p.H - 1) / (128 * p.H);
   p.kb = K / 64;
+  // split-K over a cluster only when the units alone cannot occupy the SMs; all
+  // clusters must be co-resident (GPC packing can hold fewer than num_sms / S
+  // clusters), else a second wave doubles the time
+  auto pick_s = [&](int units) {
+    int S = 1;
+    if (units < num_sms) {
+      S = num_sms / units;
+      if (S > 8) S = 8;
+      if (S > p.kb) S = p.kb;
+      while (S > 1 && units > max_clusters(S)) --S;
+    }
+    return S;
+  };
+  // H (128-row halves per tile): 2 when it keeps more SMs streaming -- e.g. the
+  // 32B shapes at M = 64: QKV 56 tiles x S 2 = 112 CTAs vs 28 x 5 = 140
+  auto util = [&](int H) {
+    const int units = (N + 128 * H - 1) / (128 * H) * p.m_blocks;
+    if (units >= num_sms) return (double)units / ((double)((units + num_sms - 1) / num_sms) * num_sms);
+    return (double)units * pick_s(units) / num_sms;
+  };
+  static const int h_env = getenv("SRL_GEMM_H") ? atoi(getenv("SRL_GEMM_H")) : 0;
+  // packed weights pad rows to 128 only: H = 2 needs an even number of 128-row tiles
+  const bool h2_ok = !(epi.w_packed && ((N + 127) / 128) % 2);
+  p.H = h_env ? h_env : ((h2_ok && util(2) > util(1) + 0.02) ? 2 : 1);
+  if (!h2_ok) p.H = 1;
+  p.n_tiles = (N + 128 * p.H - 1) / (128 * p.H);
   p.units = p.n_tiles * p.m_blocks;
   p.epi = epi;
   p.dbg = (g_dbg && g_dbg_count++ == g_dbg_target) ? g_dbg : nullptr;
-  // split-K over a cluster only when the units alone cannot occupy the SMs
-  int S = 1;
-  if (p.units < num_sms) {
-    S = num_sms / p.units;
-    if (S > 8) S = 8;
-    if (S > p.kb) S = p.kb;
-    // all clusters must be co-resident (GPC packing can hold fewer than
-    // num_sms / S clusters), else a second wave doubles the time
-    while (S > 1 && p.units > max_clusters(S)) --S;
-  }
+  const int S = pick_s(p.units);
   p.S = S;
   // smem: a short ring of activation k-slices and a deep ring of weight k-slices
   const int stage_a = p.H * kStageA;

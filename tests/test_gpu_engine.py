@@ -176,12 +176,15 @@ def test_api_state_errors():
 
 
 # ------------------------------------------------------------------ model parity (teacher forcing)
-@pytest.mark.parametrize("kv,resume", [(KV_FP32, RESUME_KEEP_KV), (KV_BF16, RESUME_KEEP_KV),
-                                       (KV_BF16, RESUME_REPREFILL)], ids=["f32", "bf16", "bf16-reprefill"])
-def test_model_parity_teacher_forced(kv, resume):
+@pytest.mark.parametrize("kv,resume,chunk", [(KV_FP32, RESUME_KEEP_KV, 256), (KV_BF16, RESUME_KEEP_KV, 256),
+                                             (KV_BF16, RESUME_REPREFILL, 256), (KV_BF16, RESUME_KEEP_KV, 24)],
+                         ids=["f32", "bf16", "bf16-reprefill", "bf16-separate-prefill"])
+def test_model_parity_teacher_forced(kv, resume, chunk):
+    """chunk = prefill_chunk: 256 lets every step's admitted prompts join the decode
+    pass (the mixed pass); 24 forces the separate prefill passes (epoch-start path)."""
     cfg = SchedConfig(Q_g=16, U=4, K=K_INF, pool_prompts=16, cap=64, kv_pages=256, kv_dtype=kv, resume=resume)
     off, toks, L = tiny_workload(n_prompts=16)
-    eng = make_engine(TINY, cfg, max_traj=64, max_prompt=16)
+    eng = make_engine(TINY, cfg, max_traj=64, max_prompt=16, prefill_chunk=chunk)
     res = run_engine(eng, TINY, off, toks, L, record_logits=True)
     eng.close()
     teacher, gpu_lp = {}, {}

@@ -24,7 +24,8 @@ def _stream():
 # ------------------------------------------------------------------ GEMM (tcgen05)
 GEMM_SHAPES = [(1, 128, 64), (16, 256, 128), (200, 384, 256), (256, 6144, 4096), (64, 4096, 14336),
                (600, 512, 128), (37, 1000, 192), (256, 7168, 5120), (256, 128256, 4096), (4096, 4096, 4096),
-               (300, 1024, 14336), (256, 4096, 14336), (128, 2048, 4096), (512, 3072, 1024)]
+               (300, 1024, 14336), (256, 4096, 14336), (128, 2048, 4096), (512, 3072, 1024),
+               (64, 7168, 5120), (64, 5120, 5120), (48, 55296, 5120)]   # 32B slice at M = 64: H = 2 tiles
 
 
 def _pack(lib, W):
@@ -90,7 +91,8 @@ def test_gemm_matches_fp64_reference(lib, M, N, K, packed):
 
 
 @pytest.mark.parametrize("packed", [False, True], ids=["rowmajor", "packed"])
-@pytest.mark.parametrize("M,N,K", [(16, 256, 128), (256, 4096, 4096), (77, 640, 14336), (256, 4096, 14336)])
+@pytest.mark.parametrize("M,N,K", [(16, 256, 128), (256, 4096, 4096), (77, 640, 14336), (256, 4096, 14336),
+                                   (64, 5120, 27648)])
 def test_gemm_residual_epilogue(lib, M, N, K, packed):
     g = torch.Generator(device="cuda").manual_seed(3)
     X = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
