@@ -225,6 +225,8 @@ struct srl_engine {
   float* logits = nullptr;
   float *rope_cos = nullptr, *rope_sin = nullptr;
   void* gemm_ws = nullptr;     // GEMM stream-K workspace (zeroed at create, left zeroed by every launch)
+  float4* samp_part = nullptr;  // [Q_g][ceil(V/128)] Gumbel-max partials of the fused LM head
+  int* samp_part_j = nullptr;
   size_t gemm_ws_bytes = 0;
   AttnArgs attn{};
   Ctl ctl{};
@@ -378,6 +380,8 @@ void plan_scratch(srl_engine* e, ScratchPlan& p, bool assign) {
   c.h_lp = (float*)P(4ull * z.h_cap_tok);
   c.h_ver = (int*)P(4ull * z.h_cap_tok);
   c.h_rec = (srl_traj*)P(sizeof(srl_traj) * kMaxGroup);
+  e->samp_part = (float4*)P(16ull * z.Q_g * ((m.V + 127) / 128));
+  e->samp_part_j = (int*)P(4ull * z.Q_g * ((m.V + 127) / 128));
   e->gemm_ws_bytes = gemm_workspace_bytes(kMaxSmsPlan);
   e->gemm_ws = P(e->gemm_ws_bytes);
   e->x_res = (float*)P(4ull * z.mmax * m.d);
@@ -413,6 +417,15 @@ size_t kv_bytes_for(const srl_model_cfg& m, const srl_sched_cfg& s) {
 bool debug_skip(int cls) {
   static const unsigned mask = getenv("SRL_DEBUG_SKIP") ? (unsigned)strtoul(getenv("SRL_DEBUG_SKIP"), nullptr, 16) : 0u;
   return cls >= 0 && ((mask >> cls) & 1u);
+}
+
+// LM head + sampler fusion (EPI_SAMPLE + sample_reduce), opt-in: SRL_FUSED_SAMPLE=1.
+// Measured r01 (cfg2): the Gumbel-max work in the LM head's 8 epilogue warps per SM
+// outlasts the MMAs it should hide behind (LM head 0.21 -> 0.77 ms per step) while
+// the stand-alone sampler, 256 CTAs x 16 warps, costs 0.22 ms -- so it stays off.
+bool fused_sample() {
+  static const bool on = getenv("SRL_FUSED_SAMPLE") != nullptr;
+  return on;
 }
 
 // ---- fused GEMM helper
@@ -518,6 +531,19 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
     fe.ldo = m.V;
     fe.w_packed = 1;
     fe.ws = e->gemm_ws;
+    if (fused_sample()) {  // the sampler's Gumbel-max rides on the LM head's epilogue
+      const Ctl& c = e->ctl;
+      fe.kind = EPI_SAMPLE;
+      fe.s_row_pos = row_pos;
+      fe.s_row_n = c.row_n;
+      fe.s_row_traj = c.row_traj;
+      fe.s_row_restarts = c.row_restarts;
+      fe.s_invT = 1.0f / e->s.temperature;
+      fe.s_seed = e->s.sample_seed;
+      fe.s_part = e->samp_part;
+      fe.s_part_j = e->samp_part_j;
+      fe.s_nblk = (m.V + 127) / 128;
+    }
     run_gemm(e, SRL_K_LM_HEAD, e->xn, m_lm >= 0 ? m_lm : M, (const __nv_bfloat16*)e->plm_head, m.V, d, fe);
   }
 }
@@ -563,7 +589,10 @@ void decode_tail(srl_engine* e, bool with_end, int M, int M_pre = 0) {
   sa.lp_out = (float*)(c.samp + (size_t)e->rank * 2 * e->s.Q_g + e->s.Q_g);
   if (!debug_skip(SRL_K_SAMPLE)) {
     Prof p(e, SRL_K_SAMPLE);
-    sample(sa, st);
+    if (fused_sample())
+      sample_reduce(sa, e->samp_part, e->samp_part_j, (e->m.V + 127) / 128, st);
+    else
+      sample(sa, st);
   }
   e->launches++;
   if (!with_end) return;

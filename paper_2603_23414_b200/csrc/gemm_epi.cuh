@@ -107,6 +107,9 @@ __device__ __forceinline__ void apply_epilogue(const GemmParams& p, int unit_n0,
     if (m < p.M && ng0 < p.N) {
       const bool full = ng0 + 16 <= p.N;
       switch (e.kind) {
+        case EPI_SAMPLE:
+          if (!e.out_f32) break;
+          [[fallthrough]];
         case EPI_F32: {
           float* dst = e.out_f32 + (size_t)m * e.ldo + ng0;
           if (full) {
@@ -185,6 +188,69 @@ __device__ __forceinline__ void apply_epilogue(const GemmParams& p, int unit_n0,
           break;
         }
       }
+    }
+  }
+  if (e.kind == EPI_SAMPLE) {
+    // Gumbel-max over this thread's 16 vocab rows of batch row m, then over the 8
+    // lanes holding the same row (128 vocab rows): the exact-RN score only where a
+    // cheap bound says it could win (gumbel.cuh); ties -> lowest index; the online
+    // LSE of z * invT for the behaviour logprob
+    const int nb = (n & 7) * 16, ng0 = unit_n0 + nb;
+    float bs = -INFINITY, bz = 0.f, mx = -INFINITY, sum = 0.f;
+    int bj = 0x7fffffff;
+    if (m < p.M && e.s_row_pos[m] >= 0) {
+      const uint32_t nt = (uint32_t)e.s_row_n[m], tj = (uint32_t)e.s_row_traj[m], rs = (uint32_t)e.s_row_restarts[m];
+      const uint2 key = make_uint2((uint32_t)(e.s_seed & 0xffffffffu), (uint32_t)(e.s_seed >> 32));
+      const float invT = e.s_invT;
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const int j4 = ng0 + 4 * q4;
+        if (j4 >= p.N) break;
+        const uint4 w = philox4x32_10(make_uint4((uint32_t)(j4 >> 2), nt, tj, rs), key);
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = j4 + q;
+          if (j >= p.N) break;
+          const float z = row[nb + 4 * q4 + q];
+          const float zs = __fmul_rn(z, invT);
+          if (__fadd_rn(zs, gumbel_fast(ws[q])) + kPrune + 1e-6f * fabsf(bs) >= bs) {
+            const float sc = __fadd_rn(zs, gumbel_from_bits(ws[q]));
+            if (better(sc, j, bs, bj)) {
+              bs = sc;
+              bj = j;
+              bz = z;
+            }
+          }
+          if (zs > mx) {
+            sum = sum * expf(mx - zs) + 1.f;
+            mx = zs;
+          } else {
+            sum += expf(zs - mx);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const float os = __shfl_xor_sync(0xffffffffu, bs, o);
+      const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+      const float oz = __shfl_xor_sync(0xffffffffu, bz, o);
+      if (better(os, oj, bs, bj)) {
+        bs = os;
+        bj = oj;
+        bz = oz;
+      }
+      const float om = __shfl_xor_sync(0xffffffffu, mx, o);
+      const float osum = __shfl_xor_sync(0xffffffffu, sum, o);
+      const float nm = fmaxf(mx, om);
+      sum = (mx == -INFINITY ? 0.f : sum * expf(mx - nm)) + (om == -INFINITY ? 0.f : osum * expf(om - nm));
+      mx = nm;
+    }
+    if ((n & 7) == 0 && m < p.M && unit_n0 < p.N) {
+      const size_t idx = (size_t)m * e.s_nblk + (unit_n0 >> 7);
+      e.s_part[idx] = make_float4(bs, bz, mx, sum);
+      e.s_part_j[idx] = bj;
     }
   }
   epi_bar(bar);  // the staging buffer is reused by the next chunk

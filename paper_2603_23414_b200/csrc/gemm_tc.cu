@@ -39,6 +39,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "gumbel.cuh"
 #include "kernels.hpp"
 #include "launch.hpp"
 #include "tma.hpp"

@@ -8,7 +8,7 @@
 
 namespace srl {
 
-enum EpiKind { EPI_F32 = 0, EPI_RESID = 1, EPI_SILU = 2, EPI_QKV = 3 };
+enum EpiKind { EPI_F32 = 0, EPI_RESID = 1, EPI_SILU = 2, EPI_QKV = 3, EPI_SAMPLE = 4 };
 
 struct GemmEpi {
   int kind;
@@ -29,6 +29,16 @@ struct GemmEpi {
   void* k_pool;
   void* v_pool;
   int Hq, Hkv, dh, kv_f32;
+  // EPI_SAMPLE (LM head): logits as EPI_F32 (out_f32, may be null) plus, per batch
+  // row and 128-row vocab block, the Gumbel-max partial of the seeded sampler
+  // (best score, its logit, its index, online max / sum of exp) -- sampler.cu's
+  // sample_reduce finishes the row
+  const int *s_row_pos, *s_row_n, *s_row_traj, *s_row_restarts;
+  float s_invT;
+  unsigned long long s_seed;
+  float4* s_part;  // [M][s_nblk] {best score, its logit, max, sum}
+  int* s_part_j;   // [M][s_nblk]
+  int s_nblk;
   // GEMM workspace (gemm_workspace_bytes, zero-filled before first use; every
   // launch leaves it zeroed): stream-K partial slots + arrival counters.  Null
   // disables stream-K (cluster split-K / whole units instead).

@@ -62,5 +62,8 @@ struct SampleArgs {
   float* lp_out;         // [M]
 };
 void sample(const SampleArgs& a, cudaStream_t st);
+// Finish the rows whose Gumbel-max partials the LM-head GEMM produced (EPI_SAMPLE):
+// part / part_j [M][nblk] in vocab-block order -> token and behaviour logprob.
+void sample_reduce(const SampleArgs& a, const float4* part, const int* part_j, int nblk, cudaStream_t st);
 
 }  // namespace srl

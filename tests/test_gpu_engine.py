@@ -133,6 +133,23 @@ def test_edge_cases_bit_exact(name, over, n, plen, cap):
     assert sum(len(h.records) for h, _ in res["groups"]) == n
 
 
+def test_fused_lm_head_sampling_matches():
+    """The opt-in LM-head-fused sampler (SRL_FUSED_SAMPLE=1: EPI_SAMPLE partials in
+    the GEMM epilogue + sample_reduce) must pass the same teacher-forced parity test
+    -- schedule bit-exact, ids bit-exact vs the oracle's Gumbel-max on the GPU
+    logits, logits / logprobs within tolerance.  Run in a subprocess: the switch is
+    read once per process.  (Off by default: slower.)"""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SRL_FUSED_SAMPLE="1")
+    out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                          "tests/test_gpu_engine.py::test_model_parity_teacher_forced"],
+                         cwd=root, capture_output=True, text=True, env=env, timeout=900)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
+
+
 def test_two_epochs_and_counters():
     cfg = SchedConfig(Q_g=8, U=4, K=K_INF, pool_prompts=8, cap=64, kv_pages=128, kv_dtype=KV_BF16)
     off, toks, L = tiny_workload(n_prompts=24)
