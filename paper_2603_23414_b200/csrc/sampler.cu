@@ -60,10 +60,10 @@ __global__ void __launch_bounds__(kSampThreads) sample_kernel(SampleArgs a) {
           }
         }
         if (zs > mx) {
-          sum = sum * expf(mx - zs) + 1.f;
+          sum = sum * __expf(mx - zs) + 1.f;
           mx = zs;
         } else {
-          sum += expf(zs - mx);
+          sum += __expf(zs - mx);
         }
       }
     }
