@@ -508,6 +508,10 @@ def main():
         "kernel_ms_per_decode_step": {k: v[0] / nb for k, v in r["breakdown"].items()},
         "kernel_breakdown_note": "one extra round with every class bracketed by CUDA events (which also cut the "
                                  "decode graph's PDL edges); not part of the timed value",
+        "paper_context": {"note": "context, not the target: P:336-339, H100/MI300X mix (P:239), GPU type/count, engine "
+                                  "capacity and length trace unstated",
+                          "bubble": {"sync_baseline": 0.74, "sortedrl_on_policy": 0.0581, "sortedrl_partial": 0.0337},
+                          "tokens_per_s": {"sync_baseline": 3987, "sortedrl_on_policy": 4289, "sortedrl_partial": 5559}},
         "gpu_launches": r["launches"],
         "clocks": r["clocks"],
         "e2e": r["e2e"],
