@@ -225,6 +225,8 @@ struct srl_engine {
   float* logits = nullptr;
   float *rope_cos = nullptr, *rope_sin = nullptr;
   void* gemm_ws = nullptr;     // GEMM stream-K workspace (zeroed at create, left zeroed by every launch)
+  float* norm_part = nullptr;    // split-K partials of the O / down projections for the next RMSNorm
+  size_t norm_part_floats = 0;
   float4* samp_part = nullptr;  // [Q_g][ceil(V/128)] Gumbel-max partials of the fused LM head
   int* samp_part_j = nullptr;
   size_t gemm_ws_bytes = 0;
@@ -380,6 +382,8 @@ void plan_scratch(srl_engine* e, ScratchPlan& p, bool assign) {
   c.h_lp = (float*)P(4ull * z.h_cap_tok);
   c.h_ver = (int*)P(4ull * z.h_cap_tok);
   c.h_rec = (srl_traj*)P(sizeof(srl_traj) * kMaxGroup);
+  e->norm_part_floats = 4ull * (z.Q_g > 512 ? z.Q_g : 512) * m.d;  // S <= 4 splits of <= 512 rows (gemm_partial_split)
+  e->norm_part = (float*)P(4ull * e->norm_part_floats);
   e->samp_part = (float4*)P(16ull * z.Q_g * ((m.V + 127) / 128));
   e->samp_part_j = (int*)P(4ull * z.Q_g * ((m.V + 127) / 128));
   e->gemm_ws_bytes = gemm_workspace_bytes(kMaxSmsPlan);
@@ -491,6 +495,17 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
   re.kind = EPI_RESID;
   re.x_res = e->x_res;
   re.ldo = d;
+  // split-K O / down projections hand their partials to the next RMSNorm (which
+  // sums them in split order and adds the residual: the same fp32 operations the
+  // GEMM's own DSMEM reduction + residual add would do) when the pair GEMM splits
+  int S_o = gemm_partial_split(M, d, qd, e->num_sms), S_d = gemm_partial_split(M, d, m.ff, e->num_sms);
+  if ((size_t)S_o * M * d > e->norm_part_floats) S_o = 1;
+  if ((size_t)S_d * M * d > e->norm_part_floats) S_d = 1;
+  GemmEpi pe = re;
+  pe.kind = EPI_PARTIAL;
+  pe.part = e->norm_part;
+  pe.part_stride = (size_t)M * d;
+  pe.ldo = d;
   GemmEpi se{};
   se.w_packed = 1;
   se.ws = e->gemm_ws;
@@ -510,17 +525,19 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
       Prof p(e, D + SRL_K_ATTN, 2);
       attn_run(a, e->kv_f32, &e->tmK[l], &e->tmV[l], st);
     }
-    run_gemm(e, D + SRL_K_GEMM_O, e->attn_out, M, (const __nv_bfloat16*)w.po, d, qd, re);
+    run_gemm(e, D + SRL_K_GEMM_O, e->attn_out, M, (const __nv_bfloat16*)w.po, d, qd, S_o > 1 ? pe : re);
     if (!debug_skip(D + SRL_K_ELEMWISE)) {
       Prof p(e, D + SRL_K_ELEMWISE);
-      rmsnorm(e->x_res, row_tok, row_pos, M, d, nullptr, w.mlp_norm, m.rms_eps, e->xn, st);
+      rmsnorm(e->x_res, row_tok, row_pos, M, d, nullptr, w.mlp_norm, m.rms_eps, e->xn, st,
+              S_o > 1 ? e->norm_part : nullptr, S_o, (size_t)M * d);
     }
     run_gemm(e, D + SRL_K_GEMM_GU, e->xn, M, (const __nv_bfloat16*)w.pgu, 2 * m.ff, d, se);  // interleaved gate/up
-    run_gemm(e, D + SRL_K_GEMM_DOWN, e->act, M, (const __nv_bfloat16*)w.pd, d, m.ff, re);
+    run_gemm(e, D + SRL_K_GEMM_DOWN, e->act, M, (const __nv_bfloat16*)w.pd, d, m.ff, S_d > 1 ? pe : re);
     if (!debug_skip(D + SRL_K_ELEMWISE)) {
       Prof p(e, D + SRL_K_ELEMWISE);
       const __nv_bfloat16* next = l + 1 < m.L ? e->lw[l + 1].attn_norm : e->final_norm;
-      rmsnorm(e->x_res, row_tok, row_pos, M, d, nullptr, next, m.rms_eps, e->xn, st);
+      rmsnorm(e->x_res, row_tok, row_pos, M, d, nullptr, next, m.rms_eps, e->xn, st,
+              S_d > 1 ? e->norm_part : nullptr, S_d, (size_t)M * d);
     }
     e->launches += 4;
   }

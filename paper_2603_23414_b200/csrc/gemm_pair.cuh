@@ -403,6 +403,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tc_fence_after();
       if (lane == 0 && qw == 0) DBG(6);
     }
+    if (p.epi.kind == EPI_PARTIAL) {
+      // hand the partial to the next RMSNorm (which sums the S splits in order and
+      // adds the residual): no DSMEM exchange, no cluster barriers
+      if (epi && unit_n0 < p.N) {
+        const uint32_t tl = tbase + ((uint32_t)(qw * 32) << 16);
+        float* dst = p.epi.part + (size_t)pi * p.epi.part_stride + unit_n0 + n;
+        const bool rok = unit_n0 + n < p.N;
+        for (int c = eg; c < nchunk; c += 2) {
+          float v[16];
+          tmem_ld16(tl + (uint32_t)(c * 16), v);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int m = m_base + c * 16 + j;
+            if (rok && m < p.M) dst[(size_t)m * p.epi.ldo] = v[j];  // a warp writes 128 contiguous bytes
+          }
+        }
+      }
+    } else {
     cluster_sync_all();  // every CTA's mainloop is done: all rings may be overwritten
     if (threadIdx.x == 0) DBG(13);
     if (epi) {
@@ -456,6 +474,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       if (w == 2 && lane == 0) DBG(15);
     }
+    }  // EPI_PARTIAL else
   }
   tc_fence_before();
   cluster_sync_all();  // both CTAs done with the pair's TMEM before it is freed

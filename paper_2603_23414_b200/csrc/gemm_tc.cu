@@ -478,7 +478,7 @@ size_t gemm_workspace_bytes(int num_sms) {
 }
 
 static int gemm_pair_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N, int K, const GemmEpi& epi,
-                           int num_sms, cudaStream_t stream) {
+                           int num_sms, cudaStream_t stream, int* plan_s = nullptr) {
   GemmParams p;
   memset(&p, 0, sizeof(p));
   p.M = M;
@@ -516,7 +516,7 @@ static int gemm_pair_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W
   p.kb = K / 64;
   p.units = p.n_tiles * p.m_blocks;
   p.epi = epi;
-  p.dbg = (g_dbg && g_dbg_count++ == g_dbg_target) ? g_dbg : nullptr;
+  p.dbg = (!plan_s && g_dbg && g_dbg_count++ == g_dbg_target) ? g_dbg : nullptr;
   const bool sk = mode == 2 && epi.ws && p.units % pairs != 0 && p.units <= kSkMaxUnits;
   int S = 1;
   if (!sk && !bsplit && p.units < pairs) {
@@ -544,6 +544,11 @@ static int gemm_pair_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W
     const int cpr = ((p.m_blk >> 4) + S - 1) / S;
     if ((size_t)S * cpr * 8192 > rings) return 1;
   }
+  if (plan_s) {  // dry run: report the split factor of the cluster split-K path
+    *plan_s = (!sk && !bsplit && S > 1) ? S : 1;
+    return 0;
+  }
+  if (epi.kind == EPI_PARTIAL && !(S > 1 && !sk && !bsplit)) return -1;  // caller must ask gemm_partial_split
   p.acc_stages = (S == 1 && 2 * p.m_blk <= 512) ? 2 : 1;
   int tc = 32;
   while (tc < p.m_blk * p.acc_stages) tc <<= 1;
@@ -581,6 +586,19 @@ static int gemm_pair_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W
   }
   if (rc) cudaGetLastError();
   return rc;
+}
+
+int gemm_partial_split(int M, int N, int K, int num_sms) {
+  static const int pair_env = getenv("SRL_GEMM_PAIR") ? atoi(getenv("SRL_GEMM_PAIR")) : -1;
+  static const bool off = getenv("SRL_NO_PARTIAL_NORM") != nullptr;
+  const bool pair = pair_env >= 0 ? pair_env > 0 : M >= 128;
+  if (off || !pair || M <= 0 || K % 64) return 1;
+  GemmEpi e{};
+  e.kind = EPI_RESID;
+  e.w_packed = 1;
+  int S = 1;
+  if (gemm_pair_fused(nullptr, M, nullptr, N, K, e, num_sms, nullptr, &S) != 0) return 1;
+  return S;
 }
 
 int gemm_bf16_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N, int K, const GemmEpi& epi,

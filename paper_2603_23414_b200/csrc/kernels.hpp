@@ -8,7 +8,7 @@
 
 namespace srl {
 
-enum EpiKind { EPI_F32 = 0, EPI_RESID = 1, EPI_SILU = 2, EPI_QKV = 3, EPI_SAMPLE = 4 };
+enum EpiKind { EPI_F32 = 0, EPI_RESID = 1, EPI_SILU = 2, EPI_QKV = 3, EPI_SAMPLE = 4, EPI_PARTIAL = 5 };
 
 struct GemmEpi {
   int kind;
@@ -29,6 +29,11 @@ struct GemmEpi {
   void* k_pool;
   void* v_pool;
   int Hq, Hkv, dh, kv_f32;
+  // EPI_PARTIAL (split-K pair GEMM only, see gemm_partial_split): CTA pair j of the
+  // split writes its fp32 partial to part + j * part_stride as [M][ldo] -- the
+  // residual add and the sum over splits are left to the next RMSNorm
+  float* part;
+  size_t part_stride;
   // EPI_SAMPLE (LM head): logits as EPI_F32 (out_f32, may be null) plus, per batch
   // row and 128-row vocab block, the Gumbel-max partial of the seeded sampler
   // (best score, its logit, its index, online max / sum of exp) -- sampler.cu's
@@ -48,6 +53,9 @@ struct GemmEpi {
 constexpr size_t kSkSlotBytes = 128 * 256 * 4;  // one CTA's fp32 partial: 128 rows x <= 256 batch columns
 constexpr int kSkMaxUnits = 8192;               // stream-K counters: pair units per launch
 size_t gemm_workspace_bytes(int num_sms);
+// The split-K factor S the pair GEMM will use for this shape (> 1: EPI_PARTIAL is
+// available and leaves S partials), else 1.
+int gemm_partial_split(int M, int N, int K, int num_sms);
 
 // ---- gemm_tc.cu
 // Y = X[M,K] . W[N,K]^T with the fused epilogue `epi` (for EPI_SILU, W's

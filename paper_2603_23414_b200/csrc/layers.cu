@@ -36,7 +36,8 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(float* __restrict
                                                                 const int* __restrict__ row_pos, int M, int d,
                                                                 const __nv_bfloat16* __restrict__ embed,
                                                                 const __nv_bfloat16* __restrict__ w, float eps,
-                                                                __nv_bfloat16* __restrict__ y) {
+                                                                __nv_bfloat16* __restrict__ y, const float* __restrict__ part,
+                                                                int nsplit, size_t part_stride) {
   __shared__ float red[kNormThreads / 32];
   pdl_trigger();
   pdl_wait();
@@ -57,6 +58,22 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(float* __restrict
         v[k] = make_float4(bf16lo(raw.x), bf16hi(raw.x), bf16lo(raw.y), bf16hi(raw.y));
       } else {
         v[k] = reinterpret_cast<const float4*>(x)[i];
+        if (part) {
+          // the previous split-K GEMM's partials: summed in split (= k) order, then
+          // added to the residual -- the same fp32 operations its own epilogue did
+          float4 acc = __ldcg(reinterpret_cast<const float4*>(part + (size_t)m * d) + i);
+          for (int sp = 1; sp < nsplit; ++sp) {
+            const float4 q = __ldcg(reinterpret_cast<const float4*>(part + sp * part_stride + (size_t)m * d) + i);
+            acc.x += q.x;
+            acc.y += q.y;
+            acc.z += q.z;
+            acc.w += q.w;
+          }
+          v[k].x += acc.x;
+          v[k].y += acc.y;
+          v[k].z += acc.z;
+          v[k].w += acc.w;
+        }
       }
       wr[k] = __ldg(reinterpret_cast<const uint2*>(w) + i);
     }
@@ -67,7 +84,7 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(float* __restrict
     const int i = threadIdx.x + k * kNormThreads;
     if (i < nv) {
       if (!active) v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (e) reinterpret_cast<float4*>(x)[i] = v[k];
+      if (e || part) reinterpret_cast<float4*>(x)[i] = v[k];
       ss += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
     }
   }
@@ -92,8 +109,11 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(float* __restrict
 }
 
 void rmsnorm(float* x_res, const int* row_tok, const int* row_pos, int M, int d, const __nv_bfloat16* embed,
-             const __nv_bfloat16* w, float eps, __nv_bfloat16* y, cudaStream_t st) {
-  if (M > 0) launch_k(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, st, 1, x_res, row_tok, row_pos, M, d, embed, w, eps, y);
+             const __nv_bfloat16* w, float eps, __nv_bfloat16* y, cudaStream_t st, const float* part, int nsplit,
+             size_t part_stride) {
+  if (M > 0)
+    launch_k(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, st, 1, x_res, row_tok, row_pos, M, d, embed, w, eps, y,
+             part, nsplit, part_stride);
 }
 
 }  // namespace srl

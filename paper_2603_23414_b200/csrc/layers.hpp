@@ -9,8 +9,11 @@ namespace srl {
 void rope_table(float* cos_t, float* sin_t, int max_pos, int dh, double theta, cudaStream_t st);
 // RMSNorm of the fp32 residual rows into the bf16 GEMM operand; with `embed`
 // non-null the residual row is first set to the embedding of row_tok[m].
+// part (optional): nsplit fp32 partials [M][d] (part_stride floats apart) of the
+// previous split-K GEMM (EPI_PARTIAL), summed in order and added to x_res first.
 void rmsnorm(float* x_res, const int* row_tok, const int* row_pos, int M, int d, const __nv_bfloat16* embed,
-             const __nv_bfloat16* w, float eps, __nv_bfloat16* y, cudaStream_t st);
+             const __nv_bfloat16* w, float eps, __nv_bfloat16* y, cudaStream_t st, const float* part = nullptr,
+             int nsplit = 0, size_t part_stride = 0);
 
 // ---- attention.cu
 // Work item = (row, kv head, chunk of kChunkPages pages).  The plan kernel
