@@ -225,6 +225,8 @@ struct srl_engine {
   float* logits = nullptr;
   float *rope_cos = nullptr, *rope_sin = nullptr;
   void* gemm_ws = nullptr;     // GEMM stream-K workspace (zeroed at create, left zeroed by every launch)
+  float* qkv_part = nullptr;     // split-K partials of the QKV projection for qkv_finish
+  size_t qkv_part_floats = 0;
   float* norm_part = nullptr;    // split-K partials of the O / down projections for the next RMSNorm
   size_t norm_part_floats = 0;
   float4* samp_part = nullptr;  // [Q_g][ceil(V/128)] Gumbel-max partials of the fused LM head
@@ -384,6 +386,8 @@ void plan_scratch(srl_engine* e, ScratchPlan& p, bool assign) {
   c.h_rec = (srl_traj*)P(sizeof(srl_traj) * kMaxGroup);
   e->norm_part_floats = 4ull * (z.Q_g > 512 ? z.Q_g : 512) * m.d;  // S <= 4 splits of <= 512 rows (gemm_partial_split)
   e->norm_part = (float*)P(4ull * e->norm_part_floats);
+  e->qkv_part_floats = 4ull * (z.Q_g > 512 ? z.Q_g : 512) * z.qkv_n;
+  e->qkv_part = (float*)P(4ull * e->qkv_part_floats);
   e->samp_part = (float4*)P(16ull * z.Q_g * ((m.V + 127) / 128));
   e->samp_part_j = (int*)P(4ull * z.Q_g * ((m.V + 127) / 128));
   e->gemm_ws_bytes = gemm_workspace_bytes(kMaxSmsPlan);
@@ -501,6 +505,19 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
   int S_o = gemm_partial_split(M, d, qd, e->num_sms), S_d = gemm_partial_split(M, d, m.ff, e->num_sms);
   if ((size_t)S_o * M * d > e->norm_part_floats) S_o = 1;
   if ((size_t)S_d * M * d > e->norm_part_floats) S_d = 1;
+  // the QKV projection can likewise leave its partials to qkv_finish (bias, RoPE, KV
+  // append) -- opt-in (SRL_QKV_FINISH=1): measured r01 slower (QKV 1.10 -> 1.34 ms per
+  // step): the one-CTA-per-row finish is latency-bound on the partial reads
+  static const bool qkv_part_on = getenv("SRL_QKV_FINISH") != nullptr;
+  int S_q = qkv_part_on ? gemm_partial_split(M, Nqkv, d, e->num_sms) : 1;
+  if ((size_t)S_q * M * Nqkv > e->qkv_part_floats) S_q = 1;
+  GemmEpi pq{};
+  pq.kind = EPI_PARTIAL;
+  pq.w_packed = 1;
+  pq.ws = e->gemm_ws;
+  pq.part = e->qkv_part;
+  pq.part_stride = (size_t)M * Nqkv;
+  pq.ldo = Nqkv;
   GemmEpi pe = re;
   pe.kind = EPI_PARTIAL;
   pe.part = e->norm_part;
@@ -517,7 +534,34 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
     qe.bias = m.qkv_bias ? w.bqkv : nullptr;
     qe.k_pool = e->kpool[l];
     qe.v_pool = e->vpool[l];
-    run_gemm(e, D + SRL_K_GEMM_QKV, e->xn, M, (const __nv_bfloat16*)w.pqkv, Nqkv, d, qe);
+    if (S_q > 1) {  // split-K partials, then bias + RoPE + KV append in one elementwise pass
+      run_gemm(e, D + SRL_K_GEMM_QKV, e->xn, M, (const __nv_bfloat16*)w.pqkv, Nqkv, d, pq);
+      if (!debug_skip(D + SRL_K_GEMM_QKV)) {
+        Prof p(e, D + SRL_K_GEMM_QKV);
+        QkvFinishArgs fa{};
+        fa.part = e->qkv_part;
+        fa.part_stride = (size_t)M * Nqkv;
+        fa.nsplit = S_q;
+        fa.bias = qe.bias;
+        fa.row_pos = row_pos;
+        fa.row_slot = row_slot;
+        fa.page_table = e->ctl.page_table;
+        fa.max_pages = e->z.max_pages;
+        fa.rope_cos = e->rope_cos;
+        fa.rope_sin = e->rope_sin;
+        fa.q_out = e->qbuf;
+        fa.k_pool = e->kpool[l];
+        fa.v_pool = e->vpool[l];
+        fa.Hq = m.Hq;
+        fa.Hkv = m.Hkv;
+        fa.dh = m.dh;
+        fa.kv_f32 = e->kv_f32 ? 1 : 0;
+        qkv_finish(fa, M, st);
+        e->launches++;
+      }
+    } else {
+      run_gemm(e, D + SRL_K_GEMM_QKV, e->xn, M, (const __nv_bfloat16*)w.pqkv, Nqkv, d, qe);
+    }
     a.k_pool = e->kpool[l];
     a.v_pool = e->vpool[l];
     a.work_ctr = e->attn.work_ctr + l;  // one counter per layer, all zeroed by attn_plan

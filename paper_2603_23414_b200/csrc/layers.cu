@@ -108,6 +108,63 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(float* __restrict
   }
 }
 
+// ---------------------------------------------------------------- QKV finish
+// The QKV projection's split-K partials (EPI_PARTIAL, [nsplit][M][N] fp32) summed in
+// split order, + bias, RoPE on the q / k heads at the row's position (rotate_half
+// pairs (i, i + dh/2)), then q -> q_out [M][Hq][dh] and k / v -> the row's KV page
+// (page_table[slot][pos / 64], row pos % 64) -- the EPI_QKV epilogue, after the
+// GEMM instead of inside it.  One CTA per row; thread t owns a (head, i < dh/2) pair.
+__global__ void __launch_bounds__(256) qkv_finish_kernel(QkvFinishArgs a) {
+  pdl_trigger();
+  pdl_wait();
+  const int m = blockIdx.x;
+  const int pos = a.row_pos[m];
+  if (pos < 0) return;
+  const int half = a.dh / 2, H = a.Hq + 2 * a.Hkv, N = H * a.dh;
+  const int page = a.page_table[(size_t)a.row_slot[m] * a.max_pages + pos / 64];
+  for (int t = threadIdx.x; t < H * half; t += blockDim.x) {
+    const int h = t / half, i = t % half;
+    const int n0 = h * a.dh + i, n1 = n0 + half;
+    float x0 = 0.f, x1 = 0.f;
+    for (int sp = 0; sp < a.nsplit; ++sp) {
+      const float* p = a.part + sp * a.part_stride + (size_t)m * N;
+      x0 += __ldcg(p + n0);
+      x1 += __ldcg(p + n1);
+    }
+    if (a.bias) {
+      x0 += __bfloat162float(a.bias[n0]);
+      x1 += __bfloat162float(a.bias[n1]);
+    }
+    float y0 = x0, y1 = x1;
+    if (h < a.Hq + a.Hkv) {
+      const float c = a.rope_cos[(size_t)pos * half + i], s = a.rope_sin[(size_t)pos * half + i];
+      y0 = x0 * c - x1 * s;
+      y1 = x1 * c + x0 * s;
+    }
+    size_t off;
+    void* base;
+    if (h < a.Hq) {
+      off = ((size_t)m * a.Hq + h) * a.dh;
+      base = a.q_out;
+    } else {
+      const int kvh = h < a.Hq + a.Hkv ? h - a.Hq : h - a.Hq - a.Hkv;
+      off = (((size_t)page * a.Hkv + kvh) * 64 + pos % 64) * a.dh;
+      base = h < a.Hq + a.Hkv ? a.k_pool : a.v_pool;
+    }
+    if (a.kv_f32) {
+      reinterpret_cast<float*>(base)[off + i] = y0;
+      reinterpret_cast<float*>(base)[off + i + half] = y1;
+    } else {
+      reinterpret_cast<__nv_bfloat16*>(base)[off + i] = __float2bfloat16(y0);
+      reinterpret_cast<__nv_bfloat16*>(base)[off + i + half] = __float2bfloat16(y1);
+    }
+  }
+}
+
+void qkv_finish(const QkvFinishArgs& a, int M, cudaStream_t st) {
+  if (M > 0) launch_k(qkv_finish_kernel, dim3(M), dim3(256), 0, st, 1, a);
+}
+
 void rmsnorm(float* x_res, const int* row_tok, const int* row_pos, int M, int d, const __nv_bfloat16* embed,
              const __nv_bfloat16* w, float eps, __nv_bfloat16* y, cudaStream_t st, const float* part, int nsplit,
              size_t part_stride) {

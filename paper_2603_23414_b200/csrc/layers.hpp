@@ -15,6 +15,25 @@ void rmsnorm(float* x_res, const int* row_tok, const int* row_pos, int M, int d,
              const __nv_bfloat16* w, float eps, __nv_bfloat16* y, cudaStream_t st, const float* part = nullptr,
              int nsplit = 0, size_t part_stride = 0);
 
+// QKV projection finish from split-K partials (see layers.cu)
+struct QkvFinishArgs {
+  const float* part;
+  size_t part_stride;
+  int nsplit;
+  const __nv_bfloat16* bias;  // nullable
+  const int* row_pos;
+  const int* row_slot;
+  const int* page_table;
+  int max_pages;
+  const float* rope_cos;
+  const float* rope_sin;
+  void* q_out;
+  void* k_pool;
+  void* v_pool;
+  int Hq, Hkv, dh, kv_f32;
+};
+void qkv_finish(const QkvFinishArgs& a, int M, cudaStream_t st);
+
 // ---- attention.cu
 // Work item = (row, kv head, chunk of kChunkPages pages).  The plan kernel
 // builds the item list from row_pos (ctx = pos + 1).
