@@ -139,3 +139,18 @@ def test_fullwidth_teacher_forced(shape, Q_g):
     # near ties: with V >= 128k the top-2 Gumbel-perturbed score gap is ~Exp(1), so a
     # 4x max-abs-error band of ~0.2 excludes ~20% of positions; most must still decide
     assert checked >= 0.6 * (checked + excluded)
+
+
+def test_fullwidth_qkv_finish_path():
+    """The opt-in QKV handoff (SRL_QKV_FINISH=1: split-K partials + the bias / RoPE /
+    KV-append kernel) passes the same full-width parity test.  Subprocess: the
+    switch is read once per process."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SRL_QKV_FINISH="1")
+    out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                          "tests/test_gpu_fullwidth.py::test_fullwidth_teacher_forced[llama8b-L2-Q256]"],
+                         cwd=root, capture_output=True, text=True, env=env, timeout=1200)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
