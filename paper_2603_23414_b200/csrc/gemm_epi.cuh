@@ -59,12 +59,38 @@ __device__ __forceinline__ void fill_row_table(const GemmParams& p, int m_base, 
   asm volatile("bar.sync 3, 256;" ::: "memory");
 }
 
+// EPI_QKV: the RoPE cos / sin run (16 values each) this thread will need for the
+// chunk whose batch rows start at m0_local (rows of the unit's row table): loaded
+// one chunk ahead by the split-K reduction loop, so the L2 latency overlaps the
+// previous chunk's epilogue instead of stalling every chunk.
+struct RopePre {
+  float4 c[4], s[4];
+  bool ok;
+};
+__device__ __forceinline__ void rope_prefetch(const GemmParams& p, int unit_n0, int n, const int* rtab_chunk, RopePre& r) {
+  const GemmEpi& e = p.epi;
+  r.ok = false;
+  if (e.kind != EPI_QKV) return;
+  const int ml = n >> 3, nb = (n & 7) * 16, ng0 = unit_n0 + nb;
+  const int pos = rtab_chunk[ml];
+  const int dh = e.dh, half = dh / 2, h = ng0 / dh, i0 = ng0 % dh;
+  if (pos < 0 || ng0 >= p.N || h >= e.Hq + e.Hkv) return;
+  const int d0 = i0 < half ? i0 : i0 - half;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    r.c[q] = __ldg(reinterpret_cast<const float4*>(e.rope_cos + (size_t)pos * half + d0) + q);
+    r.s[q] = __ldg(reinterpret_cast<const float4*>(e.rope_sin + (size_t)pos * half + d0) + q);
+  }
+  r.ok = true;
+}
+
 // ---------------------------------------------------------------- fused epilogue
 // v[j]: value of weight row unit_n0 + n for batch row m0 + j, j < 16.
+// pre: optional prefetched RoPE run for this chunk (EPI_QKV).
 // xch: this group's shared staging buffer (kXchFloats); bar: its named barrier;
 // rtab: the unit's row table (fill_row_table) advanced to row m0.
 __device__ __forceinline__ void apply_epilogue(const GemmParams& p, int unit_n0, int n, int m0, const float (&v)[16],
-                                               float* xch, int bar, const int* rtab) {
+                                               float* xch, int bar, const int* rtab, const RopePre* pre = nullptr) {
   const GemmEpi& e = p.epi;
   const int* spos = rtab;
   const int* spage = rtab + 256;
@@ -155,8 +181,9 @@ __device__ __forceinline__ void apply_epilogue(const GemmParams& p, int unit_n0,
             float c[16], s[16];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              const float4 cq = __ldg(reinterpret_cast<const float4*>(e.rope_cos + (size_t)pos * half + d0) + q);
-              const float4 sq = __ldg(reinterpret_cast<const float4*>(e.rope_sin + (size_t)pos * half + d0) + q);
+              const bool have = pre && pre->ok;
+              const float4 cq = have ? pre->c[q] : __ldg(reinterpret_cast<const float4*>(e.rope_cos + (size_t)pos * half + d0) + q);
+              const float4 sq = have ? pre->s[q] : __ldg(reinterpret_cast<const float4*>(e.rope_sin + (size_t)pos * half + d0) + q);
               c[4 * q] = cq.x; c[4 * q + 1] = cq.y; c[4 * q + 2] = cq.z; c[4 * q + 3] = cq.w;
               s[4 * q] = sq.x; s[4 * q + 1] = sq.y; s[4 * q + 2] = sq.z; s[4 * q + 3] = sq.w;
             }

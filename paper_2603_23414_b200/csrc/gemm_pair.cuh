@@ -455,7 +455,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (threadIdx.x == 0) DBG(14);
     if (epi && unit_n0 < p.N) {
       const int c0 = pi * nchunk / p.S, c1 = (pi + 1) * nchunk / p.S;
+      RopePre pre_next;
+      if (c0 + eg < c1) rope_prefetch(p, unit_n0, n, rtab + (c0 + eg) * 16, pre_next);
       for (int c = c0 + eg; c < c1; c += 2) {
+        const RopePre pre = pre_next;
+        if (c + 2 < c1) rope_prefetch(p, unit_n0, n, rtab + (c + 2) * 16, pre_next);  // one chunk ahead
         float v[16];
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) v[jj] = 0.f;
@@ -470,7 +474,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             v[4 * q4 + 3] += x.w;
           }
         }
-        apply_epilogue(p, unit_n0, n, m_base + c * 16, v, xg, 1 + eg, rtab + c * 16);
+        apply_epilogue(p, unit_n0, n, m_base + c * 16, v, xg, 1 + eg, rtab + c * 16, &pre);
       }
       if (w == 2 && lane == 0) DBG(15);
     }
