@@ -110,10 +110,27 @@ __global__ void attn_plan_kernel(AttnArgs a, int split, int min_items, int targe
   if (a.merge_ctr)
     for (int i = threadIdx.x; i < a.M * a.Hkv; i += blockDim.x) a.merge_ctr[i] = 0;
   // rows without context get no item: their (bf16) output is zeroed here, once per
-  // forward, so the O projection never reads stale values for them
-  for (int m = 0; m < a.M; ++m)
-    if (a.row_pos[m] < 0)
-      for (int i = threadIdx.x; i < a.Hq * a.dh; i += blockDim.x) a.out[(size_t)m * a.Hq * a.dh + i] = __float2bfloat16(0.f);
+  // forward, so the O projection never reads stale values for them (all threads
+  // over the inactive rows' elements, 8 bf16 per store)
+  {
+    __shared__ int n_idle;
+    __shared__ int idle[1024];
+    if (threadIdx.x == 0) n_idle = 0;
+    __syncthreads();
+    for (int m = threadIdx.x; m < a.M; m += blockDim.x)
+      if (a.row_pos[m] < 0) {
+        const int k = atomicAdd(&n_idle, 1);
+        if (k < 1024) idle[k] = m;
+      }
+    __syncthreads();
+    const int per = a.Hq * a.dh / 8;  // uint4 per row (Hq * dh % 8 == 0)
+    const int ni = min(n_idle, 1024);
+    for (int i = threadIdx.x; i < ni * per; i += blockDim.x)
+      reinterpret_cast<uint4*>(a.out + (size_t)idle[i / per] * a.Hq * a.dh)[i % per] = make_uint4(0u, 0u, 0u, 0u);
+    for (int m = 0; n_idle > 1024 && m < a.M; ++m)  // (more than 1024 idle rows: rare, slow path)
+      if (a.row_pos[m] < 0)
+        for (int i = threadIdx.x; i < a.Hq * a.dh; i += blockDim.x) a.out[(size_t)m * a.Hq * a.dh + i] = __float2bfloat16(0.f);
+  }
   // processing order: counting sort by descending page count (longest first:
   // the persistent CTAs then pull items LPT-style from a counter)
   __shared__ int hist[1024];
