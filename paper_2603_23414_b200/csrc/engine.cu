@@ -503,8 +503,8 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
   // sums them in split order and adds the residual: the same fp32 operations the
   // GEMM's own DSMEM reduction + residual add would do) when the pair GEMM splits
   int S_o = gemm_partial_split(M, d, qd, e->num_sms), S_d = gemm_partial_split(M, d, m.ff, e->num_sms);
-  if ((size_t)S_o * M * d > e->norm_part_floats) S_o = 1;
-  if ((size_t)S_d * M * d > e->norm_part_floats) S_d = 1;
+  if ((size_t)S_o * M * d > e->norm_part_floats || S_o > 4) S_o = 1;  // rmsnorm sums <= 4 splits
+  if ((size_t)S_d * M * d > e->norm_part_floats || S_d > 4) S_d = 1;
   // the QKV projection can likewise leave its partials to qkv_finish (bias, RoPE, KV
   // append) -- opt-in (SRL_QKV_FINISH=1): measured r01 slower (QKV 1.10 -> 1.34 ms per
   // step): the one-CTA-per-row finish is latency-bound on the partial reads

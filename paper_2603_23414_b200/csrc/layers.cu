@@ -61,14 +61,21 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(float* __restrict
         if (part) {
           // the previous split-K GEMM's partials: summed in split (= k) order, then
           // added to the residual -- the same fp32 operations its own epilogue did
-          float4 acc = __ldcg(reinterpret_cast<const float4*>(part + (size_t)m * d) + i);
-          for (int sp = 1; sp < nsplit; ++sp) {
-            const float4 q = __ldcg(reinterpret_cast<const float4*>(part + sp * part_stride + (size_t)m * d) + i);
-            acc.x += q.x;
-            acc.y += q.y;
-            acc.z += q.z;
-            acc.w += q.w;
-          }
+          // (up to 4 splits, all loads in flight before the adds)
+          float4 q[4];
+#pragma unroll
+          for (int sp = 0; sp < 4; ++sp)
+            q[sp] = sp < nsplit ? __ldcg(reinterpret_cast<const float4*>(part + sp * part_stride + (size_t)m * d) + i)
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+          float4 acc = q[0];
+#pragma unroll
+          for (int sp = 1; sp < 4; ++sp)
+            if (sp < nsplit) {
+              acc.x += q[sp].x;
+              acc.y += q[sp].y;
+              acc.z += q[sp].z;
+              acc.w += q[sp].w;
+            }
           v[k].x += acc.x;
           v[k].y += acc.y;
           v[k].z += acc.z;
