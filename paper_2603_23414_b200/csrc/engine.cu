@@ -506,8 +506,8 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
   if ((size_t)S_o * M * d > e->norm_part_floats || S_o > 4) S_o = 1;  // rmsnorm sums <= 4 splits
   if ((size_t)S_d * M * d > e->norm_part_floats || S_d > 4) S_d = 1;
   // the QKV projection can likewise leave its partials to qkv_finish (bias, RoPE, KV
-  // append) -- opt-in (SRL_QKV_FINISH=1): measured r01 slower (QKV 1.10 -> 1.34 ms per
-  // step): the one-CTA-per-row finish is latency-bound on the partial reads
+  // append) -- opt-in (SRL_QKV_FINISH=1): measured r01 even with the in-GEMM reduction
+  // (QKV class -0.02 ms, attention +0.1 ms per step)
   static const bool qkv_part_on = getenv("SRL_QKV_FINISH") != nullptr;
   int S_q = qkv_part_on ? gemm_partial_split(M, Nqkv, d, e->num_sms) : 1;
   if ((size_t)S_q * M * Nqkv > e->qkv_part_floats) S_q = 1;

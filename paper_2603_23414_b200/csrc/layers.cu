@@ -129,24 +129,47 @@ __global__ void __launch_bounds__(256) qkv_finish_kernel(QkvFinishArgs a) {
   if (pos < 0) return;
   const int half = a.dh / 2, H = a.Hq + 2 * a.Hkv, N = H * a.dh;
   const int page = a.page_table[(size_t)a.row_slot[m] * a.max_pages + pos / 64];
-  for (int t = threadIdx.x; t < H * half; t += blockDim.x) {
-    const int h = t / half, i = t % half;
+  const int quads = half / 4;  // 4 consecutive rotary pairs per thread step (vector loads)
+  for (int t = threadIdx.x; t < H * quads; t += blockDim.x) {
+    const int h = t / quads, i = (t % quads) * 4;
     const int n0 = h * a.dh + i, n1 = n0 + half;
-    float x0 = 0.f, x1 = 0.f;
-    for (int sp = 0; sp < a.nsplit; ++sp) {
-      const float* p = a.part + sp * a.part_stride + (size_t)m * N;
-      x0 += __ldcg(p + n0);
-      x1 += __ldcg(p + n1);
+    float4 q0[4], q1[4];
+#pragma unroll
+    for (int sp = 0; sp < 4; ++sp) {  // <= 4 splits, every load in flight before the adds
+      const float* pp = a.part + sp * a.part_stride + (size_t)m * N;
+      q0[sp] = sp < a.nsplit ? __ldcg(reinterpret_cast<const float4*>(pp + n0)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      q1[sp] = sp < a.nsplit ? __ldcg(reinterpret_cast<const float4*>(pp + n1)) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    float x0[4] = {q0[0].x, q0[0].y, q0[0].z, q0[0].w}, x1[4] = {q1[0].x, q1[0].y, q1[0].z, q1[0].w};
+#pragma unroll
+    for (int sp = 1; sp < 4; ++sp)
+      if (sp < a.nsplit) {
+        x0[0] += q0[sp].x; x0[1] += q0[sp].y; x0[2] += q0[sp].z; x0[3] += q0[sp].w;
+        x1[0] += q1[sp].x; x1[1] += q1[sp].y; x1[2] += q1[sp].z; x1[3] += q1[sp].w;
+      }
     if (a.bias) {
-      x0 += __bfloat162float(a.bias[n0]);
-      x1 += __bfloat162float(a.bias[n1]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        x0[k] += __bfloat162float(a.bias[n0 + k]);
+        x1[k] += __bfloat162float(a.bias[n1 + k]);
+      }
     }
-    float y0 = x0, y1 = x1;
+    float y0[4], y1[4];
     if (h < a.Hq + a.Hkv) {
-      const float c = a.rope_cos[(size_t)pos * half + i], s = a.rope_sin[(size_t)pos * half + i];
-      y0 = x0 * c - x1 * s;
-      y1 = x1 * c + x0 * s;
+      const float4 c = __ldg(reinterpret_cast<const float4*>(a.rope_cos + (size_t)pos * half + i));
+      const float4 sn = __ldg(reinterpret_cast<const float4*>(a.rope_sin + (size_t)pos * half + i));
+      const float cc[4] = {c.x, c.y, c.z, c.w}, ss[4] = {sn.x, sn.y, sn.z, sn.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        y0[k] = x0[k] * cc[k] - x1[k] * ss[k];
+        y1[k] = x1[k] * cc[k] + x0[k] * ss[k];
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        y0[k] = x0[k];
+        y1[k] = x1[k];
+      }
     }
     size_t off;
     void* base;
@@ -159,11 +182,13 @@ __global__ void __launch_bounds__(256) qkv_finish_kernel(QkvFinishArgs a) {
       base = h < a.Hq + a.Hkv ? a.k_pool : a.v_pool;
     }
     if (a.kv_f32) {
-      reinterpret_cast<float*>(base)[off + i] = y0;
-      reinterpret_cast<float*>(base)[off + i + half] = y1;
+      float* b = reinterpret_cast<float*>(base) + off;
+      *reinterpret_cast<float4*>(b + i) = make_float4(y0[0], y0[1], y0[2], y0[3]);
+      *reinterpret_cast<float4*>(b + i + half) = make_float4(y1[0], y1[1], y1[2], y1[3]);
     } else {
-      reinterpret_cast<__nv_bfloat16*>(base)[off + i] = __float2bfloat16(y0);
-      reinterpret_cast<__nv_bfloat16*>(base)[off + i + half] = __float2bfloat16(y1);
+      __nv_bfloat16* b = reinterpret_cast<__nv_bfloat16*>(base) + off;
+      *reinterpret_cast<uint2*>(b + i) = make_uint2(pack_bf16(y0[0], y0[1]), pack_bf16(y0[2], y0[3]));
+      *reinterpret_cast<uint2*>(b + i + half) = make_uint2(pack_bf16(y1[0], y1[1]), pack_bf16(y1[2], y1[3]));
     }
   }
 }
