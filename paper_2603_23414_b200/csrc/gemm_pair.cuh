@@ -80,30 +80,34 @@ SRL_DEV void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
 __device__ __forceinline__ long long sk_bound(const GemmParams& p, int q) {
   return (long long)q * p.sk_total / p.sk_pairs;
 }
-// piece i of pair `pid` (unit, k0, k1); *n = piece count when i < 0
+// piece i of pair `pid` (unit, k0, k1); *n = piece count when i < 0.  Stream-K
+// pieces of the remainder units first, then (hybrid) the pair's whole units.
 __device__ __forceinline__ Seg sk_piece(const GemmParams& p, int pid, int i, int* n = nullptr) {
   long long g = sk_bound(p, pid);
   const long long e = sk_bound(p, pid + 1);
   Seg sg{0, 0, 0};
   int j = 0;
   while (g < e) {
-    sg.u = (int)(g / p.kb);
-    sg.k0 = (int)(g - (long long)sg.u * p.kb);
+    const int r = (int)(g / p.kb);
+    sg.u = p.sk_unit0 + r;
+    sg.k0 = (int)(g - (long long)r * p.kb);
     sg.k1 = (int)min((long long)p.kb, sg.k0 + (e - g));
     if (j == i) return sg;
     g += sg.k1 - sg.k0;
     ++j;
   }
+  for (int f = 0; f < p.sk_full; ++f, ++j)
+    if (j == i) return Seg{pid + f * p.sk_pairs, 0, p.kb};
   if (n) *n = j;
   return sg;
 }
 // workspace slot of pair q's piece of unit u: 2q for its first piece, 2q + 1 for a later one
 __device__ __forceinline__ int sk_slot(const GemmParams& p, int q, int u) {
-  return 2 * q + (sk_bound(p, q) >= (long long)u * p.kb ? 0 : 1);
+  return 2 * q + (sk_bound(p, q) >= (long long)(u - p.sk_unit0) * p.kb ? 0 : 1);
 }
 // pairs whose ranges intersect unit u: [*q0, *q1]
 __device__ __forceinline__ void sk_unit_pairs(const GemmParams& p, int u, int* q0, int* q1) {
-  const long long a = (long long)u * p.kb, b = a + p.kb - 1;
+  const long long a = (long long)(u - p.sk_unit0) * p.kb, b = a + p.kb - 1;
   int q = (int)(a * p.sk_pairs / p.sk_total);
   while (q > 0 && sk_bound(p, q) > a) --q;
   while (q + 1 < p.sk_pairs && sk_bound(p, q + 1) <= a) ++q;

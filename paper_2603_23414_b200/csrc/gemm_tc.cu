@@ -60,8 +60,10 @@ struct GemmParams {
   // stream-K (pair kernel, SPLIT == 2): partial slots, per-(unit, row half) arrival counters
   float* sk_ws;
   int* sk_cnt;
-  long long sk_total;  // units * kb
+  long long sk_total;  // k-blocks of the stream-K space: (units - sk_unit0) * kb
   int sk_pairs;
+  int sk_unit0;        // hybrid: units [0, sk_unit0) are whole, sk_full of them per pair, done AFTER
+  int sk_full;         //         each pair's stream-K pieces of the remainder units (so their fix-ups overlap)
 };
 
 static constexpr int kStageA = 128 * 128;  // 128 weight rows x 64 bf16 (128 B)
@@ -517,7 +519,11 @@ static int gemm_pair_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W
   p.units = p.n_tiles * p.m_blocks;
   p.epi = epi;
   p.dbg = (!plan_s && g_dbg && g_dbg_count++ == g_dbg_target) ? g_dbg : nullptr;
-  const bool sk = mode == 2 && epi.ws && p.units % pairs != 0 && p.units <= kSkMaxUnits;
+  // hybrid stream-K (mode 3): whole units round-robin plus the remainder units cut into
+  // equal stream-K ranges, pieces first -- balances e.g. gate/up's 112 units on 74 pairs
+  const bool hyb = mode == 3 && epi.ws && p.units > pairs && p.units % pairs != 0 && p.units < 4 * pairs &&
+                   p.units <= kSkMaxUnits;
+  const bool sk = (mode == 2 && epi.ws && p.units % pairs != 0 && p.units <= kSkMaxUnits) || hyb;
   int S = 1;
   if (!sk && !bsplit && p.units < pairs) {
     S = pairs / p.units;
@@ -527,8 +533,10 @@ static int gemm_pair_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W
   }
   p.S = S;
   if (sk) {
-    p.sk_total = (long long)p.units * p.kb;
-    p.sk_pairs = (int)(p.sk_total < pairs ? p.sk_total : pairs);
+    p.sk_full = hyb ? p.units / pairs : 0;
+    p.sk_unit0 = p.sk_full * pairs;
+    p.sk_total = (long long)(p.units - p.sk_unit0) * p.kb;
+    p.sk_pairs = hyb ? pairs : (int)(p.sk_total < pairs ? p.sk_total : pairs);
     p.sk_ws = reinterpret_cast<float*>(epi.ws);
     p.sk_cnt = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(epi.ws) + (size_t)num_sms * 2 * kSkSlotBytes);
   }
