@@ -411,6 +411,15 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
           uint8_t* vb = kb + C::kBlockBytes;
           hdr[s] = it;  // published by the arrive below (release), read after the consumers' wait
           mbar_arrive_expect_tx(&full[s], C::kStageBytes);
+          if (a.l2_prefetch > 0 && p + a.l2_prefetch < ii.p1) {  // more HBM requests in flight
+            const int page2 = a.page_table[(size_t)ii.slot * a.max_pages + p + a.l2_prefetch];
+            const int row2 = (page2 * a.Hkv + ii.kvh) * 64;
+#pragma unroll
+            for (int b = 0; b < C::kBoxes; ++b) {
+              tma_prefetch_l2_2d(&tmK, b * C::kBoxCols, row2);
+              tma_prefetch_l2_2d(&tmV, b * C::kBoxCols, row2);
+            }
+          }
 #pragma unroll
           for (int b = 0; b < C::kBoxes; ++b) {
             tma_load_2d_hint(kb + b * C::kBoxBytes, &tmK, &full[s], b * C::kBoxCols, row, pol);
@@ -652,8 +661,13 @@ void attn_plan(const AttnArgs& a, int split, cudaStream_t st) {
   launch_k(attn_plan_kernel, dim3(1), dim3(1024), 0, st, 1, a, split, mi, ti);
 }
 
-void attn_run(const AttnArgs& a, bool kv_fp32, const void* tmap_k, const void* tmap_v, cudaStream_t st) {
-  if (a.M <= 0) return;
+void attn_run(const AttnArgs& a_in, bool kv_fp32, const void* tmap_k, const void* tmap_v, cudaStream_t st) {
+  if (a_in.M <= 0) return;
+  // SRL_ATTN_L2PF=<pages>: L2 prefetch beyond the ring -- measured r01 slower at every
+  // distance tried (2/4/8 pages: -3..-10 %), so off
+  static const int pf = getenv("SRL_ATTN_L2PF") ? atoi(getenv("SRL_ATTN_L2PF")) : 0;
+  AttnArgs a = a_in;
+  a.l2_prefetch = pf;
   if (kv_fp32) {
     const int G = a.Hq / a.Hkv;
     const size_t smem = (size_t)G * a.dh * 4 + (size_t)G * 64 * kChunkPages * 4;

@@ -63,6 +63,7 @@ struct AttnArgs {
   int n_ctr;
   int* merge_ctr;        // [M * Hkv] split-KV chunk arrivals (zeroed by the plan kernel, reset by the merger)
   int* chunk_pages;      // device int: split-KV chunk size in pages, chosen by the plan kernel
+  int l2_prefetch;       // bf16 kernel: pages of L2 prefetch beyond the smem ring (0 = none)
 };
 void attn_plan(const AttnArgs& a, int split, cudaStream_t st);
 void attn_run(const AttnArgs& a, bool kv_fp32, const void* tmap_k, const void* tmap_v, cudaStream_t st);
