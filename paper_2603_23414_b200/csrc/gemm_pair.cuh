@@ -147,7 +147,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int npairs = gridDim.x >> 1;
   const int pid = blockIdx.x >> 1;
   const int cl = SPLIT == 1 ? (int)(blockIdx.x / (2 * p.S)) : 0;
-  const int pi = SPLIT == 1 ? (int)(rank >> 1) : 0;
+  // split index: the pair's rank in its (2S)-CTA cluster, or (EPI_PARTIAL, clusters of
+  // one pair) its position among the unit's S consecutive pairs
+  const int pi = SPLIT == 1 ? (p.split_pairs ? (int)((blockIdx.x >> 1) % p.S) : (int)(rank >> 1)) : 0;
   int nseg;
   if (SPLIT == 1) nseg = 1;
   else if (SPLIT == 2) sk_piece(p, pid, -1, &nseg);

@@ -51,6 +51,7 @@ struct GemmParams {
   int m_blk, m_blocks, n_tiles, kb, units;
   int H;   // 128-row halves per weight tile (1 or 2): both multiply one activation slice
   int S;   // cluster split-K factor (1 = persistent whole-unit mode)
+  int split_pairs;  // EPI_PARTIAL: the S splits of a unit are S independent CTA pairs (cluster of 2)
   int w_shared;  // pair kernel: several batch blocks stream the same weight tile (keep it in L2)
   int hp;  // SPLIT: tile halves reduced per DSMEM phase (what fits in the idle rings)
   int stages, xstages, tmem_cols, acc_stages;
@@ -525,13 +526,17 @@ static int gemm_pair_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W
                    p.units <= kSkMaxUnits;
   const bool sk = (mode == 2 && epi.ws && p.units % pairs != 0 && p.units <= kSkMaxUnits) || hyb;
   int S = 1;
+  // EPI_PARTIAL needs no exchange between the splits: they run as independent CTA
+  // pairs, so S is not limited by how many (2S)-CTA clusters can be co-resident
+  const bool part = epi.kind == EPI_PARTIAL;
   if (!sk && !bsplit && p.units < pairs) {
     S = pairs / p.units;
     if (S > 4) S = 4;
     if (S > p.kb) S = p.kb;
-    while (S > 1 && p.units > max_clusters_pair(2 * S)) --S;
+    while (!part && S > 1 && p.units > max_clusters_pair(2 * S)) --S;
   }
   p.S = S;
+  p.split_pairs = part && S > 1;
   if (sk) {
     p.sk_full = hyb ? p.units / pairs : 0;
     p.sk_unit0 = p.sk_full * pairs;
@@ -548,7 +553,7 @@ static int gemm_pair_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W
   p.stages = stages;
   p.xstages = xstages;
   const size_t rings = (size_t)stages * kStageA + (size_t)xstages * stage_b;
-  if (S > 1) {
+  if (S > 1 && !part) {
     const int cpr = ((p.m_blk >> 4) + S - 1) / S;
     if ((size_t)S * cpr * 8192 > rings) return 1;
   }
@@ -590,7 +595,7 @@ static int gemm_pair_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W
     const int np = p.units < pairs ? p.units : pairs;
     rc = launch_cluster(gemm_pair_kernel<0>, 2 * np, 2, smem, stream, tmW, tmX, p);
   } else {
-    rc = launch_cluster(gemm_pair_kernel<1>, p.units * 2 * S, 2 * S, smem, stream, tmW, tmX, p);
+    rc = launch_cluster(gemm_pair_kernel<1>, p.units * 2 * S, p.split_pairs ? 2 : 2 * S, smem, stream, tmW, tmX, p);
   }
   if (rc) cudaGetLastError();
   return rc;
@@ -602,7 +607,7 @@ int gemm_partial_split(int M, int N, int K, int num_sms) {
   const bool pair = pair_env >= 0 ? pair_env > 0 : M >= 128;
   if (off || !pair || M <= 0 || K % 64) return 1;
   GemmEpi e{};
-  e.kind = EPI_RESID;
+  e.kind = EPI_PARTIAL;
   e.w_packed = 1;
   int S = 1;
   if (gemm_pair_fused(nullptr, M, nullptr, N, K, e, num_sms, nullptr, &S) != 0) return 1;
