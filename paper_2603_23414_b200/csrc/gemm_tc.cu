@@ -339,7 +339,34 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   }
 
-  if (SPLIT) {
+  if (SPLIT && p.epi.kind == EPI_PARTIAL) {
+    // ------------------------------ split k-range r's fp32 partial -> part[r] for the next
+    // RMSNorm (independent CTAs: no exchange, no cluster barriers)
+    const Seg sg = seg_at<SPLIT>(p, 0);
+    const int t = sg.u % p.n_tiles, m_base = (sg.u / p.n_tiles) * p.m_blk;
+    const int ncol = unit_cols(p, sg.u), nh = halves_valid(p, sg.u), nchunk = ncol >> 4;
+    const int pi = blockIdx.x % p.S;
+    if (w >= 2 && w <= 9) {
+      const int qw = w & 3, n = qw * 32 + lane, eg = (w - 2) >> 2;
+      mbar_wait(&tfull[0], 0);
+      tc_fence_after();
+      for (int h = 0; h < nh; ++h) {
+        const int unit_n0 = (t * p.H + h) * 128;
+        const uint32_t tl = tbase + ((uint32_t)(qw * 32) << 16) + (uint32_t)(h * p.m_blk);
+        float* dst = p.epi.part + (size_t)pi * p.epi.part_stride + unit_n0 + n;
+        const bool rok = unit_n0 + n < p.N;
+        for (int c = eg; c < nchunk; c += 2) {
+          float v[16];
+          tmem_ld16(tl + (uint32_t)(c * 16), v);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int m = m_base + c * 16 + j;
+            if (rok && m < p.M) dst[(size_t)m * p.epi.ldo] = v[j];
+          }
+        }
+      }
+    }
+  } else if (SPLIT) {
     // ------------------------------ cluster split-K reduction over DSMEM
     // Phase = the weight-tile halves whose partials fit in the (now idle) rings at once.
     const Seg sg = seg_at<SPLIT>(p, 0);
@@ -476,6 +503,15 @@ static int launch_cluster(void (*kern)(const CUtensorMap, const CUtensorMap, Gem
 }
 
 // CTA-pair variant (gemm_pair.cuh) for wide batches; returns 1 when not applicable
+// split factor of the single-CTA kernel's partial mode (1: it would not split)
+static int single_partial_split(int units, int kb, int num_sms) {
+  if (units >= num_sms) return 1;
+  int S = num_sms / units;
+  if (S > 4) S = 4;
+  if (S > kb) S = kb;
+  return S;
+}
+
 size_t gemm_workspace_bytes(int num_sms) {
   return (size_t)num_sms * 2 * kSkSlotBytes + (size_t)kSkMaxUnits * 2 * sizeof(int);
 }
@@ -605,7 +641,15 @@ int gemm_partial_split(int M, int N, int K, int num_sms) {
   static const int pair_env = getenv("SRL_GEMM_PAIR") ? atoi(getenv("SRL_GEMM_PAIR")) : -1;
   static const bool off = getenv("SRL_NO_PARTIAL_NORM") != nullptr;
   const bool pair = pair_env >= 0 ? pair_env > 0 : M >= 128;
-  if (off || !pair || M <= 0 || K % 64) return 1;
+  if (off || M <= 0 || K % 64) return 1;
+  if (!pair) {  // single-CTA kernel (H = 1 in partial mode) -- opt-in, SRL_PARTIAL_SMALL_M=1:
+    // measured r01 neutral on the 32B slice (O / down -0.37 ms, the norms +0.25 ms per step)
+    static const bool small_on = getenv("SRL_PARTIAL_SMALL_M") != nullptr;
+    if (!small_on) return 1;
+    const int m_blk = pick_mblk(M);
+    const int units = (N + 127) / 128 * ((M + m_blk - 1) / m_blk);
+    return single_partial_split(units, K / 64, num_sms);
+  }
   GemmEpi e{};
   e.kind = EPI_PARTIAL;
   e.w_packed = 1;
@@ -656,13 +700,16 @@ int gemm_bf16_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N
   static const int h_env = getenv("SRL_GEMM_H") ? atoi(getenv("SRL_GEMM_H")) : 0;
   // packed weights pad rows to 128 only: H = 2 needs an even number of 128-row tiles
   const bool h2_ok = !(epi.w_packed && ((N + 127) / 128) % 2);
+  const bool part = epi.kind == EPI_PARTIAL;
   p.H = h_env ? h_env : ((h2_ok && util(2) > util(1) + 0.02) ? 2 : 1);
-  if (!h2_ok) p.H = 1;
+  if (!h2_ok || part) p.H = 1;
   p.n_tiles = (N + 128 * p.H - 1) / (128 * p.H);
   p.units = p.n_tiles * p.m_blocks;
   p.epi = epi;
   p.dbg = (g_dbg && g_dbg_count++ == g_dbg_target) ? g_dbg : nullptr;
-  const int S = pick_s(p.units);
+  // EPI_PARTIAL: the splits are independent CTAs (no cluster), <= 4 (what the RMSNorm sums)
+  const int S = part ? single_partial_split(p.units, p.kb, num_sms) : pick_s(p.units);
+  if (part && S < 2) return -1;  // caller must ask gemm_partial_split
   p.S = S;
   // smem: a short ring of activation k-slices and a deep ring of weight k-slices
   const int stage_a = p.H * kStageA;
@@ -724,7 +771,7 @@ int gemm_bf16_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N
       fprintf(stderr, "gemm M=%d N=%d K=%d H=%d units=%d S=%d hp=%d stages=%d smem=%zu max_active_clusters=%d\n", M,
               N, K, p.H, p.units, S, p.hp, stages, smem, ncl);
     }
-    launch_k(gemm_bf16_tc_kernel<1>, dim3(p.units * S), dim3(kGemmThreads), smem, stream, S, tmW, tmX, p);
+    launch_k(gemm_bf16_tc_kernel<1>, dim3(p.units * S), dim3(kGemmThreads), smem, stream, part ? 1 : S, tmW, tmX, p);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : -3;
 }
