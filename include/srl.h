@@ -288,6 +288,37 @@ int32_t srl_nccl_unique_id(uint8_t* out128);
 int32_t srl_local_group_create(int32_t world, void** out);
 int32_t srl_local_group_destroy(void* group);
 
+/* Kernel-selection settings, process-wide (all engines and op calls of the
+ * process).  The defaults (srl_default_tuning) are the production choices; the
+ * alternatives are kept selectable for measurement and for their parity tests
+ * (DESIGN.md §7 gives each one's measured cost).  Nothing in the library reads
+ * the environment.  Settings are read when a launch is planned:
+ * an engine's captured decode graphs keep the settings they were captured
+ * with, and `graphs` / `mixed_prefill` are read by srl_create -- so set them
+ * before creating engines.  srl_set_tuning returns -1 (srl_last_error) for an
+ * out-of-range field and changes nothing then. */
+typedef struct srl_tuning {
+  int32_t gemm_split;      /* decomposition when whole pair units leave SM pairs idle: 1 cluster split-K
+                              (default), 0 batch split, 2 stream-K with L2 fix-up, 3 hybrid stream-K */
+  int32_t gemm_pair;       /* -1 auto (CTA-pair tcgen05 kernel for M >= 128), 0 never, 1 always */
+  int32_t gemm_h;          /* single-CTA kernel 128-row halves per tile: 0 auto, 1, 2 */
+  int32_t gemm_stages;     /* weight ring depth cap (0 = auto) */
+  int32_t gemm_xstages;    /* activation ring depth (0 = auto) */
+  int32_t partial_norm;    /* 1: O / down split-K partials summed (in split order) by the next RMSNorm */
+  int32_t partial_small_m; /* 1: the same for the single-CTA kernel (M < 128) */
+  int32_t qkv_finish;      /* 1: QKV split-K partials + a bias/RoPE/KV-append kernel */
+  int32_t fused_sample;    /* 1: Gumbel-max sampling fused into the LM head epilogue */
+  int32_t attn_min_items, attn_target_items; /* split-KV planning (0 = built-in) */
+  int32_t attn_l2_prefetch; /* pages of L2 prefetch beyond the attention TMA ring (0..16) */
+  int32_t pdl;             /* 1: programmatic dependent launch across the decode chain */
+  int32_t graphs;          /* 1: replay the decode tail from CUDA graphs */
+  int32_t mixed_prefill;   /* 1: admitted prompts ride in the decode pass when they fit one chunk */
+  int32_t verbose;         /* 1: print GEMM plans to stderr */
+} srl_tuning;
+void srl_default_tuning(srl_tuning* t);
+int32_t srl_get_tuning(srl_tuning* t);
+int32_t srl_set_tuning(const srl_tuning* t);
+
 const char* srl_last_error(void);
 
 #ifdef __cplusplus

@@ -8,6 +8,17 @@ SURVEY §8(c) O-S fixes this algorithm for the Gumbel noise g = -LOG(-LOG(u))
 so that CPU and GPU samplers agree bit for bit; numpy float32 element-wise
 operations are single IEEE operations, so this vectorised transcription
 rounds exactly like the scalar C code evaluated left to right.
+
+The algorithm follows FreeBSD msun e_logf.c, which carries this notice:
+  Conversion to float by Ian Lance Taylor, Cygnus Support, ian@cygnus.com.
+  ====================================================
+  Copyright (C) 1993 by Sun Microsystems, Inc. All rights reserved.
+
+  Developed at SunPro, a Sun Microsystems, Inc. business.
+  Permission to use, copy, modify, and distribute this
+  software is freely granted, provided that this notice
+  is preserved.
+  ====================================================
 """
 from __future__ import annotations
 

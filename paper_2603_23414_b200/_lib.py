@@ -62,6 +62,14 @@ class TraceRec(C.Structure):
     _fields_ = [("kind", _I32), ("a", _I32), ("b", _I32), ("c", _I32), ("d", _I32), ("e", _I32)]
 
 
+class Tuning(C.Structure):
+    """srl.h srl_tuning: process-wide kernel selection (defaults = production)."""
+    _fields_ = [(n, _I32) for n in ("gemm_split", "gemm_pair", "gemm_h", "gemm_stages", "gemm_xstages",
+                                    "partial_norm", "partial_small_m", "qkv_finish", "fused_sample",
+                                    "attn_min_items", "attn_target_items", "attn_l2_prefetch", "pdl", "graphs",
+                                    "mixed_prefill", "verbose")]
+
+
 _MP, _SP, _AP, _CP = C.POINTER(ModelCfg), C.POINTER(SchedCfg), C.POINTER(Arena), C.POINTER(Comm)
 _U64P, _I64P, _I32P = C.POINTER(_U64), C.POINTER(_I64), C.POINTER(_I32)
 
@@ -95,6 +103,9 @@ SIGNATURES = {
     "srl_load_policy_tensor": (_I32, [_P, C.c_char_p, _P]),
     "srl_local_group_create": (_I32, [_I32, C.POINTER(_P)]),
     "srl_local_group_destroy": (_I32, [_P]),
+    "srl_default_tuning": (None, [C.POINTER(Tuning)]),
+    "srl_get_tuning": (_I32, [C.POINTER(Tuning)]),
+    "srl_set_tuning": (_I32, [C.POINTER(Tuning)]),
 }
 
 GEMM_W_PACKED = 0x100   # srl_ops.h SRL_GEMM_W_PACKED
@@ -127,3 +138,28 @@ def check(rc: int, what: str) -> int:
     if rc < 0:
         raise SRLError(f"{what} failed ({rc}): {load().srl_last_error().decode()}")
     return rc
+
+
+def get_tuning() -> dict:
+    t = Tuning()
+    check(load().srl_get_tuning(C.byref(t)), "srl_get_tuning")
+    return {n: getattr(t, n) for n, _ in Tuning._fields_}
+
+
+def set_tuning(**fields) -> dict:
+    """Change some srl_tuning fields (the rest keep their values); returns the
+    previous settings, so `set_tuning(**old)` restores them.  defaults=True first
+    resets every field to srl_default_tuning."""
+    lib = load()
+    old = get_tuning()
+    t = Tuning()
+    if fields.pop("defaults", False):
+        lib.srl_default_tuning(C.byref(t))
+    else:
+        check(lib.srl_get_tuning(C.byref(t)), "srl_get_tuning")
+    for k, v in fields.items():
+        if k not in old:
+            raise KeyError(f"unknown srl_tuning field {k}")
+        setattr(t, k, int(v))
+    check(lib.srl_set_tuning(C.byref(t)), "srl_set_tuning")
+    return old

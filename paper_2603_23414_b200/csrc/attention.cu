@@ -642,11 +642,8 @@ template <int DH>
 static void launch_bf16(const AttnArgs& a, const void* tk, const void* tv, cudaStream_t st) {
   using C = AttnCfg<DH>;
   const size_t smem = 1024 + kStages * C::kStageBytes + kConsumerWarps * 8 * (DH + 2) * 4 + 2 * kStages * 8 + 64;
-  static bool set = false;
-  if (!set) {
+  if (once_per_device(DH == 128 ? kOnceAttn128 : (DH == 64 ? kOnceAttn64 : kOnceAttn32)))  // per-device attribute
     cudaFuncSetAttribute(attn_bf16_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    set = true;
-  }
   int grid = 148;
   const int occ = (int)((228 * 1024) / (smem + 1024));
   grid *= occ < 1 ? 1 : occ;
@@ -655,17 +652,17 @@ static void launch_bf16(const AttnArgs& a, const void* tk, const void* tv, cudaS
 }
 
 void attn_plan(const AttnArgs& a, int split, cudaStream_t st) {
-  // experiment knobs (timing only): SRL_ATTN_MIN_ITEMS, SRL_ATTN_TARGET_ITEMS
-  static const int mi = getenv("SRL_ATTN_MIN_ITEMS") ? atoi(getenv("SRL_ATTN_MIN_ITEMS")) : kMinItems;
-  static const int ti = getenv("SRL_ATTN_TARGET_ITEMS") ? atoi(getenv("SRL_ATTN_TARGET_ITEMS")) : kTargetItems;
+  // split-KV planning (srl_tuning; 0 = the built-in values)
+  const int mi = tuning().attn_min_items ? tuning().attn_min_items : kMinItems;
+  const int ti = tuning().attn_target_items ? tuning().attn_target_items : kTargetItems;
   launch_k(attn_plan_kernel, dim3(1), dim3(1024), 0, st, 1, a, split, mi, ti);
 }
 
 void attn_run(const AttnArgs& a_in, bool kv_fp32, const void* tmap_k, const void* tmap_v, cudaStream_t st) {
   if (a_in.M <= 0) return;
-  // SRL_ATTN_L2PF=<pages>: L2 prefetch beyond the ring -- measured r01 slower at every
-  // distance tried (2/4/8 pages: -3..-10 %), so off
-  static const int pf = getenv("SRL_ATTN_L2PF") ? atoi(getenv("SRL_ATTN_L2PF")) : 0;
+  // srl_tuning.attn_l2_prefetch = <pages>: L2 prefetch beyond the ring -- measured r01
+  // slower at every distance tried (2/4/8 pages: -3..-10 %), so off
+  const int pf = tuning().attn_l2_prefetch;
   AttnArgs a = a_in;
   a.l2_prefetch = pf;
   if (kv_fp32) {

@@ -40,13 +40,9 @@ const Api& api() {
   static Api a;
   static std::once_flag once;
   std::call_once(once, [] {
-    // prefer the libnccl already mapped into the process (torch's), then an
-    // explicit path, then the loader's search path
+    // prefer the libnccl already mapped into the process (torch's), then the
+    // loader's search path
     void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
-    if (!h) {
-      const char* p = getenv("SRL_NCCL_LIB");
-      if (p) h = dlopen(p, RTLD_NOW | RTLD_GLOBAL);
-    }
     if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) {
       a.why = std::string("dlopen(libnccl.so.2) failed: ") + dlerror();

@@ -193,8 +193,10 @@ __device__ void maybe_load(const Ctl& c) {  // thread 0
   s->loaded += n;
 }
 
-// Early termination / selective batching (all threads).  Returns true if a group was emitted.
-__device__ bool emission_check(const Ctl& c, long long* keys) {
+// Early termination / selective batching (all threads).  Returns 1 if a group was
+// emitted, 0 if not, -1 if the ready list outgrew the sort buffer (SRL_E_CAPACITY;
+// validate() rules this out for every accepted configuration).
+__device__ int emission_check(const Ctl& c, long long* keys) {
   CtlState* s = c.s;
   __shared__ int sh_flag, sh_final, sh_n;
   int occ = 0;
@@ -225,8 +227,9 @@ __device__ bool emission_check(const Ctl& c, long long* keys) {
   }
   __syncthreads();
   const int flag = sh_flag, n = sh_n;
-  if (!flag) return false;
+  if (!flag) return 0;
   const int nr = s->n_ready;
+  if (flag == 2 && nr > kMaxSortReady) return -1;  // uniform: every thread reads the same n_ready
   if (flag == 1) {  // SYNC: completion order, no sorting
     for (int i = threadIdx.x; i < n; i += blockDim.x) c.group[i] = c.ready[i];
     __syncthreads();
@@ -264,7 +267,7 @@ __device__ bool emission_check(const Ctl& c, long long* keys) {
     s->n_groups++;
   }
   __syncthreads();
-  return true;
+  return 1;
 }
 
 __device__ void fill_status(const Ctl& c, int status) {
@@ -302,8 +305,8 @@ __global__ void __launch_bounds__(kCtlThreads, 1) ctl_begin_kernel(Ctl c) {
   __syncthreads();
   if (sh_stop) return;
   // 0 pre: emission check (leftover ready >= U after an update / SYNC next group)
-  if (emission_check(c, keys)) {
-    if (threadIdx.x == 0) fill_status(c, SRL_GROUP_READY);
+  if (const int em = emission_check(c, keys)) {
+    if (threadIdx.x == 0) fill_status(c, em > 0 ? SRL_GROUP_READY : SRL_E_CAPACITY);
     return;
   }
   // 1 load
@@ -583,8 +586,8 @@ __global__ void __launch_bounds__(kCtlThreads, 1) ctl_end_kernel(Ctl c) {
     s->k++;
   }
   __syncthreads();
-  const bool emitted = emission_check(c, keys);
-  if (threadIdx.x == 0) fill_status(c, emitted ? SRL_GROUP_READY : SRL_OK);
+  const int em = emission_check(c, keys);
+  if (threadIdx.x == 0) fill_status(c, em > 0 ? SRL_GROUP_READY : (em < 0 ? SRL_E_CAPACITY : SRL_OK));
 }
 
 // ------------------------------------------------------------------ BUMP (load_policy_weights)
@@ -744,7 +747,14 @@ __global__ void ctl_submit_kernel(Ctl c, int n_traj, int n_prompts) {
   }
 }
 
-static size_t sort_smem() { return (size_t)kMaxSortReady * sizeof(long long); }
+static size_t sort_smem() {
+  if (once_per_device(kOnceCtl)) {  // > 48 KB of dynamic shared memory: a per-device attribute
+    cudaFuncSetAttribute(ctl_begin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSortReady * 8);
+    cudaFuncSetAttribute(ctl_end_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSortReady * 8);
+    cudaFuncSetAttribute(ctl_bump_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSortReady * 8);
+  }
+  return (size_t)kMaxSortReady * sizeof(long long);
+}
 
 void ctl_begin(const Ctl& c, cudaStream_t st) { ctl_begin_kernel<<<1, kCtlThreads, sort_smem(), st>>>(c); }
 void ctl_end(const Ctl& c, cudaStream_t st) { launch_k(ctl_end_kernel, dim3(1), dim3(kCtlThreads), sort_smem(), st, 1, c); }

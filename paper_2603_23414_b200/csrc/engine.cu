@@ -15,6 +15,7 @@
 #include "kernels.hpp"
 #include "layers.hpp"
 #include "tma.hpp"
+#include "tuning.hpp"
 
 namespace srl {
 extern thread_local std::string g_last_error;
@@ -169,6 +170,13 @@ int validate(const srl_model_cfg* m, const srl_sched_cfg* s, int world, std::str
   if (s->mode < SRL_MODE_SORTED || s->mode > SRL_MODE_POSTHOC) return why = "mode", -1;
   if (s->mode != SRL_MODE_SYNC && s->U > s->pool_prompts * s->G) return why = "U larger than the prompt pool (S:252)", -1;
   if (s->U > kMaxGroup) return why = "U too large", -1;
+  // the emission sort holds the whole ready list in shared memory: before a step it
+  // has < U entries (>= U emits first), a step adds <= Q_tot finishes; POSTHOC keeps
+  // the whole pool until it has finished
+  if (s->mode == SRL_MODE_SORTED && (long long)s->U - 1 + (long long)s->Q_g * world > kMaxSortReady)
+    return why = "U - 1 + Q_tot exceeds the emission sort capacity (16384)", -1;
+  if (s->mode == SRL_MODE_POSTHOC && (long long)s->pool_prompts * s->G + s->U - 1 > kMaxSortReady)
+    return why = "POSTHOC pool_prompts * G exceeds the emission sort capacity (16384)", -1;
   if (s->stop == SRL_STOP_EOS && s->eos_id < 0) return why = "EOS stop needs eos_id", -1;
   if (s->temperature <= 0.f) return why = "temperature must be > 0", -1;
   if (s->max_traj <= 0 || s->max_prompt <= 0 || s->prefill_chunk <= 0) return why = "max_traj, max_prompt, prefill_chunk must be positive", -1;
@@ -272,6 +280,9 @@ struct srl_engine {
   };
   std::map<int, Graph> graphs;
   int last_m = 0;  // decode rows of the last step
+  bool mixed_ok = true;
+  int launch_rc = 0;             // first failed launch of the current step (note_launch)
+  const char* launch_what = "";
 };
 
 namespace {
@@ -419,30 +430,27 @@ size_t kv_bytes_for(const srl_model_cfg& m, const srl_sched_cfg& s) {
   return al((size_t)s.kv_pages * m.Hkv * kPage * m.dh * el) * 2 * m.L;
 }
 
-// Timing ablation (never for results): SRL_DEBUG_SKIP=<hex mask of SRL_K_* classes>
-// drops those launches from the DECODE path, to measure what each class really
-// costs inside the PDL-linked graph (per-class events would cut those links).
-bool debug_skip(int cls) {
-  static const unsigned mask = getenv("SRL_DEBUG_SKIP") ? (unsigned)strtoul(getenv("SRL_DEBUG_SKIP"), nullptr, 16) : 0u;
-  return cls >= 0 && ((mask >> cls) & 1u);
-}
-
-// LM head + sampler fusion (EPI_SAMPLE + sample_reduce), opt-in: SRL_FUSED_SAMPLE=1.
+// LM head + sampler fusion (EPI_SAMPLE + sample_reduce), opt-in (srl_tuning.fused_sample).
 // Measured r01 (cfg2): the Gumbel-max work in the LM head's 8 epilogue warps per SM
 // outlasts the MMAs it should hide behind (LM head 0.21 -> 0.77 ms per step) while
 // the stand-alone sampler, 256 CTAs x 16 warps, costs 0.22 ms -- so it stays off.
-bool fused_sample() {
-  static const bool on = getenv("SRL_FUSED_SAMPLE") != nullptr;
-  return on;
+bool fused_sample() { return tuning().fused_sample != 0; }
+
+// Records the first failed launch of a step (reported by srl_decode_step as
+// SRL_E_CUDA; the launchers clear the non-sticky error they saw).
+void note_launch(srl_engine* e, const char* what, int rc) {
+  if (rc == 0 || e->launch_rc) return;
+  e->launch_rc = rc;
+  e->launch_what = what;
 }
 
 // ---- fused GEMM helper
 // one fused GEMM launch, profiled under `cls`
 void run_gemm(srl_engine* e, int cls, const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N, int K,
               const GemmEpi& epi) {
-  if (debug_skip(cls)) return;
   Prof p(e, cls);
-  gemm_bf16_fused(X, M, W, N, K, epi, e->num_sms, e->st);
+  if (cudaError_t pre = cudaGetLastError()) note_launch(e, "launch before a GEMM", (int)pre);
+  note_launch(e, "GEMM launch", gemm_bf16_fused(X, M, W, N, K, epi, e->num_sms, e->st));
   e->launches++;
 }
 
@@ -473,7 +481,7 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
     Prof p1(e, D + SRL_K_ATTN);
     attn_plan(a, split >= 0 ? split : (decode ? 1 : 0), st);
   }
-  if (!debug_skip(D + SRL_K_ELEMWISE)) {
+  {
     Prof p2(e, D + SRL_K_ELEMWISE);
     rmsnorm(e->x_res, row_tok, row_pos, M, d, e->embed, e->lw[0].attn_norm, m.rms_eps, e->xn, st);
   }
@@ -506,10 +514,9 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
   if ((size_t)S_o * M * d > e->norm_part_floats || S_o > 4) S_o = 1;  // rmsnorm sums <= 4 splits
   if ((size_t)S_d * M * d > e->norm_part_floats || S_d > 4) S_d = 1;
   // the QKV projection can likewise leave its partials to qkv_finish (bias, RoPE, KV
-  // append) -- opt-in (SRL_QKV_FINISH=1): measured r01 even with the in-GEMM reduction
-  // (QKV class -0.02 ms, attention +0.1 ms per step)
-  static const bool qkv_part_on = getenv("SRL_QKV_FINISH") != nullptr;
-  int S_q = qkv_part_on ? gemm_partial_split(M, Nqkv, d, e->num_sms) : 1;
+  // append) -- opt-in (srl_tuning.qkv_finish): measured r01 even with the in-GEMM
+  // reduction (QKV class -0.02 ms, attention +0.1 ms per step)
+  int S_q = tuning().qkv_finish ? gemm_partial_split(M, Nqkv, d, e->num_sms) : 1;
   if ((size_t)S_q * M * Nqkv > e->qkv_part_floats) S_q = 1;
   GemmEpi pq{};
   pq.kind = EPI_PARTIAL;
@@ -536,7 +543,7 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
     qe.v_pool = e->vpool[l];
     if (S_q > 1) {  // split-K partials, then bias + RoPE + KV append in one elementwise pass
       run_gemm(e, D + SRL_K_GEMM_QKV, e->xn, M, (const __nv_bfloat16*)w.pqkv, Nqkv, d, pq);
-      if (!debug_skip(D + SRL_K_GEMM_QKV)) {
+      {
         Prof p(e, D + SRL_K_GEMM_QKV);
         QkvFinishArgs fa{};
         fa.part = e->qkv_part;
@@ -565,19 +572,19 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
     a.k_pool = e->kpool[l];
     a.v_pool = e->vpool[l];
     a.work_ctr = e->attn.work_ctr + l;  // one counter per layer, all zeroed by attn_plan
-    if (!debug_skip(D + SRL_K_ATTN)) {
+    {
       Prof p(e, D + SRL_K_ATTN, 2);
       attn_run(a, e->kv_f32, &e->tmK[l], &e->tmV[l], st);
     }
     run_gemm(e, D + SRL_K_GEMM_O, e->attn_out, M, (const __nv_bfloat16*)w.po, d, qd, S_o > 1 ? pe : re);
-    if (!debug_skip(D + SRL_K_ELEMWISE)) {
+    {
       Prof p(e, D + SRL_K_ELEMWISE);
       rmsnorm(e->x_res, row_tok, row_pos, M, d, nullptr, w.mlp_norm, m.rms_eps, e->xn, st,
               S_o > 1 ? e->norm_part : nullptr, S_o, (size_t)M * d);
     }
     run_gemm(e, D + SRL_K_GEMM_GU, e->xn, M, (const __nv_bfloat16*)w.pgu, 2 * m.ff, d, se);  // interleaved gate/up
     run_gemm(e, D + SRL_K_GEMM_DOWN, e->act, M, (const __nv_bfloat16*)w.pd, d, m.ff, S_d > 1 ? pe : re);
-    if (!debug_skip(D + SRL_K_ELEMWISE)) {
+    {
       Prof p(e, D + SRL_K_ELEMWISE);
       const __nv_bfloat16* next = l + 1 < m.L ? e->lw[l + 1].attn_norm : e->final_norm;
       rmsnorm(e->x_res, row_tok, row_pos, M, d, nullptr, next, m.rms_eps, e->xn, st,
@@ -648,7 +655,7 @@ void decode_tail(srl_engine* e, bool with_end, int M, int M_pre = 0) {
   sa.seed = e->s.sample_seed;
   sa.tok_out = c.samp + (size_t)e->rank * 2 * e->s.Q_g;
   sa.lp_out = (float*)(c.samp + (size_t)e->rank * 2 * e->s.Q_g + e->s.Q_g);
-  if (!debug_skip(SRL_K_SAMPLE)) {
+  {
     Prof p(e, SRL_K_SAMPLE);
     if (fused_sample())
       sample_reduce(sa, e->samp_part, e->samp_part_j, (e->m.V + 127) / 128, st);
@@ -693,6 +700,14 @@ void read_status(srl_engine* e) {
 // end of a decode step: status read-back, profiling, step info
 static int32_t finish_step(srl_engine* e, const CtlStatus& b, srl_step_info* info, srl_engine::EvSet* gset) {
   cudaStream_t st = e->st;
+  if (e->launch_rc) {  // a launch of this step failed: its outputs are stale, say so
+    const int rc = e->launch_rc;
+    e->launch_rc = 0;
+    cudaGetLastError();
+    char buf[160];
+    snprintf(buf, sizeof(buf), "srl_decode_step: %s failed (code %d)", e->launch_what, rc);
+    return fail(SRL_E_CUDA, buf);
+  }
   cudaEventRecord(e->ev1, st);
   read_status(e);
   if (cudaError_t ce = cudaGetLastError()) return cuda_fail("decode step", ce);
@@ -784,7 +799,8 @@ int32_t srl_create(const srl_model_cfg* m, const srl_sched_cfg* s, int32_t devic
   e->st = (cudaStream_t)stream;
   e->kv_f32 = s->kv_dtype == SRL_KV_FP32;
   e->z = compute_sizes(m, s, world);
-  e->use_graph = getenv("SRL_NO_GRAPH") == nullptr && stream != nullptr;  // the legacy stream cannot be captured
+  e->use_graph = tuning().graphs != 0 && stream != nullptr;  // the legacy stream cannot be captured
+  e->mixed_ok = tuning().mixed_prefill != 0;
   if (comm) {
     e->comm = comm->kind == SRL_COMM_NCCL ? comm_create_nccl(comm->nccl_unique_id, comm->rank, world, why)
                                           : comm_create_local(comm->local_group, comm->rank, world, why);
@@ -990,8 +1006,7 @@ int32_t srl_decode_step(srl_engine* e, srl_step_info* info) {
     return b.status;
   }
   const Ctl& c = e->ctl;
-  static const bool mixed_ok = getenv("SRL_NO_MIXED") == nullptr;
-  if (mixed_ok && b.m_pre > 0 && b.m_pre <= e->s.prefill_chunk) {
+  if (e->mixed_ok && b.m_pre > 0 && b.m_pre <= e->s.prefill_chunk) {
     // steady state: the few admitted prompts join the decode pass (direct launches:
     // the row count varies)
     e->last_m = e->s.Q_g;
@@ -1038,7 +1053,7 @@ int32_t srl_decode_step(srl_engine* e, srl_step_info* info) {
     }
   }
   if (G.exec) {
-    cudaGraphLaunch(G.exec, st);
+    if (cudaError_t ge = cudaGraphLaunch(G.exec, st)) note_launch(e, "decode graph launch", (int)ge);
     e->launches += G.launches;
   } else {
     decode_tail(e, e->comm == nullptr, M);
@@ -1299,8 +1314,20 @@ extern "C" int32_t srl_load_policy_tensor(srl_engine* e, const char* name, const
     else if (t == "wg") rc = pack_weight_rows(s, m.ff, m.d, w.pgu, 64, 128, 0, e->st);
     else if (t == "wu") rc = pack_weight_rows(s, m.ff, m.d, w.pgu, 64, 128, 64, e->st);
     else return fail(SRL_E_INVALID_ARG, "srl_load_policy_tensor: not loadable: " + n);
-    if (!e->m.weights_compact && en->off != kNoOff)  // keep the staging image consistent too
-      cudaMemcpyAsync(e->W + en->off, src, en->numel * 2, cudaMemcpyDeviceToDevice, e->st);
+    if (!e->m.weights_compact && en->off != kNoOff) {  // keep the staging image consistent too
+      // (wg / wu: the source is plain row-major, the staging image interleaves
+      // row_block-row blocks at block_stride rows -- scatter block by block)
+      const size_t rowb = en->cols * 2;
+      if (en->row_block == en->rows) {
+        if (cudaMemcpyAsync(e->W + en->off, src, en->numel * 2, cudaMemcpyDeviceToDevice, e->st) != cudaSuccess) rc = -3;
+      } else if (en->rows % en->row_block == 0) {
+        if (cudaMemcpy2DAsync(e->W + en->off, en->block_stride * rowb, src, en->row_block * rowb, en->row_block * rowb,
+                              en->rows / en->row_block, cudaMemcpyDeviceToDevice, e->st) != cudaSuccess)
+          rc = -3;
+      } else {
+        rc = -1;
+      }
+    }
   }
   e->launches++;
   if (rc || cudaGetLastError() != cudaSuccess) return cuda_fail("srl_load_policy_tensor");

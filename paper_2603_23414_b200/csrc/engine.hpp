@@ -16,7 +16,7 @@ namespace srl {
 constexpr int kPage = 64;       // tokens per KV page
 constexpr int kMaxR = 64;       // max data-parallel replicas
 constexpr int kCtlThreads = 1024;
-constexpr int kMaxSortReady = 4096;  // bitonic-sort capacity of the ready list
+constexpr int kMaxSortReady = 16384;  // bitonic-sort capacity of the ready list (128 KB of shared memory)
 constexpr int kMaxGroup = 2048;      // largest update group that can be harvested
 
 enum TrajState { TS_STREAM = 0, TS_PENDING = 1, TS_RUNNING = 2, TS_READY = 3, TS_EMITTED = 4 };

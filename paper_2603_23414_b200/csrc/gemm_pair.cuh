@@ -24,7 +24,7 @@
 //     shared memory of the CTA (same row half) that owns the chunk
 //     (st.shared::cluster, fire-and-forget), and the owner sums the S partials
 //     in pair (= k) order from local memory -- deterministic;
-//  2  stream-K (opt-in, SRL_GEMM_SPLIT=2): the flattened (unit, k-block) space
+//  2  stream-K (opt-in, srl_tuning.gemm_split = 2): the flattened (unit, k-block) space
 //     is cut into #pairs equal ranges; a unit cut between pairs is finished by
 //     its LAST arriving piece: every piece stores its fp32 partial to an
 //     L2-resident workspace slot and bumps the unit's counter, and the CTA

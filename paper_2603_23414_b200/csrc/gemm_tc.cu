@@ -534,7 +534,7 @@ static int gemm_pair_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W
   //     deduplicated by L2 (QKV 32 vs 30 us, down 72 vs 42 us per launch);
   //   2 stream-K with an L2 fix-up (gemm_pair.cuh).  Measured r01: slower (QKV
   //     53 us in the decode graph): 128 KB fp32 partials per piece through L2.
-  static const int mode = getenv("SRL_GEMM_SPLIT") ? atoi(getenv("SRL_GEMM_SPLIT")) : 1;
+  const int mode = tuning().gemm_split;
   int mb = pick_mblk(M);
   bool bsplit = false;
   if (mode == 0 && M <= 256 && p.n_tiles < pairs) {
@@ -613,15 +613,12 @@ static int gemm_pair_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W
   }
   if (tma_encode_2d(&tmX, X, M, K, (uint64_t)K * 2, p.m_blk >> 1, 64, 2, true)) return -2;
   const size_t smem = 1024 + rings + (2 * stages + 2 * xstages + 4) * 8 + 16 + 2 * kXchFloats * 4 + kRowTab * 4;
-  static bool attr_set = false;
-  if (!attr_set) {
+  if (once_per_device(kOnceGemmPair)) {  // a per-device function attribute
     cudaFuncSetAttribute(gemm_pair_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(gemm_pair_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(gemm_pair_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_set = true;
   }
-  static const bool verbose = getenv("SRL_GEMM_VERBOSE") != nullptr;
-  if (verbose)
+  if (tuning().verbose)
     fprintf(stderr, "gemm(pair) M=%d N=%d K=%d units=%d S=%d sk=%d stages=%d/%d smem=%zu\n", M, N, K, p.units, S,
             (int)sk, stages, xstages, smem);
   int rc;
@@ -638,14 +635,13 @@ static int gemm_pair_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W
 }
 
 int gemm_partial_split(int M, int N, int K, int num_sms) {
-  static const int pair_env = getenv("SRL_GEMM_PAIR") ? atoi(getenv("SRL_GEMM_PAIR")) : -1;
-  static const bool off = getenv("SRL_NO_PARTIAL_NORM") != nullptr;
-  const bool pair = pair_env >= 0 ? pair_env > 0 : M >= 128;
+  const int pair_sel = tuning().gemm_pair;
+  const bool off = !tuning().partial_norm;
+  const bool pair = pair_sel >= 0 ? pair_sel > 0 : M >= 128;
   if (off || M <= 0 || K % 64) return 1;
-  if (!pair) {  // single-CTA kernel (H = 1 in partial mode) -- opt-in, SRL_PARTIAL_SMALL_M=1:
+  if (!pair) {  // single-CTA kernel (H = 1 in partial mode) -- opt-in (srl_tuning.partial_small_m):
     // measured r01 neutral on the 32B slice (O / down -0.37 ms, the norms +0.25 ms per step)
-    static const bool small_on = getenv("SRL_PARTIAL_SMALL_M") != nullptr;
-    if (!small_on) return 1;
+    if (!tuning().partial_small_m) return 1;
     const int m_blk = pick_mblk(M);
     const int units = (N + 127) / 128 * ((M + m_blk - 1) / m_blk);
     return single_partial_split(units, K / 64, num_sms);
@@ -663,8 +659,8 @@ int gemm_bf16_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N
   if (M <= 0 || N <= 0) return 0;
   if (K % 64 != 0) return -1;
   if (epi.kind == EPI_SILU && N % 128 != 0) return -1;  // N counts interleaved gate/up rows
-  static const int pair_env = getenv("SRL_GEMM_PAIR") ? atoi(getenv("SRL_GEMM_PAIR")) : -1;
-  const bool pair = pair_env >= 0 ? pair_env > 0 : M >= 128;
+  const int pair_sel = tuning().gemm_pair;
+  const bool pair = pair_sel >= 0 ? pair_sel > 0 : M >= 128;
   if (pair) {
     const int r = gemm_pair_fused(X, M, W, N, K, epi, num_sms, stream);
     if (r <= 0) return r;
@@ -697,7 +693,7 @@ int gemm_bf16_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N
     if (units >= num_sms) return (double)units / ((double)((units + num_sms - 1) / num_sms) * num_sms);
     return (double)units * pick_s(units) / num_sms;
   };
-  static const int h_env = getenv("SRL_GEMM_H") ? atoi(getenv("SRL_GEMM_H")) : 0;
+  const int h_env = tuning().gemm_h;
   // packed weights pad rows to 128 only: H = 2 needs an even number of 128-row tiles
   const bool h2_ok = !(epi.w_packed && ((N + 127) / 128) % 2);
   const bool part = epi.kind == EPI_PARTIAL;
@@ -715,8 +711,8 @@ int gemm_bf16_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N
   const int stage_a = p.H * kStageA;
   const int stage_b = p.m_blk * 128;
   const int budget = 200 * 1024;
-  static const int xs_env = getenv("SRL_GEMM_XSTAGES") ? atoi(getenv("SRL_GEMM_XSTAGES")) : 0;
-  static const int ws_env = getenv("SRL_GEMM_STAGES") ? atoi(getenv("SRL_GEMM_STAGES")) : 0;
+  const int xs_env = tuning().gemm_xstages;
+  const int ws_env = tuning().gemm_stages;
   int xstages = stage_b <= 8192 ? 4 : (stage_b <= 16384 ? 3 : 2);
   if (xs_env) xstages = xs_env;
   int stages = (budget - xstages * stage_b) / stage_a;
@@ -742,11 +738,9 @@ int gemm_bf16_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N
   }
   if (tma_encode_2d(&tmX, X, M, K, (uint64_t)K * 2, p.m_blk, 64, 2, true)) return -2;
   const size_t smem = 1024 + rings + (2 * stages + 2 * xstages + 4) * 8 + 16 + 2 * kXchFloats * 4 + kRowTab * 4;
-  static bool attr_set = false;
-  if (!attr_set) {
+  if (once_per_device(kOnceGemmSingle)) {  // a per-device function attribute
     cudaFuncSetAttribute(gemm_bf16_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(gemm_bf16_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_set = true;
   }
   if (S == 1) {
     const int grid = p.units < num_sms ? p.units : num_sms;
@@ -764,8 +758,7 @@ int gemm_bf16_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    static const bool verbose = getenv("SRL_GEMM_VERBOSE") != nullptr;
-    if (verbose) {
+    if (tuning().verbose) {
       int ncl = -1;
       cudaOccupancyMaxActiveClusters(&ncl, gemm_bf16_tc_kernel<1>, &cfg);
       fprintf(stderr, "gemm M=%d N=%d K=%d H=%d units=%d S=%d hp=%d stages=%d smem=%zu max_active_clusters=%d\n", M,

@@ -2,6 +2,16 @@
 // Gumbel-max sampler (sampler.cu) and the LM-head GEMM's fused sampling
 // epilogue (gemm_epi.cuh, EPI_SAMPLE).  One definition so both paths take the
 // token decision with the same correctly rounded fp32 operations.
+// The log_rn algorithm below follows FreeBSD msun e_logf.c, which carries:
+//   Conversion to float by Ian Lance Taylor, Cygnus Support, ian@cygnus.com.
+//   ====================================================
+//   Copyright (C) 1993 by Sun Microsystems, Inc. All rights reserved.
+//
+//   Developed at SunPro, a Sun Microsystems, Inc. business.
+//   Permission to use, copy, modify, and distribute this
+//   software is freely granted, provided that this notice
+//   is preserved.
+//   ====================================================
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>

@@ -9,19 +9,17 @@
 // graph these become programmatic edges: a kernel's launch latency, prologue
 // (barrier init, TMEM allocation, descriptor prefetch) and -- for the GEMMs --
 // the first weight tiles of its stream overlap the predecessor's tail.
-// SRL_NO_PDL=1 launches everything with plain stream order.
+// srl_tuning.pdl = 0 launches everything with plain stream order.
 #pragma once
 #include <cuda_runtime.h>
 
-#include <cstdlib>
 #include <utility>
+
+#include "tuning.hpp"
 
 namespace srl {
 
-inline bool pdl_enabled() {
-  static const bool on = getenv("SRL_NO_PDL") == nullptr;
-  return on;
-}
+inline bool pdl_enabled() { return tuning().pdl != 0; }
 
 template <typename... Exp, typename... Act>
 inline cudaError_t launch_k(void (*kern)(Exp...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int cluster,

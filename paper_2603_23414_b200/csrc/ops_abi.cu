@@ -1,9 +1,11 @@
 // ops_abi.cu — extern "C" op-level entry points (include/srl_ops.h).
+#include <atomic>
 #include <cstdio>
 #include <string>
 
 #include "kernels.hpp"
 #include "srl_ops.h"
+#include "tuning.hpp"
 
 namespace srl {
 thread_local std::string g_last_error = "ok";
@@ -17,6 +19,54 @@ void set_error(const char* fmt, const char* a = "", long b = 0) {
 using namespace srl;
 
 extern "C" const char* srl_last_error(void) { return g_last_error.c_str(); }
+
+// ------------------------------------------------------------------ tuning
+namespace srl {
+srl_tuning g_tuning = {
+    /*gemm_split*/ 1, /*gemm_pair*/ -1, /*gemm_h*/ 0, /*gemm_stages*/ 0, /*gemm_xstages*/ 0,
+    /*partial_norm*/ 1, /*partial_small_m*/ 0, /*qkv_finish*/ 0, /*fused_sample*/ 0,
+    /*attn_min_items*/ 0, /*attn_target_items*/ 0, /*attn_l2_prefetch*/ 0,
+    /*pdl*/ 1, /*graphs*/ 1, /*mixed_prefill*/ 1, /*verbose*/ 0};
+
+bool once_per_device(int slot) {
+  static std::atomic<unsigned long long> done[kOnceSlots];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (slot < 0 || slot >= kOnceSlots || dev < 0 || dev >= 64) return true;
+  const unsigned long long bit = 1ull << dev;
+  return (done[slot].fetch_or(bit) & bit) == 0;
+}
+}  // namespace srl
+
+extern "C" void srl_default_tuning(srl_tuning* t) {
+  if (!t) return;
+  srl_tuning d = {1, -1, 0, 0, 0, 1, 0, 0, 0, 0, 0, 0, 1, 1, 1, 0};
+  *t = d;
+}
+
+extern "C" int32_t srl_get_tuning(srl_tuning* t) {
+  if (!t) {
+    set_error("srl_get_tuning: %s", "null argument", 0);
+    return -1;
+  }
+  *t = g_tuning;
+  return 0;
+}
+
+extern "C" int32_t srl_set_tuning(const srl_tuning* t) {
+  if (!t) {
+    set_error("srl_set_tuning: %s", "null argument", 0);
+    return -1;
+  }
+  if (t->gemm_split < 0 || t->gemm_split > 3 || t->gemm_pair < -1 || t->gemm_pair > 1 || t->gemm_h < 0 ||
+      t->gemm_h > 2 || t->gemm_stages < 0 || t->gemm_xstages < 0 || t->attn_min_items < 0 ||
+      t->attn_target_items < 0 || t->attn_l2_prefetch < 0 || t->attn_l2_prefetch > 16) {
+    set_error("srl_set_tuning: %s", "field out of range", 0);
+    return -1;
+  }
+  g_tuning = *t;
+  return 0;
+}
 
 static int op_sms() {
   int dev = 0, n = 148;

@@ -104,3 +104,51 @@ def test_compact_weights_sizing_on_cpu(lib):
     mt = _lib.ModelCfg(TINY.L, TINY.d, TINY.Hq, TINY.Hkv, TINY.dh, TINY.ff, TINY.V, 1e4, 1e-5, 0, 1)
     s.U = 4
     assert L.srl_arena_sizes(ctypes.byref(mt), ctypes.byref(s), 1, None, None, None) < 0
+
+
+def test_emission_sort_capacity_is_validated(lib):
+    """the emission sort keeps the ready list in shared memory
+    (16384 keys).  SORTED can hold U-1+Q_tot ready trajectories and POSTHOC the
+    whole pool, so configurations beyond that are rejected up front."""
+    from paper_2603_23414_b200 import _lib
+    from workload.configs import TINY
+    L = _lib.load()
+    m = _lib.ModelCfg(TINY.L, TINY.d, TINY.Hq, TINY.Hkv, TINY.dh, TINY.ff, TINY.V, 1e4, 1e-5, 0)
+
+    def ok(Q_g, U, pool, mode, world=1):
+        s = _lib.SchedCfg(Q_g, U, -1, pool, 1, 64, 64, 64, mode, 0, 0, 0, -1, 1, 1.0, 3, 64, 16, 256)
+        return L.srl_arena_sizes(ctypes.byref(m), ctypes.byref(s), world, None, None, None) == 0
+    assert ok(4096, 2048, 8192, 0)                      # U-1+Q_tot = 6143 <= 16384
+    assert ok(512, 64, 8192, 2, world=8)                # bench --mode posthoc --gpus 8: pool 8192
+    assert not ok(512, 64, 16384, 2, world=8)           # POSTHOC pool + U - 1 > 16384
+    assert b"POSTHOC" in L.srl_last_error()
+    assert ok(512, 64, 16384, 0, world=8)               # SORTED with the same pool is fine
+    assert ok(512, 64, 16384, 1, world=8)               # SYNC never sorts
+
+
+def test_tuning_roundtrip_and_validation(lib):
+    """srl_tuning replaces every environment override: defaults are the
+    production choices, out-of-range values are rejected without changing anything."""
+    from paper_2603_23414_b200 import _lib
+    d = _lib.get_tuning()
+    assert d["gemm_split"] == 1 and d["gemm_pair"] == -1 and d["partial_norm"] == 1 and d["pdl"] == 1
+    assert d["graphs"] == 1 and d["mixed_prefill"] == 1 and d["fused_sample"] == 0 and d["qkv_finish"] == 0
+    old = _lib.set_tuning(fused_sample=1, attn_l2_prefetch=4)
+    try:
+        t = _lib.get_tuning()
+        assert t["fused_sample"] == 1 and t["attn_l2_prefetch"] == 4 and t["gemm_split"] == 1
+        with pytest.raises(_lib.SRLError):
+            _lib.set_tuning(gemm_split=7)
+        assert _lib.get_tuning() == t
+    finally:
+        _lib.set_tuning(**old)
+    assert _lib.get_tuning() == d
+    _lib.set_tuning(defaults=True)
+    assert _lib.get_tuning() == d
+
+
+def test_library_reads_no_environment():
+    """No getenv in the product library (the knobs moved to srl_tuning)."""
+    import glob
+    for f in glob.glob(os.path.join(ROOT, "paper_2603_23414_b200", "csrc", "*")):
+        assert "getenv" not in open(f).read(), f

@@ -134,7 +134,7 @@ def test_edge_cases_bit_exact(name, over, n, plen, cap):
 
 
 def test_fused_lm_head_sampling_matches():
-    """The opt-in LM-head-fused sampler (SRL_FUSED_SAMPLE=1: EPI_SAMPLE partials in
+    """The opt-in LM-head-fused sampler (srl_tuning.fused_sample: EPI_SAMPLE partials in
     the GEMM epilogue + sample_reduce) must pass the same teacher-forced parity test
     -- schedule bit-exact, ids bit-exact vs the oracle's Gumbel-max on the GPU
     logits, logits / logprobs within tolerance.  Run in a subprocess: the switch is
@@ -143,7 +143,7 @@ def test_fused_lm_head_sampling_matches():
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, SRL_FUSED_SAMPLE="1")
+    env = dict(os.environ, SRL_TEST_TUNING="fused_sample=1")
     out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
                           "tests/test_gpu_engine.py::test_model_parity_teacher_forced"],
                          cwd=root, capture_output=True, text=True, env=env, timeout=900)

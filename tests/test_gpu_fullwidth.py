@@ -142,14 +142,14 @@ def test_fullwidth_teacher_forced(shape, Q_g):
 
 
 def test_fullwidth_qkv_finish_path():
-    """The opt-in QKV handoff (SRL_QKV_FINISH=1: split-K partials + the bias / RoPE /
+    """The opt-in QKV handoff (srl_tuning.qkv_finish: split-K partials + the bias / RoPE /
     KV-append kernel) passes the same full-width parity test.  Subprocess: the
     switch is read once per process."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, SRL_QKV_FINISH="1")
+    env = dict(os.environ, SRL_TEST_TUNING="qkv_finish=1")
     out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
                           "tests/test_gpu_fullwidth.py::test_fullwidth_teacher_forced[llama8b-L2-Q256]"],
                          cwd=root, capture_output=True, text=True, env=env, timeout=1200)

@@ -6,6 +6,8 @@ import torch
 from paper_2603_23414_b200 import _lib
 
 lib = _lib.load()
+if os.environ.get("BENCH_TUNING"):  # e.g. "gemm_h=2,gemm_stages=4" (tools/gemm_sweep.sh)
+    _lib.set_tuning(**{k: int(v) for k, v in (kv.split("=") for kv in os.environ["BENCH_TUNING"].split(","))})
 s = torch.cuda.current_stream().cuda_stream
 res = {}
 PACKED = os.environ.get("BENCH_PACKED", "1") == "1"

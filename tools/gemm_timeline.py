@@ -2,7 +2,7 @@
 
   gemm_timeline.py op M N K epi      one srl_op_gemm_bf16 launch
   gemm_timeline.py engine [L]        layer-0 QKV / O / GU / DOWN launches of an
-                                     8B-width decode step (SRL_NO_GRAPH, L layers)
+                                     8B-width decode step (no graphs, L layers)
 """
 import ctypes
 import os
@@ -64,7 +64,8 @@ def op(M, N, K, epi):
 
 
 def engine(L):
-    os.environ["SRL_NO_GRAPH"] = "1"
+    from paper_2603_23414_b200 import _lib as _L
+    _L.set_tuning(graphs=0)
     from paper_2603_23414_b200.engine import RolloutEngine
     from workload.configs import LLAMA8B, SchedConfig, KV_BF16
     from workload.lengths import LengthModel, sample_lengths

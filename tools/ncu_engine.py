@@ -3,10 +3,11 @@ bracket ONE decode step with cudaProfilerStart/Stop (for ncu --profile-from-star
 usage: ncu_engine.py [L] [warm_steps]"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ.setdefault("SRL_NO_GRAPH", "1")
 import numpy as np
 import torch
 from paper_2603_23414_b200.engine import RolloutEngine
+from paper_2603_23414_b200 import _lib
+_lib.set_tuning(graphs=0)  # direct launches, one kernel per ncu record
 from workload.configs import LLAMA8B, SchedConfig, KV_BF16
 from workload.lengths import LengthModel, sample_lengths
 from workload.prompts import make_prompts

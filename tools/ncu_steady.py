@@ -1,17 +1,18 @@
 """The bench's cfg2 engine brought to mid-rollout (P decode steps, ~mean context
 1700 at P = 1500), then ONE decode step bracketed by cudaProfilerStart/Stop for
-`ncu --profile-from-start off` (direct launches: SRL_NO_GRAPH=1).
+`ncu --profile-from-start off` (direct launches: srl_tuning.graphs = 0).
 usage: ncu_steady.py [P]"""
 import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ.setdefault("SRL_NO_GRAPH", "1")
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import bench  # noqa: E402
 from paper_2603_23414_b200.engine import GROUP_READY, RolloutEngine  # noqa: E402
+from paper_2603_23414_b200 import _lib  # noqa: E402
+_lib.set_tuning(graphs=0)  # direct launches, one kernel per ncu record
 from workload.configs import LLAMA8B  # noqa: E402
 from workload.weights import fill_engine_weights  # noqa: E402
 
