@@ -67,6 +67,23 @@ def silu(x):
     return x / (1.0 + np.exp(-x))
 
 
+def bf16_round(x) -> np.ndarray:
+    """x rounded to the nearest bfloat16 value (ties to even), returned as float64.
+    bfloat16 is the top 16 bits of an IEEE binary32; x is first rounded to binary32
+    (as a GPU kernel holds it), then the low 16 bits are rounded off RNE."""
+    b = np.asarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    b = ((b + 0x7FFF + ((b >> 16) & 1)) >> 16) << 16
+    return b.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+# Where a bf16 decode path stores values in bf16 (DESIGN.md reading R29): the
+# normalised activations that feed the projection GEMMs, the RoPE'd query, the
+# KV cache (K after RoPE, V), the softmax numerators before the P.V product, the
+# attention output (O-projection operand), silu(g)*u (down-projection operand)
+# and the final-norm output (LM-head operand).  Everything else stays exact.
+STORAGE_POINTS = ("xn", "q", "kv", "p", "o", "act", "xf")
+
+
 class Model:
     def __init__(self, m: ModelShape, W: dict):
         self.m = m
@@ -112,33 +129,45 @@ class Model:
     def new_kv(self):
         return [([], []) for _ in range(self.m.L)]
 
-    def full_forward(self, toks) -> np.ndarray:
-        """Non-incremental causal forward over a whole sequence; returns logits [T, V].
-        Used only to pin the incremental decode (prefill == step-by-step decode)."""
+    def full_forward(self, toks, positions=None, storage_bf16=()) -> np.ndarray:
+        """Non-incremental causal forward over a whole sequence; returns logits [T, V]
+        (or only the rows `positions`).  Pins the incremental decode (prefill ==
+        step-by-step decode).
+
+        storage_bf16: names from STORAGE_POINTS (or True for all of them) at which
+        the value is rounded to bf16 (bf16_round) before it is used, exactly where a
+        bf16 decode path stores it (reading R29); the softmax denominator sums the
+        unrounded numerators.  Default: none -- the plain fp64 definition."""
         m, W = self.m, self.W
+        pts = set(STORAGE_POINTS) if storage_bf16 is True else set(storage_bf16)
+        assert pts <= set(STORAGE_POINTS), pts
+
+        def r(a, key):
+            return bf16_round(a) if key in pts else a
         T = len(toks)
         X = np.stack([self.embed(t) for t in toks])
         for l in range(m.L):
             p = f"L{l}."
-            H = rmsnorm(X, W[p + "attn_norm"], m.rms_eps)
+            H = r(rmsnorm(X, W[p + "attn_norm"], m.rms_eps), "xn")
             Qm, Km, Vm = H @ W[p + "wq"].T, H @ W[p + "wk"].T, H @ W[p + "wv"].T
             if m.qkv_bias:
                 Qm, Km, Vm = Qm + W[p + "bq"], Km + W[p + "bk"], Vm + W[p + "bv"]
-            Qr = np.stack([rope(Qm[t].reshape(m.Hq, m.dh), t, m.rope_theta) for t in range(T)])
-            Kr = np.stack([rope(Km[t].reshape(m.Hkv, m.dh), t, m.rope_theta) for t in range(T)])
-            Vr = Vm.reshape(T, m.Hkv, m.dh)
+            Qr = r(np.stack([rope(Qm[t].reshape(m.Hq, m.dh), t, m.rope_theta) for t in range(T)]), "q")
+            Kr = r(np.stack([rope(Km[t].reshape(m.Hkv, m.dh), t, m.rope_theta) for t in range(T)]), "kv")
+            Vr = r(Vm.reshape(T, m.Hkv, m.dh), "kv")
             grp = m.Hq // m.Hkv
             O = np.zeros((T, m.Hq, m.dh))
+            causal = np.tril(np.ones((T, T), dtype=bool))
             for h in range(m.Hq):
                 S = Qr[:, h, :] @ Kr[:, h // grp, :].T / np.sqrt(m.dh)
-                S = np.where(np.tril(np.ones((T, T), dtype=bool)), S, -np.inf)
+                S = np.where(causal, S, -np.inf)
                 P = np.exp(S - S.max(axis=1, keepdims=True))
-                P /= P.sum(axis=1, keepdims=True)
-                O[:, h, :] = P @ Vr[:, h // grp, :]
-            X = X + O.reshape(T, -1) @ W[p + "wo"].T
-            H2 = rmsnorm(X, W[p + "mlp_norm"], m.rms_eps)
-            X = X + (silu(H2 @ W[p + "wg"].T) * (H2 @ W[p + "wu"].T)) @ W[p + "wd"].T
-        return rmsnorm(X, W["final_norm"], m.rms_eps) @ W["lm_head"].T
+                O[:, h, :] = (r(P, "p") @ Vr[:, h // grp, :]) / P.sum(axis=1, keepdims=True)
+            X = X + r(O.reshape(T, -1), "o") @ W[p + "wo"].T
+            H2 = r(rmsnorm(X, W[p + "mlp_norm"], m.rms_eps), "xn")
+            X = X + r(silu(H2 @ W[p + "wg"].T) * (H2 @ W[p + "wu"].T), "act") @ W[p + "wd"].T
+        Xf = X if positions is None else X[np.asarray(positions)]
+        return r(rmsnorm(Xf, W["final_norm"], m.rms_eps), "xf") @ W["lm_head"].T
 
 
 class ModelRunner:

@@ -1314,19 +1314,20 @@ extern "C" int32_t srl_load_policy_tensor(srl_engine* e, const char* name, const
     else if (t == "wg") rc = pack_weight_rows(s, m.ff, m.d, w.pgu, 64, 128, 0, e->st);
     else if (t == "wu") rc = pack_weight_rows(s, m.ff, m.d, w.pgu, 64, 128, 64, e->st);
     else return fail(SRL_E_INVALID_ARG, "srl_load_policy_tensor: not loadable: " + n);
-    if (!e->m.weights_compact && en->off != kNoOff) {  // keep the staging image consistent too
-      // (wg / wu: the source is plain row-major, the staging image interleaves
-      // row_block-row blocks at block_stride rows -- scatter block by block)
-      const size_t rowb = en->cols * 2;
-      if (en->row_block == en->rows) {
-        if (cudaMemcpyAsync(e->W + en->off, src, en->numel * 2, cudaMemcpyDeviceToDevice, e->st) != cudaSuccess) rc = -3;
-      } else if (en->rows % en->row_block == 0) {
-        if (cudaMemcpy2DAsync(e->W + en->off, en->block_stride * rowb, src, en->row_block * rowb, en->row_block * rowb,
-                              en->rows / en->row_block, cudaMemcpyDeviceToDevice, e->st) != cudaSuccess)
-          rc = -3;
-      } else {
-        rc = -1;
-      }
+  }
+  if (is_packed_tensor(n) && !e->m.weights_compact && en->off != kNoOff) {
+    // keep the staging image consistent too (srl_load_policy_weights(NULL) re-packs
+    // from it); wg / wu: the source is plain row-major, the staging image
+    // interleaves row_block-row blocks at block_stride rows -- scatter block-wise
+    const size_t rowb = en->cols * 2;
+    if (en->row_block == en->rows) {
+      if (cudaMemcpyAsync(e->W + en->off, src, en->numel * 2, cudaMemcpyDeviceToDevice, e->st) != cudaSuccess) rc = -3;
+    } else if (en->rows % en->row_block == 0) {
+      if (cudaMemcpy2DAsync(e->W + en->off, en->block_stride * rowb, src, en->row_block * rowb, en->row_block * rowb,
+                            en->rows / en->row_block, cudaMemcpyDeviceToDevice, e->st) != cudaSuccess)
+        rc = -3;
+    } else {
+      rc = -1;
     }
   }
   e->launches++;
