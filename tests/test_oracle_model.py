@@ -140,3 +140,73 @@ def test_weight_generator_numpy_equals_torch():
     a = gen_weight_np(m, "L0.bk", version=2)
     b = gen_weight_torch(m, "L0.bk", version=2, device="cpu")
     np.testing.assert_array_equal(a.view(np.int16), b.view(torch.int16).numpy())
+
+
+# ------------------------------------------------------------------ hand-derived pins
+def _worked_example():
+    import json
+    import os
+    d = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "model_worked_example.json")))
+    m = ModelShape("worked", L=1, d=2, Hq=1, Hkv=1, dh=2, ff=1, V=2, rope_theta=1e4, rms_eps=0.0)
+    W = {("L0." + k if k not in ("embed", "final_norm", "lm_head") else k): np.array(v, dtype=np.float64)
+         for k, v in d["weights"].items()}
+    return d, m, W
+
+
+def test_model_hand_derived_worked_example():
+    """silu on the GATE rows, the up rows as the multiplier, the final RMSNorm applied
+    BEFORE the LM head: a 1-layer d=2 block derived by hand (tests/golden).  Each
+    plausible misreading gives a logit at least 1e-2 away."""
+    d, m, W = _worked_example()
+    mdl = Model(m, W)
+    x = mdl.decode_token(d["token"], 0, mdl.new_kv())
+    z = mdl.logits(x)
+    np.testing.assert_allclose(z, d["logits"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(mdl.full_forward([d["token"]])[0], d["logits"], rtol=0, atol=1e-12)
+    for name, wrong in d["wrong_readings"].items():
+        assert np.abs(np.asarray(wrong) - d["logits"]).max() > 1e-2, name
+
+
+def test_silu_closed_forms():
+    """silu(x) = x * sigmoid(x): silu(0) = 0, sigmoid(ln 3) = 3/4, silu(-x) = silu(x) - x."""
+    from oracle.model import silu
+    assert silu(0.0) == 0.0
+    assert abs(silu(np.log(3.0)) - 0.75 * np.log(3.0)) < 1e-15
+    x = np.linspace(-20, 20, 101)
+    np.testing.assert_allclose(silu(-x), silu(x) - x, rtol=0, atol=1e-12)
+    assert abs(silu(50.0) - 50.0) < 1e-15 and abs(silu(-50.0)) < 1e-18
+
+
+def test_bf16_round_matches_torch_rne():
+    """The storage-point rounding (reading R29) equals torch's float32 -> bfloat16
+    conversion (round to nearest, ties to even) on random values, exact ties and
+    subnormal / huge magnitudes."""
+    import torch
+    from oracle.model import bf16_round
+    rng = np.random.default_rng(7)
+    x = np.concatenate([rng.normal(size=200000) * 10.0 ** rng.uniform(-30, 30, 200000),
+                        np.array([1 + 2.0 ** -8, 1 + 3 * 2.0 ** -8, -(1 + 2.0 ** -8), 2.0 ** -130, 3e38, 0.0])])
+    x32 = x.astype(np.float32)
+    ref = torch.from_numpy(x32).to(torch.bfloat16).float().numpy().astype(np.float64)
+    got = bf16_round(x32)
+    assert np.array_equal(got, ref)
+    assert bf16_round(1 + 2.0 ** -8) == 1.0 and bf16_round(1 + 3 * 2.0 ** -8) == 1 + 2.0 ** -6   # ties to even
+
+
+def test_storage_rounding_points_each_act_and_positions_subset():
+    """Every storage point of the rounding variant is used (each one alone changes the
+    logits), none changes them by more than a few bf16 ulps' worth, and `positions`
+    returns exactly those rows of the full output."""
+    from oracle.model import STORAGE_POINTS
+    W = load_weights(TINY)
+    mdl = Model(TINY, W)
+    toks = [5, 17, 300, 2, 99, 41, 7]
+    z = mdl.full_forward(toks)
+    np.testing.assert_array_equal(mdl.full_forward(toks, positions=[1, 4, 6]), z[[1, 4, 6]])
+    rel = lambda a: np.linalg.norm(a - z, axis=1) / np.linalg.norm(z, axis=1)  # noqa: E731
+    for p in STORAGE_POINTS:
+        r = rel(mdl.full_forward(toks, storage_bf16=[p]))
+        assert r.max() > 0, p
+        assert r.max() < 2e-2, (p, r.max())
+    r_all = rel(mdl.full_forward(toks, storage_bf16=True))
+    assert 1e-4 < r_all.mean() < 2e-2

@@ -136,13 +136,22 @@ def test_sampler_low_temperature_is_argmax():
     assert tok == int(np.argmax(z))
 
 
-def test_sampler_logprob_is_log_softmax():
-    rng = np.random.default_rng(2)
-    z = (rng.normal(size=512) * 3).astype(np.float32)
-    tok, lp, _ = sample_row(z, np.float32(1.0), 3, 4, 9, 1)
-    zz = z.astype(np.float64)
-    ref = zz[tok] - np.log(np.exp(zz - zz.max()).sum()) - zz.max()
-    assert abs(lp - ref) < 1e-12
+def test_sampler_logprob_closed_forms():
+    """log pi(tok) for logits z_j = ln w_j is ln(w_tok / sum w) (P:180 caches this
+    value); at temperature T the policy is softmax(z / T), i.e. p_j ~ w_j^(1/T);
+    a common shift of the logits changes nothing."""
+    w = np.array([1.0, 2.0, 3.0, 4.0])
+    z = np.log(w).astype(np.float32)
+    for n in range(20):
+        tok, lp, _ = sample_row(z, np.float32(1.0), 3, n, 9, 1)
+        assert abs(lp - np.log(w[tok] / w.sum())) < 1e-6
+        tok2, lp2, _ = sample_row(z + np.float32(5.0), np.float32(1.0), 3, n, 9, 1)
+        assert tok2 == tok and abs(lp2 - lp) < 1e-6
+        T = 0.5
+        tok3, lp3, _ = sample_row(z, np.float32(1.0 / T), 3, n, 9, 1)
+        assert abs(lp3 - np.log(w[tok3] ** 2 / (w ** 2).sum())) < 1e-6
+    tok, lp, _ = sample_row(np.zeros(8, np.float32), np.float32(1.0), 3, 0, 0, 0)
+    assert abs(lp + np.log(8.0)) < 1e-12
 
 
 def test_gumbel_max_frequencies_match_softmax_chi2():
@@ -161,7 +170,21 @@ def test_gumbel_max_frequencies_match_softmax_chi2():
 
 
 def test_sampler_ties_lowest_index():
-    z = np.zeros(8, dtype=np.float32)
-    # identical scores only if noise identical: force by huge logits difference elsewhere
-    _, _, s = sample_row(z, np.float32(1.0), 3, 0, 0, 0)
-    assert int(np.argmax(s)) == int(np.flatnonzero(s == s.max())[0])
+    """Two perturbed scores made exactly equal (fp32) and larger than all others:
+    the token is the lower index, wherever the pair sits."""
+    from oracle.sampler import gumbel
+    for (i, j) in [(0, 1), (3, 6), (2, 7)]:
+        g = gumbel(3, 8, 0, 0, 0)
+        z = np.full(8, -1e4, np.float32)
+        z[i] = np.float32(0.0)
+        target = np.float32(g[i])                     # s_i = 0 + g_i
+        d = np.float32(target - g[j])
+        for _ in range(64):                           # nudge z_j until fl(z_j + g_j) == s_i exactly
+            s_j = np.float32(d + g[j])
+            if s_j == target:
+                break
+            d = np.nextafter(d, np.float32(np.inf) if s_j < target else np.float32(-np.inf), dtype=np.float32)
+        z[j] = d
+        tok, _, s = sample_row(z, np.float32(1.0), 3, 0, 0, 0)
+        assert s[i] == s[j] == s.max()
+        assert tok == i

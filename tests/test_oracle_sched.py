@@ -381,3 +381,53 @@ def test_state_errors():
     c.load_policy_weights(1)
     with pytest.raises(SchedError):
         Controller(SchedConfig(Q_g=0))
+
+
+# ---------------------------------------------------------------- metrics pins
+def test_staleness_spec_segment_example():
+    """S:366 (P:180 partial mode): segments (v3: 5 tokens)(v4: 7)(v5: 2) emitted at
+    version 5 -> per-token staleness 2 x5, 1 x7, 0 x2; the trajectory's v_emit - v_first = 2."""
+    from oracle.metrics import staleness
+    rec = {"v_first": 3, "vers": [3] * 5 + [4] * 7 + [5] * 2}
+    tok, traj = staleness([([rec], 5)])
+    assert tok == {2: 5, 1: 7, 0: 2} and traj == {2: 1}
+
+
+def test_staleness_sync_baseline_four_off_policy_updates():
+    """P:263 (section 4.3): rollout batch 512, update batch 128 -> '4 off-policy updates in
+    each iteration': the k-th group of a SYNC batch (0-based) is emitted k versions after
+    the batch was generated, so the last one has staleness 3 on every token.  Scaled to a
+    rollout batch of 8 and update groups of 2 (the same 4:1 ratio)."""
+    from oracle.metrics import staleness
+    L = [3, 1, 4, 1, 5, 9, 2, 6]
+    c, groups = run(L, Q_g=8, U=2, pool_prompts=8, cap=16, mode=MODE_SYNC)
+    assert len(groups) == 4
+    for k, g in enumerate(groups):
+        tok, traj = staleness([(g, k)])
+        assert set(tok) == {k} and set(traj) == {k}
+    tok, _ = staleness([(g, k) for k, g in enumerate(groups)])
+    assert tok[3] == sum(r["len"] for r in groups[-1])
+
+
+def test_curriculum_profile_worked_example():
+    """golden/sched_worked_example.json (K = inf, Q >= N, one epoch): groups are the
+    consecutive U-slices of the sorted lengths [1,1 | 2,3 | 4,5 | 6,9], so the profile
+    of group means is [1, 2.5, 4.5, 7.5] -- the short-to-long micro-curriculum."""
+    from oracle.metrics import curriculum_profile
+    c, groups = run([3, 1, 4, 1, 5, 9, 2, 6], Q_g=8, U=2, pool_prompts=8, cap=16, K=K_INF)
+    prof = curriculum_profile([(g, c.stream[g[0]["traj_id"]].epoch) for g in groups])
+    assert prof == {0: [1.0, 2.5, 4.5, 7.5]}
+    # two epochs of the same lengths: the profile restarts short in each epoch
+    c, groups = run([3, 1, 4, 1, 5, 9, 2, 6] * 2, Q_g=8, U=2, pool_prompts=8, cap=16, K=K_INF)
+    prof = curriculum_profile([(g, c.stream[g[0]["traj_id"]].epoch) for g in groups])
+    assert prof == {0: [1.0, 2.5, 4.5, 7.5], 1: [1.0, 2.5, 4.5, 7.5]}
+
+
+def test_throughput_function_identity():
+    """metrics.throughput over the abstract trace (dt = 1) equals Q (1 - B)."""
+    from oracle.metrics import throughput
+    c, _ = run([3, 1, 4, 1, 5, 9, 2, 6], Q_g=4, U=2, pool_prompts=8, cap=16, K=K_INF)
+    B = bubble_ratio(c.trace, 4)
+    assert throughput(c.raw_tokens, Fraction(len(c.trace))) == 4 * (1 - B)
+    with pytest.raises(ValueError):
+        throughput(5, 0)
