@@ -1,30 +1,36 @@
 """Full-width parity: LLaMA-3.1-8B- and Qwen-2.5-32B-shaped policies (2-layer
-slices at full width, SURVEY §8(c) "shape-faithful shallow slices"), at the
-per-GPU batch the benchmark runs (Q_g = 256 for 8B / cfg2, Q_g = 64 for 32B /
-cfg4), through the C ABI with the same GEMM / attention / sampler launch
-configurations bench.py times (the GEMM picks its split from M, N, K only).
+slices at full width, SURVEY §8(c) "shape-faithful shallow slices") through the
+C ABI with the launch configurations bench.py times (the GEMM picks its split
+from M, N, K only; attention its split-KV plan from rows x kv heads).
 
-Per sampled row and generated index n (teacher forcing on the GPU's own
-tokens, oracle.model.Model.full_forward in fp64 -- pinned against incremental
-decode in test_oracle_model.py):
-* logits: per-(row, n) relative L2 -- mean over the checked rows <= 1e-2 (the
-  BASELINE.json north-star bar), every one <= 1.5e-2.  DESIGN.md reading R29:
-  at full width the bf16 rounding points of the path (GEMM activation operands,
-  q, KV cache, P, attention output, SiLU product, LM-head input) alone give
-  0.0083 mean / 0.0097 max rel-L2 at 2 layers (numpy fp64 model with exactly
-  those roundings, tools/precision_budget.py), so the per-element bar is the
-  mean, the max carries the derived headroom;
-* the sampler's id on the GPU logits equals oracle.sampler.sample_row's
-  (bit-exact Gumbel-max on identical logits) and the harvested token;
-* the oracle's own sample on its own logits equals the GPU's token unless the
-  top-2 perturbed-score gap is below 4x the observed logits error (at V >= 128k
-  that band holds ~20% of positions; >= 60% must be decided);
-* logprobs within 4x the max-abs logits error + 1e-4.
+Per checked (row, generated index n) -- teacher forcing on the GPU's own tokens,
+oracle.model.Model.full_forward in fp64 (pinned against incremental decode and
+a hand-derived example in test_oracle_model.py) -- three oracle logits vectors
+at exactly that position:
+  z_x  the plain fp64 definition,
+  z_e  the same forward with bf16 rounding at the path's storage points
+       (oracle.model.STORAGE_POINTS, reading R29),
+  z_p  the forward with only the softmax-weight rounding (point "p").
+Bars:
+* per position  rel(z_gpu, z_x) <= rel(z_e, z_x) + 2 rel(z_p, z_x) + 1e-3:
+  the GPU rounds at the same points as z_e, except that it rounds the softmax
+  weights relative to running (online-softmax) maxima instead of the row
+  maximum -- a different draw of the p-rounding, bounded by twice that term --
+  plus fp32 accumulation (the 1e-3 slack, ~10x the fp32 GEMM bound measured
+  in test_gpu_ops).  This is the per-position bound VERDICT r1 asked for,
+  derived at exactly the rows and positions checked (it replaces the round-1
+  "mean <= 1e-2, max <= 1.5e-2" reading);
+* per position  rel(z_gpu, z_e) <= 2 rel(z_p, z_x) + 1e-3 (the GPU tracks the
+  rounding model, not just the exact one);
+* the mean of rel(z_gpu, z_x) over checked positions <= 1e-2 (north star);
+* sampled ids: the oracle's Gumbel-max on the GPU logits equals the GPU's token
+  (bit-exact sampler); the oracle's sample on z_e equals the GPU's token unless
+  the top-2 perturbed-score gap is under 4x max|z_gpu - z_e| (counted, must be
+  rare); logprobs within 4x max|z_gpu - z_x| + 1e-4.
 
 Weights: the workload generator's torch implementation (bit-identical to its
 numpy one, pinned in test_oracle_model.py) evaluated on the GPU and copied to
-host -- generating 1e9 elements with numpy would take minutes; the embedding
-table is never materialised (rows on demand).
+host; the embedding table is never materialised (rows on demand).
 """
 import numpy as np
 import pytest
@@ -66,11 +72,83 @@ def _oracle_weights(m):
     return W
 
 
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def check_positions(mdl, cases, seed, invT=np.float32(1.0), label=""):
+    """cases: list of (traj_id, prompt tokens, generated tokens, behaviour logprobs,
+    {n: gpu logits row}).  Applies the bars of the module docstring at every n."""
+    stats = dict(rel_x=[], rel_e=[], bound=[], checked=0, excluded=0)
+    for tid, prompt, gen, lps, zg_by_n in cases:
+        ns = sorted(zg_by_n)
+        seq = list(prompt) + list(gen[:max(ns)])
+        pos = [len(prompt) - 1 + n for n in ns]
+        zx = mdl.full_forward(seq, positions=pos)
+        ze = mdl.full_forward(seq, positions=pos, storage_bf16=True)
+        zp = mdl.full_forward(seq, positions=pos, storage_bf16=["p"])
+        for i, n in enumerate(ns):
+            zg = zg_by_n[n].astype(np.float64)
+            # bit-exact sampler on identical logits
+            assert sample_row(zg_by_n[n], invT, seed, n, tid, 0)[0] == gen[n], (tid, n)
+            rx, re_, rp, rge = _rel(zg, zx[i]), _rel(ze[i], zx[i]), _rel(zp[i], zx[i]), _rel(zg, ze[i])
+            bound = re_ + 2 * rp + 1e-3
+            if rx > bound or rge > 2 * rp + 1e-3:
+                stats.setdefault("violations", []).append((tid, n, round(rx, 5), round(re_, 5), round(rp, 5),
+                                                           round(rge, 5)))
+            stats["rel_x"].append(rx)
+            stats["rel_e"].append(rge)
+            stats["bound"].append(bound)
+            err_e = float(np.abs(zg - ze[i]).max())
+            tok_e, _, sc = sample_row(ze[i].astype(np.float32), invT, seed, n, tid, 0)
+            ss = np.sort(sc.astype(np.float64))
+            if ss[-1] - ss[-2] < 4 * err_e:
+                stats["excluded"] += 1
+            else:
+                stats["checked"] += 1
+                if tok_e != gen[n]:
+                    stats.setdefault("violations", []).append((tid, n, "token", tok_e, gen[n]))
+            err_x = float(np.abs(zg - zx[i]).max())
+            _, lp_x, _ = sample_row(zx[i].astype(np.float32), invT, seed, n, tid, 0)
+            # the GPU's behaviour logprob is log-softmax of ITS logits at ITS token; the
+            # exact one at the same token differs by at most 2 max|dz|
+            lse = zx[i].max() + np.log(np.exp(zx[i] - zx[i].max()).sum())
+            if abs(lps[n] - (zx[i][gen[n]] - lse)) > 4 * err_x + 1e-4:
+                stats.setdefault("violations", []).append((tid, n, "logprob", lps[n], zx[i][gen[n]] - lse))
+    rx = np.array(stats["rel_x"])
+    print(f"{label}: rel-L2 vs exact mean {rx.mean():.2e} max {rx.max():.2e} (bound max "
+          f"{max(stats['bound']):.2e}); vs bf16-storage model mean {np.mean(stats['rel_e']):.2e} max "
+          f"{np.max(stats['rel_e']):.2e}; ids checked {stats['checked']}, near-tie excluded {stats['excluded']}; "
+          f"violations (tid, n, rel_x, rel_e_x, rel_p_x, rel_gpu_e) {stats.get('violations', [])}", flush=True)
+    assert not stats.get("violations"), stats["violations"]
+    assert rx.mean() <= 1e-2
+    return stats
+
+
 STEPS = 6
+
+
+def _drain(eng, Q_g):
+    """Run to the end; every trajectory's tokens + behaviour logprobs from the groups."""
+    gpu_tok, gpu_lp, v = {}, {}, 0
+    while True:
+        st, _ = eng.decode_step()
+        if st == 2:
+            break
+        if st == 1:
+            h = eng.harvest_finished(cap_recs=Q_g * 4)
+            for r in h.records:
+                seg = slice(r["tok_offset"], r["tok_offset"] + r["len"])
+                gpu_tok[r["traj_id"]], gpu_lp[r["traj_id"]] = h.tokens[seg].tolist(), h.logprobs[seg].tolist()
+            v += 1
+            eng.load_policy_weights(v)
+    return gpu_tok, gpu_lp
 
 
 @pytest.mark.parametrize("shape,Q_g", [(LLAMA8B, 256), (QWEN32B, 64)], ids=["llama8b-L2-Q256", "qwen32b-L2-Q64"])
 def test_fullwidth_teacher_forced(shape, Q_g):
+    """The benchmark's batch (Q_g = 256 / 64 rows, the pair / single-CTA GEMM paths
+    with their split-K decompositions), short prompts, 6 decode steps."""
     from paper_2603_23414_b200.engine import RolloutEngine
     from workload.weights import fill_engine_weights
     m = shape.with_layers(2)
@@ -90,14 +168,67 @@ def test_fullwidth_teacher_forced(shape, Q_g):
         z = eng.debug_logits()
         zs.append(z[rows].copy())
         del z
-    # run to the end; every trajectory's tokens + behaviour logprobs come back in the groups
-    gpu_tok, gpu_lp, v = {}, {}, 0
+    gpu_tok, gpu_lp = _drain(eng, Q_g)
+    eng.close()
+    torch.cuda.empty_cache()
+    assert sorted(gpu_tok) == list(range(Q_g)) and all(len(t) == cap for t in gpu_tok.values())
+    mdl = Model(m, _oracle_weights(m))
+    cases = [(s, [int(t) for t in toks[off[s]:off[s + 1]]], gpu_tok[s], gpu_lp[s], {n: zs[n][j] for n in range(STEPS)})
+             for j, s in enumerate(rows)]
+    st = check_positions(mdl, cases, cfg.sample_seed, label=m.name)
+    assert st["excluded"] <= 0.1 * (st["checked"] + st["excluded"])
+
+
+def test_fullwidth_long_context_split_kv_and_mixed_pass():
+    """LLaMA-8B width, prefilled contexts of 0.3-4k tokens over 8 slots: the epoch-start
+    prompts (10k tokens) run as separate prefill passes in 4096-row chunks (a prompt
+    split across chunks attends to its earlier chunk through the page table); the
+    decode steps run the 16-row bucket (graph-replayed from its second use) with
+    split-KV attention (8 rows x 8 kv heads = 64 pairs < 148 SMs) in longest-first
+    order; two trajectories finish early and the two remaining prompts are admitted
+    in MIXED passes (their prompt rows ride in the decode forward).  Checked rows:
+    the longest prompt, a 2k one, a short one, and a mixed-pass admission."""
+    from paper_2603_23414_b200.engine import DONE, GROUP_READY, RolloutEngine
+    from workload.weights import fill_engine_weights
+    m = LLAMA8B.with_layers(2)
+    plens = [4000, 2000, 700, 300, 1500, 64, 900, 500, 1200, 350]    # 8 slots, then 2 admitted later
+    forced = [14, 14, 3, 14, 14, 5, 14, 14, 9, 9]
+    n = len(plens)
+    rng = np.random.default_rng(11)
+    toks = [rng.integers(1, m.V, size=p).astype(np.int32) for p in plens]
+    off = np.concatenate([[0], np.cumsum(plens)]).astype(np.int32)
+    cfg = SchedConfig(Q_g=8, U=2, K=K_INF, pool_prompts=n, cap=16, kv_pages=260, kv_dtype=KV_BF16)
+    eng = RolloutEngine(m, cfg, max_traj=n, max_prompt=4096, prefill_chunk=4096)
+    fill_engine_weights(eng, m, 0)
+    eng.load_policy_weights(0)
+    eng.submit_prompts(np.arange(n, dtype=np.uint64) + 1, off, np.concatenate(toks), np.array(forced, np.int32))
+    check_tids = [0, 1, 3, 8]
+    slot_of, zrec = {}, {t: {} for t in check_tids}
+    ntok = {t: 0 for t in range(n)}
+    infos = []
+    v = 0
+    gpu_tok, gpu_lp = {}, {}
     while True:
-        st, _ = eng.decode_step()
-        if st == 2:
+        st, info = eng.decode_step()
+        if st == DONE:
             break
-        if st == 1:
-            h = eng.harvest_finished(cap_recs=Q_g)
+        if info.k >= 0:
+            infos.append(info)
+            tr, _ = eng.trace()
+            for kind, _k, slot, tid, _kept, _ in tr:
+                if kind == 2:                        # ADMIT (srl.h SRL_EV_ADMIT): a=k, b=slot, c=traj
+                    slot_of[tid] = slot
+            z = eng.debug_logits()
+            for t in check_tids:
+                s = slot_of.get(t)
+                if s is not None and ntok[t] < forced[t] and not np.isnan(z[s]).any():
+                    zrec[t][ntok[t]] = z[s].copy()
+            for t, s in list(slot_of.items()):
+                if ntok[t] < forced[t]:
+                    ntok[t] += 1
+            del z
+        if st == GROUP_READY:
+            h = eng.harvest_finished(cap_recs=16)
             for r in h.records:
                 seg = slice(r["tok_offset"], r["tok_offset"] + r["len"])
                 gpu_tok[r["traj_id"]], gpu_lp[r["traj_id"]] = h.tokens[seg].tolist(), h.logprobs[seg].tolist()
@@ -105,46 +236,22 @@ def test_fullwidth_teacher_forced(shape, Q_g):
             eng.load_policy_weights(v)
     eng.close()
     torch.cuda.empty_cache()
-    assert sorted(gpu_tok) == list(range(Q_g)) and all(len(t) == cap for t in gpu_tok.values())
-    W = _oracle_weights(m)
-    mdl = Model(m, W)
-    invT = np.float32(1.0)
-    rels = []
-    excluded = checked = 0
-    for j, s in enumerate(rows):
-        prompt = [int(t) for t in toks[off[s]:off[s + 1]]]
-        gen = gpu_tok[s]
-        for n in range(STEPS):    # bit-exact sampler: the oracle's Gumbel-max on the GPU's logits
-            assert sample_row(zs[n][j], invT, cfg.sample_seed, n, s, 0)[0] == gen[n], (s, n)
-        seq = prompt + gen[:STEPS - 1]
-        zo_all = mdl.full_forward(seq)                     # logits at every position
-        for n in range(STEPS):
-            zo = zo_all[len(prompt) - 1 + n]
-            zg = zs[n][j].astype(np.float64)
-            rel = np.linalg.norm(zg - zo) / np.linalg.norm(zo)
-            rels.append(rel)
-            err = float(np.abs(zg - zo).max())
-            tok_o, lp_o, sc = sample_row(zo.astype(np.float32), invT, cfg.sample_seed, n, s, 0)
-            ss = np.sort(sc.astype(np.float64))
-            if ss[-1] - ss[-2] < 4 * err:
-                excluded += 1
-            else:
-                checked += 1
-                assert tok_o == gen[n], (s, n)
-            assert abs(gpu_lp[s][n] - lp_o) <= 4 * err + 1e-4, (s, n)
-    rels = np.array(rels)
-    print(f"{m.name}: logits rel-L2 mean {rels.mean():.2e} max {rels.max():.2e}; ids checked {checked}, "
-          f"near-tie excluded {excluded}")
-    assert rels.mean() <= 1e-2 and rels.max() <= 1.5e-2, rels
-    # near ties: with V >= 128k the top-2 Gumbel-perturbed score gap is ~Exp(1), so a
-    # 4x max-abs-error band of ~0.2 excludes ~20% of positions; most must still decide
-    assert checked >= 0.6 * (checked + excluded)
+    assert sorted(gpu_tok) == list(range(n))
+    assert [len(gpu_tok[t]) for t in range(n)] == forced
+    assert any(i.n_prefill_tokens == plens[8] and i.n_admitted == 1 for i in infos)   # the mixed pass ran
+    assert infos[0].n_prefill_tokens == sum(plens[:8])                               # chunked epoch-start prefill
+    for t in check_tids:
+        assert sorted(zrec[t]) == list(range(forced[t])), (t, sorted(zrec[t]))
+    mdl = Model(m, _oracle_weights(m))
+    cases = [(t, toks[t].tolist(), gpu_tok[t], gpu_lp[t], zrec[t]) for t in check_tids]
+    st = check_positions(mdl, cases, cfg.sample_seed, label="llama8b-L2 long context")
+    assert st["excluded"] <= 0.1 * (st["checked"] + st["excluded"])
 
 
 def test_fullwidth_qkv_finish_path():
     """The opt-in QKV handoff (srl_tuning.qkv_finish: split-K partials + the bias / RoPE /
     KV-append kernel) passes the same full-width parity test.  Subprocess: the
-    switch is read once per process."""
+    test harness applies the setting at session start (tests/conftest.py)."""
     import os
     import subprocess
     import sys
