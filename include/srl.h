@@ -270,7 +270,9 @@ int32_t srl_set_cache_bound(srl_engine* e, int32_t K);
  * Only the classes in the profile mask (bit SRL_K_*; default all) are bracketed
  * by CUDA events.  Event records sit between kernels, so they also cut the
  * programmatic (PDL) edges of the decode graph: with profiling off the graph
- * holds no events at all.  Changing either setting recaptures the graph. */
+ * holds no events at all.  Decode graphs are cached per (row bucket, bracketed
+ * class set), so switching the mask between steps -- e.g. every class on a
+ * sample of steps -- replays an already captured graph of each kind. */
 int32_t srl_set_profiling(srl_engine* e, int32_t on);
 int32_t srl_set_profile_mask(srl_engine* e, uint32_t class_mask);
 /* ms[SRL_K_NCLASS]: accumulated device milliseconds per class over decode steps

