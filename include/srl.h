@@ -101,18 +101,42 @@ typedef struct srl_sched_cfg {
  *   SRL_COMM_NCCL   one process per GPU; nccl_unique_id from srl_nccl_unique_id
  *                   on rank 0, shared by the caller (e.g. torch.distributed);
  *                   world may be 1 (a one-rank communicator: same code path).
+ *                   The communicator is created non-blocking and polled.
  *   SRL_COMM_LOCAL  `world` engines in one process, each driven by its own host
  *                   thread (any devices, several may share one GPU); local_group
  *                   from srl_local_group_create(world), destroyed after every
  *                   engine of the group.  Peer copies + CUDA events + a host
- *                   barrier (300 s timeout => SRL_E_NCCL on every rank).
+ *                   barrier.
+ *   SRL_COMM_HOST   caller callbacks (`host`, an srl_host_transport that must
+ *                   outlive the engine): rows staged through pinned host memory,
+ *                   exchanged by the caller -- e.g. over a torch.distributed gloo
+ *                   group, several processes sharing one GPU.  Slow; for tests
+ *                   and GPU-less interconnects.
+ * Failure handling: timeout_s (0 = 300 s) bounds communicator creation and every
+ * wait on a step / update that contains a collective.  An asynchronous transport
+ * error (ncclCommGetAsyncError) or a timeout aborts the communicator
+ * (ncclCommAbort) and the call returns SRL_E_NCCL; every later call on that
+ * engine returns SRL_E_NCCL too (destroy it).  A dead peer therefore fails the
+ * surviving ranks instead of hanging them.
  * All ranks must make the same sequence of srl_submit_prompts /
  * srl_decode_step / srl_harvest_finished / srl_load_policy_weights calls. */
-enum { SRL_COMM_NCCL = 0, SRL_COMM_LOCAL = 1 };
+enum { SRL_COMM_NCCL = 0, SRL_COMM_LOCAL = 1, SRL_COMM_HOST = 2 };
+/* SRL_COMM_HOST callbacks; return 0 on success, non-zero on failure.
+ *   allgather(ctx, buf, seg): buf holds world segments of seg bytes; this rank's
+ *     segment (offset rank*seg) is filled; on return every segment must hold its
+ *     owner's bytes.
+ *   broadcast(ctx, buf, bytes): rank 0's buf holds `bytes` bytes; on return every
+ *     rank's buf must hold them. */
+typedef struct srl_host_transport {
+  int32_t (*allgather)(void* ctx, void* buf, uint64_t seg_bytes);
+  int32_t (*broadcast)(void* ctx, void* buf, uint64_t bytes);
+  void* ctx;
+} srl_host_transport;
 typedef struct srl_comm {
   int32_t rank, world;
-  int32_t kind, pad_;
+  int32_t kind, timeout_s;
   void* local_group;
+  const srl_host_transport* host;
   uint8_t nccl_unique_id[128];
 } srl_comm;
 

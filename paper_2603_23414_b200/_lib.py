@@ -29,12 +29,19 @@ class SchedCfg(C.Structure):
                 ("sample_seed", _U64), ("max_traj", _I32), ("max_prompt", _I32), ("prefill_chunk", _I32)]
 
 
-COMM_NCCL, COMM_LOCAL = 0, 1   # srl.h SRL_COMM_*
+COMM_NCCL, COMM_LOCAL, COMM_HOST = 0, 1, 2   # srl.h SRL_COMM_*
+
+# srl_host_transport callbacks: int32 (*)(void* ctx, void* buf, uint64 bytes)
+HOST_FN = C.CFUNCTYPE(_I32, _P, _P, _U64)
+
+
+class HostTransport(C.Structure):
+    _fields_ = [("allgather", HOST_FN), ("broadcast", HOST_FN), ("ctx", _P)]
 
 
 class Comm(C.Structure):
-    _fields_ = [("rank", _I32), ("world", _I32), ("kind", _I32), ("pad_", _I32), ("local_group", _P),
-                ("nccl_unique_id", C.c_uint8 * 128)]
+    _fields_ = [("rank", _I32), ("world", _I32), ("kind", _I32), ("timeout_s", _I32), ("local_group", _P),
+                ("host", C.POINTER(HostTransport)), ("nccl_unique_id", C.c_uint8 * 128)]
 
 
 class Arena(C.Structure):

@@ -3,10 +3,12 @@
 // (gemm_tc.cu, layers.cu, attention.cu, sampler.cu, ctl.cu); this file plans
 // memory, chains the launches on the caller's stream and mirrors a handful
 // of host-side counters.
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <map>
 #include <string>
+#include <thread>
 #include <unordered_set>
 #include <vector>
 
@@ -283,6 +285,9 @@ struct srl_engine {
   std::map<std::pair<int, uint32_t>, Graph> graphs;
   int last_m = 0;  // decode rows of the last step
   bool mixed_ok = true;
+  long long comm_timeout_ms = 300000;
+  bool comm_dead = false;        // the replica transport failed or timed out: every call fails
+  cudaEvent_t ev_sync = nullptr;
   int launch_rc = 0;             // first failed launch of the current step (note_launch)
   const char* launch_what = "";
 };
@@ -679,8 +684,11 @@ int exchange_and_end(srl_engine* e) {
   std::string err;
   {
     Prof p(e, SRL_K_COMM);
-    if (e->comm->allgather_inplace(e->ctl.samp, 8ull * e->s.Q_g, e->st, err))
+    if (e->comm->allgather_inplace(e->ctl.samp, 8ull * e->s.Q_g, e->st, err)) {
+      e->comm->abort();
+      e->comm_dead = true;
       return fail(SRL_E_NCCL, "srl_decode_step: replica all-gather: " + err);
+    }
   }
   {
     Prof p(e, SRL_K_CTL);
@@ -690,9 +698,36 @@ int exchange_and_end(srl_engine* e) {
   return SRL_OK;
 }
 
-void read_status(srl_engine* e) {
+// Waits for the engine stream.  Alone: a plain synchronise.  With replicas the
+// stream may hold a collective whose peer died, so the wait is a poll with a
+// deadline that also watches the transport's asynchronous error; on either the
+// communicator is aborted and the engine is dead (SRL_E_NCCL from then on).
+int stream_wait(srl_engine* e, const char* what) {
+  if (!e->comm) {
+    const cudaError_t ce = cudaStreamSynchronize(e->st);
+    return ce == cudaSuccess ? 0 : cuda_fail(what, ce);
+  }
+  if (cudaEventRecord(e->ev_sync, e->st) != cudaSuccess) return cuda_fail(what);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaEventQuery(e->ev_sync);
+    if (q == cudaSuccess) return 0;
+    if (q != cudaErrorNotReady) return cuda_fail(what, q);
+    std::string err;
+    const bool late = std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(e->comm_timeout_ms);
+    if (e->comm->poll_error(err) || late) {
+      e->comm->abort();
+      e->comm_dead = true;
+      return fail(SRL_E_NCCL, std::string(what) + ": replica transport " + (late ? "timed out" : "failed: " + err) +
+                                  " -- communicator aborted");
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
+int read_status(srl_engine* e, const char* what = "status read-back") {
   cudaMemcpyAsync(e->hst, &e->ctl.s->st, sizeof(CtlStatus), cudaMemcpyDeviceToHost, e->st);
-  cudaStreamSynchronize(e->st);
+  return stream_wait(e, what);
 }
 
 }  // namespace
@@ -711,7 +746,7 @@ static int32_t finish_step(srl_engine* e, const CtlStatus& b, srl_step_info* inf
     return fail(SRL_E_CUDA, buf);
   }
   cudaEventRecord(e->ev1, st);
-  read_status(e);
+  if (int rc = read_status(e, "srl_decode_step")) return rc;
   if (cudaError_t ce = cudaGetLastError()) return cuda_fail("decode step", ce);
   prof_collect(e, e->direct, false);
   if (gset) prof_collect(e, *gset, true);
@@ -785,8 +820,9 @@ int32_t srl_create(const srl_model_cfg* m, const srl_sched_cfg* s, int32_t devic
   const int world = comm ? comm->world : 1;
   std::string why;
   if (validate(m, s, world, why)) return fail(SRL_E_INVALID_ARG, "srl_create: " + why);
-  if (comm && (comm->rank < 0 || comm->rank >= world || (comm->kind != SRL_COMM_NCCL && comm->kind != SRL_COMM_LOCAL)))
-    return fail(SRL_E_INVALID_ARG, "srl_create: bad srl_comm (rank / kind)");
+  if (comm && (comm->rank < 0 || comm->rank >= world || comm->kind < SRL_COMM_NCCL || comm->kind > SRL_COMM_HOST ||
+               comm->timeout_s < 0))
+    return fail(SRL_E_INVALID_ARG, "srl_create: bad srl_comm (rank / kind / timeout)");
   uint64_t wb, kb, sb;
   srl_arena_sizes(m, s, world, &wb, &kb, &sb);
   if (mem->weights_bytes < wb || mem->kv_bytes < kb || mem->scratch_bytes < sb || !mem->weights || !mem->kv || !mem->scratch)
@@ -804,8 +840,13 @@ int32_t srl_create(const srl_model_cfg* m, const srl_sched_cfg* s, int32_t devic
   e->use_graph = tuning().graphs != 0 && stream != nullptr;  // the legacy stream cannot be captured
   e->mixed_ok = tuning().mixed_prefill != 0;
   if (comm) {
-    e->comm = comm->kind == SRL_COMM_NCCL ? comm_create_nccl(comm->nccl_unique_id, comm->rank, world, why)
-                                          : comm_create_local(comm->local_group, comm->rank, world, why);
+    e->comm_timeout_ms = (comm->timeout_s > 0 ? comm->timeout_s : 300) * 1000LL;
+    if (comm->kind == SRL_COMM_NCCL)
+      e->comm = comm_create_nccl(comm->nccl_unique_id, comm->rank, world, (int)e->comm_timeout_ms, why);
+    else if (comm->kind == SRL_COMM_LOCAL)
+      e->comm = comm_create_local(comm->local_group, comm->rank, world, (int)e->comm_timeout_ms, why);
+    else
+      e->comm = comm_create_host(comm->host, comm->rank, world, why);
     if (!e->comm) {
       delete e;
       return fail(SRL_E_NCCL, "srl_create: replica communicator: " + why);
@@ -898,6 +939,7 @@ int32_t srl_create(const srl_model_cfg* m, const srl_sched_cfg* s, int32_t devic
   }
   cudaEventCreate(&e->ev0);
   cudaEventCreate(&e->ev1);
+  cudaEventCreateWithFlags(&e->ev_sync, cudaEventDisableTiming);
   if (cudaStreamSynchronize(e->st) != cudaSuccess) {
     delete e;
     return cuda_fail("srl_create init");
@@ -911,6 +953,7 @@ int32_t srl_destroy(srl_engine* e) {
   if (e->hst) cudaFreeHost(e->hst);
   if (e->ev0) cudaEventDestroy(e->ev0);
   if (e->ev1) cudaEventDestroy(e->ev1);
+  if (e->ev_sync) cudaEventDestroy(e->ev_sync);
   for (cudaEvent_t ev : e->direct.ev) cudaEventDestroy(ev);
   for (auto& kv : e->graphs) {
     for (cudaEvent_t ev : kv.second.gset.ev) cudaEventDestroy(ev);
@@ -979,6 +1022,7 @@ int32_t srl_submit_prompts(srl_engine* e, int32_t n, const uint64_t* prompt_ids,
 
 int32_t srl_decode_step(srl_engine* e, srl_step_info* info) {
   if (!e) return fail(SRL_E_INVALID_ARG, "srl_decode_step: null engine");
+  if (e->comm_dead) return fail(SRL_E_NCCL, "srl_decode_step: the replica transport failed earlier (destroy the engine)");
   if (info) {
     memset(info, 0, sizeof(*info));
     info->k = -1;
@@ -992,7 +1036,7 @@ int32_t srl_decode_step(srl_engine* e, srl_step_info* info) {
     ctl_begin(e->ctl, st);
   }
   e->launches++;
-  read_status(e);
+  if (int rc = read_status(e, "srl_decode_step")) return rc;
   if (cudaError_t ce = cudaGetLastError()) return cuda_fail("ctl_begin", ce);
   CtlStatus b = *e->hst;
   if (info) {
@@ -1068,10 +1112,11 @@ int32_t srl_decode_step(srl_engine* e, srl_step_info* info) {
 int32_t srl_harvest_finished(srl_engine* e, int32_t cap_recs, srl_traj* recs, int32_t* n_out, int32_t* toks,
                              float* logprobs, int32_t* versions, int64_t cap_toks) {
   if (!e) return fail(SRL_E_INVALID_ARG, "srl_harvest_finished: null engine");
+  if (e->comm_dead) return fail(SRL_E_NCCL, "srl_harvest_finished: the replica transport failed earlier");
   if (e->group_state != 1) return fail(SRL_E_STATE, "srl_harvest_finished: no group is ready");
   ctl_harvest(e->ctl, e->st);
   e->launches++;
-  read_status(e);
+  if (int rc = read_status(e, "srl_harvest_finished")) return rc;
   const CtlStatus& h = *e->hst;
   if (h.status == SRL_E_CAPACITY) return fail(SRL_E_CAPACITY, "srl_harvest_finished: engine staging too small");
   const int n = h.group_n;
@@ -1084,7 +1129,7 @@ int32_t srl_harvest_finished(srl_engine* e, int32_t cap_recs, srl_traj* recs, in
   if (versions) cudaMemcpyAsync(versions, e->ctl.h_ver, 4 * total, cudaMemcpyDeviceToHost, e->st);
   const int two = 2;
   cudaMemcpyAsync(&e->ctl.s->group_state, &two, 4, cudaMemcpyHostToDevice, e->st);
-  if (cudaStreamSynchronize(e->st) != cudaSuccess) return cuda_fail("srl_harvest_finished");
+  if (int rc = stream_wait(e, "srl_harvest_finished")) return rc;
   for (int i = 0; i < n; ++i) {
     const long long pi = recs[i].prompt_id;
     recs[i].prompt_id = (pi >= 0 && pi < (long long)e->prompt_ids.size()) ? (int64_t)e->prompt_ids[pi] : -1;
@@ -1095,6 +1140,7 @@ int32_t srl_harvest_finished(srl_engine* e, int32_t cap_recs, srl_traj* recs, in
 
 int32_t srl_load_policy_weights(srl_engine* e, const void* flat_w, int64_t version) {
   if (!e) return fail(SRL_E_INVALID_ARG, "srl_load_policy_weights: null engine");
+  if (e->comm_dead) return fail(SRL_E_NCCL, "srl_load_policy_weights: the replica transport failed earlier");
   if (e->group_state == 1) return fail(SRL_E_STATE, "srl_load_policy_weights: harvest the ready group first");
   if (version < 0 || (e->v_valid && version <= e->v))
     return fail(SRL_E_STATE, "srl_load_policy_weights: policy version must increase");
@@ -1142,11 +1188,15 @@ int32_t srl_load_policy_weights(srl_engine* e, const void* flat_w, int64_t versi
     rr.push_back({e->W + e->pk.base, e->pk.total - e->pk.base});
     std::string err;
     Prof p(e, SRL_K_COMM);
-    if (e->comm->broadcast_inplace(rr, e->st, err)) return fail(SRL_E_NCCL, "srl_load_policy_weights: broadcast: " + err);
+    if (e->comm->broadcast_inplace(rr, e->st, err)) {
+      e->comm->abort();
+      e->comm_dead = true;
+      return fail(SRL_E_NCCL, "srl_load_policy_weights: broadcast: " + err);
+    }
   }
   ctl_bump(e->ctl, (int)version, e->st);
   e->launches++;
-  read_status(e);
+  if (int rc = read_status(e, "srl_load_policy_weights")) return rc;
   if (cudaError_t ce = cudaGetLastError()) return cuda_fail("srl_load_policy_weights", ce);
   if (e->hst->status < 0) return fail(e->hst->status, "srl_load_policy_weights: capacity (resumed list)");
   e->v = version;

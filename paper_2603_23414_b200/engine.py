@@ -12,7 +12,8 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from ._lib import COMM_LOCAL, COMM_NCCL, Arena, Comm, ModelCfg, SchedCfg, StepInfo, TraceRec, TrajRec, check
+from ._lib import (COMM_HOST, COMM_LOCAL, COMM_NCCL, HOST_FN, Arena, Comm, HostTransport, ModelCfg, SchedCfg,
+                   StepInfo, TraceRec, TrajRec, check)
 
 OK, GROUP_READY, DONE = 0, 1, 2
 EV_NAMES = {0: "STEP", 1: "LOAD", 2: "ADMIT", 3: "PREEMPT", 4: "FINISH", 5: "EMIT", 6: "DISCARD", 7: "SCAVENGE",
@@ -35,6 +36,52 @@ def share_nccl_unique_id(dist, rank: int) -> bytes:
     obj = [nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     return obj[0]
+
+
+class HostGroup:
+    """SRL_COMM_HOST: the replica exchange through caller callbacks.  `allgather(buf)`
+    receives a uint8 numpy view of `world` equal segments (this rank's filled) and
+    must fill the rest; `broadcast(buf)` a uint8 view that rank 0 filled.  Each
+    returns nothing and raises on failure (the engine then reports SRL_E_NCCL).
+    `gloo(dist)` builds one over a torch.distributed (e.g. gloo) process group."""
+
+    def __init__(self, allgather, broadcast):
+        def wrap(fn):
+            def cb(ctx, buf, n):
+                try:
+                    fn(np.ctypeslib.as_array(C.cast(buf, C.POINTER(C.c_uint8)), shape=(int(n) if fn is broadcast
+                                                                                     else int(n) * self.world,)))
+                    return 0
+                except Exception as exc:   # noqa: BLE001 -- reported through the C status
+                    self.error = exc
+                    return 1
+            return HOST_FN(cb)
+        self.world = None
+        self.error = None
+        self._cbs = (wrap(allgather), wrap(broadcast))      # kept alive with the group
+        self.t = HostTransport(self._cbs[0], self._cbs[1], None)
+
+    @classmethod
+    def gloo(cls, dist):
+        import torch
+        world = dist.get_world_size()
+        rank = dist.get_rank()
+
+        def allgather(buf):
+            seg = buf.size // world
+            mine = torch.from_numpy(buf[rank * seg:(rank + 1) * seg].copy())
+            outs = [torch.empty(seg, dtype=torch.uint8) for _ in range(world)]
+            dist.all_gather(outs, mine)
+            for r in range(world):
+                buf[r * seg:(r + 1) * seg] = outs[r].numpy()
+
+        def broadcast(buf):
+            t = torch.from_numpy(buf.copy()) if rank == 0 else torch.empty(buf.size, dtype=torch.uint8)
+            dist.broadcast(t, src=0)
+            buf[:] = t.numpy()
+        g = cls(allgather, broadcast)
+        g.world = world
+        return g
 
 
 class LocalGroup:
@@ -67,7 +114,8 @@ class RolloutEngine:
 
     def __init__(self, model, sched, *, max_traj: int, max_prompt: int, prefill_chunk: int = 2048,
                  device: int = 0, stream=None, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
-                 local_group: LocalGroup | None = None, compact_weights: bool = False):
+                 local_group: LocalGroup | None = None, host_group: HostGroup | None = None,
+                 compact_weights: bool = False, comm_timeout_s: int = 0):
         """world > 1 (or an explicit nccl_id / local_group) makes this engine rank
         `rank` of a lockstep replica group: NCCL when `nccl_id` is given (one process
         per GPU), in-process when `local_group` is."""
@@ -95,17 +143,23 @@ class RolloutEngine:
         self.stream = stream if stream is not None else torch.cuda.Stream(self.dev)
         arena = Arena(self.W.data_ptr(), self.KV.data_ptr(), self.S.data_ptr(), wb.value, kb.value, sb.value)
         comm = None
-        if world > 1 or nccl_id is not None or local_group is not None:
-            if (nccl_id is None) == (local_group is None):
-                raise ValueError("a replica engine needs exactly one of nccl_id / local_group")
+        transports = [x for x in (nccl_id, local_group, host_group) if x is not None]
+        if world > 1 or transports:
+            if len(transports) != 1:
+                raise ValueError("a replica engine needs exactly one of nccl_id / local_group / host_group")
             comm = Comm()
-            comm.rank, comm.world = rank, world
+            comm.rank, comm.world, comm.timeout_s = rank, world, int(comm_timeout_s)
             if nccl_id is not None:
                 comm.kind = COMM_NCCL
                 C.memmove(comm.nccl_unique_id, nccl_id, 128)
-            else:
+            elif local_group is not None:
                 comm.kind = COMM_LOCAL
                 comm.local_group = local_group.h
+            else:
+                comm.kind = COMM_HOST
+                host_group.world = world
+                comm.host = C.pointer(host_group.t)
+                self._host_group = host_group      # the callbacks must outlive the engine
         self.h = C.c_void_p()
         check(self.lib.srl_create(C.byref(self.m), C.byref(self.s), device, C.c_void_p(self.stream.cuda_stream),
                                   C.byref(arena), C.byref(comm) if comm else None, C.byref(self.h)), "srl_create")

@@ -5,7 +5,9 @@ controller (oracle/sched.py, global slot g = s*R + r, reading R24).
 One B200 is available, so R engines share cuda:0 in one process, each driven
 by its own host thread, exchanging through the in-process transport
 (SRL_COMM_LOCAL); the NCCL transport runs as a one-rank communicator (the same
-calls a multi-GPU launch makes).  Checked per rank:
+calls a multi-GPU launch makes); and R PROCESSES share cuda:0 exchanging through
+the host-callback transport (SRL_COMM_HOST over a torch.distributed gloo group):
+libsrl's replica protocol across process boundaries.  Checked per rank:
 * event log and (k, r_k) trace bit-exact vs oracle Controller(R, Q_g);
 * every rank emits the same groups with identical tokens / logprobs / versions
   (the replicated state really is replicated);
@@ -202,3 +204,119 @@ def test_nccl_transport_one_rank():
     c, og = _oracle(cfg, off, toks, L)
     _compare(res, c, og)
     assert prof is not None
+
+
+# ------------------------------------------------------------------ across processes (SRL_COMM_HOST + gloo)
+def _w_host_replica(rank, port, world, over, outdir):
+    import os
+    import pickle
+
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2603_23414_b200.engine import HostGroup
+    cfg = SchedConfig(**dict(dict(Q_g=8, U=4, pool_prompts=16, cap=64, kv_pages=256, kv_dtype=KV_BF16, R=world),
+                             **over))
+    off, toks, L = tiny_workload(n_prompts=16)
+    eng = make_engine(TINY, cfg, max_traj=64, max_prompt=16, rank=rank, world=world, host_group=HostGroup.gloo(dist))
+    res = run_engine(eng, TINY, off, toks, L)           # refreshed weights broadcast from rank 0 every update
+    cnt = eng.counters()
+    eng.close()
+    out = dict(events=res["events"], steps=res["steps"], counters=cnt,
+               groups=[(v, [dict(r) for r in h.records], h.tokens, h.logprobs, h.versions) for h, v in res["groups"]])
+    with open(os.path.join(outdir, f"r{rank}.pkl"), "wb") as fh:
+        pickle.dump(out, fh)
+    dist.destroy_process_group()
+
+
+HOST_CASES = [("R2_partial", dict(K=K_INF)), ("R2_K1_eos", dict(K=1, stop=STOP_EOS, eos_id=7)),
+              ("R3_onpolicy", dict(K=0, Q_g=4))]
+
+
+@pytest.mark.parametrize("name,over", HOST_CASES, ids=[c[0] for c in HOST_CASES])
+def test_replicas_across_processes_host_transport(tmp_path, name, over):
+    """World-R processes, one engine each (all on cuda:0), exchanging the per-step
+    [R][2][Q_g] rows and the refreshed policy through gloo: every rank's event log
+    equals oracle Controller(R) bit for bit and the groups are identical on all
+    ranks (tokens, logprob bits, versions)."""
+    import pickle
+    import socket
+
+    import torch.multiprocessing as mp
+    world = 3 if name.startswith("R3") else 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    mp.start_processes(_w_host_replica, args=(port, world, over, str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    outs = [pickle.load(open(tmp_path / f"r{r}.pkl", "rb")) for r in range(world)]
+    cfg = SchedConfig(**dict(dict(Q_g=8, U=4, pool_prompts=16, cap=64, kv_pages=256, kv_dtype=KV_BF16, R=world),
+                             **over))
+    off, toks, L = tiny_workload(n_prompts=16)
+    if cfg.stop == STOP_EOS:   # EOS stops depend on the tokens: compare the ranks with each other and
+        c = None               # the schedule with the single-process R-replica run instead
+        ref = _run_replicas(cfg, off, toks, L)[0]
+        assert outs[0]["events"] == ref["events"] and outs[0]["steps"] == ref["steps"]
+    else:
+        c, og = _oracle(cfg, off, toks, L)
+        assert outs[0]["events"] == c.events and outs[0]["steps"] == c.trace
+        assert [[r["traj_id"] for r in g[1]] for g in outs[0]["groups"]] == [[r["traj_id"] for r in recs]
+                                                                              for recs, _ in og]
+    for o in outs[1:]:
+        assert o["events"] == outs[0]["events"] and o["steps"] == outs[0]["steps"]
+        assert o["counters"]["raw_tokens"] == outs[0]["counters"]["raw_tokens"]
+        for g, g0 in zip(o["groups"], outs[0]["groups"]):
+            assert g[0] == g0[0] and [r["traj_id"] for r in g[1]] == [r["traj_id"] for r in g0[1]]
+            assert np.array_equal(g[2], g0[2]) and np.array_equal(g[3].view(np.int32), g0[3].view(np.int32))
+            assert np.array_equal(g[4], g0[4])
+
+
+def test_replica_peer_failure_fails_fast_not_hang():
+    """A rank that stops participating (dies) must not hang the others: with a 5 s
+    transport timeout the surviving rank's srl_decode_step returns SRL_E_NCCL
+    (communicator aborted) and every later call keeps failing."""
+    import time
+
+    from paper_2603_23414_b200._lib import SRLError
+    from paper_2603_23414_b200.engine import LocalGroup
+    cfg = SchedConfig(Q_g=8, U=4, R=2, pool_prompts=16, cap=64, kv_pages=256, kv_dtype=KV_BF16)
+    off, toks, L = tiny_workload(n_prompts=16)
+    grp = LocalGroup(2)
+    res = {}
+
+    def work(r):
+        torch.cuda.set_device(0)
+        eng = make_engine(TINY, cfg, max_traj=64, max_prompt=16, rank=r, world=2, local_group=grp,
+                          comm_timeout_s=5)
+        eng.submit_prompts(np.arange(16, dtype=np.uint64) + 1000, off, toks, L)
+        for _ in range(3):
+            eng.decode_step()
+        if r == 1:
+            res[1] = "stopped"     # rank 1 "dies": never calls again
+            return
+        t0 = time.time()
+        try:
+            for _ in range(100):
+                eng.decode_step()
+            res[0] = ("no error", time.time() - t0)
+        except SRLError as ex:
+            res[0] = (str(ex), time.time() - t0)
+            try:
+                eng.decode_step()
+                res["after"] = "no error"
+            except SRLError as ex2:
+                res["after"] = str(ex2)
+        eng.close()
+
+    th = [threading.Thread(target=work, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    assert not any(t.is_alive() for t in th), "a rank hung"
+    grp.close()
+    msg, dt = res[0]
+    assert "(-7)" in msg and dt < 60, res
+    assert "(-7)" in res["after"], res

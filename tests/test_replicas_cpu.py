@@ -165,3 +165,33 @@ def test_bench_whole_job_aggregation(tmp_path):
         assert mx == 20.0                                     # max over ranks
         assert tok_s == pytest.approx(4000.0 / 20e-3)         # all ranks' tokens / slowest rank's time
         assert useful_s == pytest.approx(1000.0 / 20e-3)
+
+
+# ------------------------------------------------------------------ SRL_COMM_HOST callbacks over gloo
+def _w_host_transport(rank, port, outdir):
+    """The srl_host_transport callbacks HostGroup.gloo builds, invoked exactly as
+    libsrl invokes them (through the C function pointers, on a raw byte buffer)."""
+    import ctypes as C
+    _init(rank, port)
+    from paper_2603_23414_b200.engine import HostGroup
+    hg = HostGroup.gloo(dist)
+    seg = 24
+    buf = (C.c_uint8 * (seg * WORLD))()
+    for i in range(seg):
+        buf[rank * seg + i] = (rank * 37 + i) & 0xFF
+    rc = hg.t.allgather(None, C.cast(buf, C.c_void_p), seg)
+    gathered = bytes(buf)
+    bbuf = (C.c_uint8 * 10)()
+    if rank == 0:
+        for i in range(10):
+            bbuf[i] = 200 + i
+    rc2 = hg.t.broadcast(None, C.cast(bbuf, C.c_void_p), 10)
+    np.save(os.path.join(outdir, f"host{rank}.npy"), np.frombuffer(gathered + bytes(bbuf) + bytes([rc, rc2]), np.uint8))
+    dist.destroy_process_group()
+
+
+def test_host_transport_callbacks_over_gloo(tmp_path):
+    _spawn(_w_host_transport, str(tmp_path))
+    want = bytes(((r * 37 + i) & 0xFF) for r in range(WORLD) for i in range(24)) + bytes(range(200, 210)) + b"\0\0"
+    for r in range(WORLD):
+        assert np.load(tmp_path / f"host{r}.npy").tobytes() == want
