@@ -17,4 +17,6 @@ Modules
   attention  brute-force softmax attention over a paged KV cache
   sched    the SortedRL controller / rollout buffer state machine
   metrics  bubble ratio Eq. (bubble), throughput, staleness, curriculum
+  learner  the update group's consumer: Eq. (1) clipped objective, Eq. (2) GAE,
+           Eq. (3) Reinforce++ advantages, token staleness
 """
