@@ -40,7 +40,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 from workload.configs import (BARRIER_ADMITTED, BARRIER_TRAINED, K_INF, KV_BF16, LLAMA8B, MODE_POSTHOC,  # noqa: E402
-                              MODE_SORTED, MODE_SYNC, QWEN32B, RESUME_KEEP_KV,
+                              MODE_SORTED, MODE_SYNC, QWEN32B, RESUME_KEEP_KV, RESUME_REPREFILL,
                               STOP_FORCED, SchedConfig)
 from workload.lengths import LengthModel, sample_lengths  # noqa: E402
 from workload.prompts import make_prompts  # noqa: E402
@@ -221,7 +221,8 @@ def run_gpu(args, rank, world, dist):
     # scheduler variants (the paper's comparisons; defaults = SortedRL partial mode)
     sched = dataclasses.replace(sched, mode={"sorted": MODE_SORTED, "sync": MODE_SYNC, "posthoc": MODE_POSTHOC}[args.mode],
                                 K=args.K, U=args.U,
-                                barrier={"trained": BARRIER_TRAINED, "admitted": BARRIER_ADMITTED}[args.barrier])
+                                barrier={"trained": BARRIER_TRAINED, "admitted": BARRIER_ADMITTED}[args.barrier],
+                                resume={"keep_kv": RESUME_KEEP_KV, "reprefill": RESUME_REPREFILL}[args.resume])
     off, toks, L = workload_inputs(world, epochs=EPOCHS, pool=pool, V=model.V, cap=cap)
     ids = np.arange(len(off) - 1, dtype=np.uint64) + 1
     max_traj = EPOCHS * pool * world
@@ -550,6 +551,9 @@ def main():
     ap.add_argument("--K", type=int, default=K_INF, help="cache bound in policy versions (-1 = inf, 0 = on-policy)")
     ap.add_argument("--U", type=int, default=64, help="update group size")
     ap.add_argument("--barrier", default="trained", choices=["trained", "admitted"], help="cache-aware loading barrier")
+    ap.add_argument("--resume", default="keep_kv", choices=["keep_kv", "reprefill"],
+                    help="how kept partial trajectories resume (reading R10): keep their KV (default) or re-prefill "
+                         "prompt + generated tokens (P:180 literal)")
     ap.add_argument("--prof-every", type=int, default=8,
                     help="every class is bracketed by events on one decode step in this many (the breakdown); "
                          "the rest bracket attention only (the roofline)")
@@ -649,7 +653,8 @@ def main():
         "warmup": r.get("warmup_rounds", args.warmup), "ms_per_step": ms / max(1, steps), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": MODELS[args.model][7] or WORKLOAD,
-                   "scheduler": {"mode": args.mode, "K": args.K, "U": args.U, "barrier": args.barrier},
+                   "scheduler": {"mode": args.mode, "K": args.K, "U": args.U, "barrier": args.barrier,
+                                 "resume": args.resume},
                    "step": "one early-update round: decode steps (refill, prefill, decode GEMMs, paged attention, "
                            "Philox sampling, stop detection, compaction) until the length-sorted update group of "
                            f"U={args.U} is ready, its harvest, and the policy refresh (load_policy_weights, K bound)",

@@ -247,6 +247,15 @@ int32_t srl_decode_step(srl_engine* e, srl_step_info* info);
 int32_t srl_harvest_finished(srl_engine* e, int32_t cap_recs, srl_traj* recs, int32_t* n_out, int32_t* toks,
                              float* logprobs, int32_t* versions, int64_t cap_toks);
 
+/* Device views of the group the last srl_harvest_finished copied out (the same
+ * data: tokens / behaviour logprobs / generating versions concatenated in group
+ * order, and the records with prompt_id = the engine's prompt index), for a
+ * trainer on the same GPU (srl_learner.h) without a host round trip.  Valid
+ * until the next srl_harvest_finished (also across srl_load_policy_weights);
+ * *n_tok = total tokens.  SRL_E_STATE if nothing has been harvested yet. */
+int32_t srl_harvest_device(srl_engine* e, const int32_t** toks, const float** logprobs, const int32_t** versions,
+                           const srl_traj** recs, int32_t* n_recs, int64_t* n_tok);
+
 /* Collective over the replicas.  Install policy version `version` (> current;
  * the first call may use any version >= 0).  flat_w: device pointer to a flat
  * weight image (srl_weight_offset layout) on rank 0 (ignored elsewhere), or

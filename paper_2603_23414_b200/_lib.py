@@ -110,6 +110,13 @@ SIGNATURES = {
     "srl_load_policy_tensor": (_I32, [_P, C.c_char_p, _P]),
     "srl_local_group_create": (_I32, [_I32, C.POINTER(_P)]),
     "srl_local_group_destroy": (_I32, [_P]),
+    "srl_harvest_device": (_I32, [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P), C.POINTER(_P), _I32P, _I64P]),
+    "srl_learner_reinforcepp": (_I32, [_P, _I32, _P, _P]),
+    "srl_learner_expand": (_I32, [_P, _P, _I32, _P, _P]),
+    "srl_learner_gae": (_I32, [_P, _P, _P, _I32, C.c_float, C.c_float, _P, _P]),
+    "srl_learner_ppo_workspace": (_I64, [_I64]),
+    "srl_learner_ppo_objective": (_I32, [_P, _P, _P, _I64, C.c_float, C.c_float, _P, _P, _P, _P, _P]),
+    "srl_learner_staleness": (_I32, [_P, _I64, _I32, _I32, _P, _P]),
     "srl_default_tuning": (None, [C.POINTER(Tuning)]),
     "srl_get_tuning": (_I32, [C.POINTER(Tuning)]),
     "srl_set_tuning": (_I32, [C.POINTER(Tuning)]),

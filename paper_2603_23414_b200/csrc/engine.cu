@@ -286,7 +286,10 @@ struct srl_engine {
   int last_m = 0;  // decode rows of the last step
   bool mixed_ok = true;
   long long comm_timeout_ms = 300000;
-  bool comm_dead = false;        // the replica transport failed or timed out: every call fails
+  bool comm_dead = false;
+  long long last_harvest_tok = 0;  // tokens / records of the last harvested group (srl_harvest_device)
+  int last_harvest_n = 0;
+  bool harvest_valid = false;        // the replica transport failed or timed out: every call fails
   cudaEvent_t ev_sync = nullptr;
   int launch_rc = 0;             // first failed launch of the current step (note_launch)
   const char* launch_what = "";
@@ -1114,6 +1117,7 @@ int32_t srl_harvest_finished(srl_engine* e, int32_t cap_recs, srl_traj* recs, in
   if (!e) return fail(SRL_E_INVALID_ARG, "srl_harvest_finished: null engine");
   if (e->comm_dead) return fail(SRL_E_NCCL, "srl_harvest_finished: the replica transport failed earlier");
   if (e->group_state != 1) return fail(SRL_E_STATE, "srl_harvest_finished: no group is ready");
+  e->harvest_valid = false;  // the staging buffers are rewritten now
   ctl_harvest(e->ctl, e->st);
   e->launches++;
   if (int rc = read_status(e, "srl_harvest_finished")) return rc;
@@ -1121,6 +1125,8 @@ int32_t srl_harvest_finished(srl_engine* e, int32_t cap_recs, srl_traj* recs, in
   if (h.status == SRL_E_CAPACITY) return fail(SRL_E_CAPACITY, "srl_harvest_finished: engine staging too small");
   const int n = h.group_n;
   const long long total = h.m_pre;
+  e->last_harvest_tok = total;
+  e->last_harvest_n = n;
   if (n_out) *n_out = n;
   if (n > cap_recs || total > cap_toks || !recs) return fail(SRL_E_CAPACITY, "srl_harvest_finished: caller buffers too small");
   cudaMemcpyAsync(recs, e->ctl.h_rec, sizeof(srl_traj) * n, cudaMemcpyDeviceToHost, e->st);
@@ -1135,6 +1141,20 @@ int32_t srl_harvest_finished(srl_engine* e, int32_t cap_recs, srl_traj* recs, in
     recs[i].prompt_id = (pi >= 0 && pi < (long long)e->prompt_ids.size()) ? (int64_t)e->prompt_ids[pi] : -1;
   }
   e->group_state = 2;
+  e->harvest_valid = true;
+  return SRL_OK;
+}
+
+int32_t srl_harvest_device(srl_engine* e, const int32_t** toks, const float** logprobs, const int32_t** versions,
+                           const srl_traj** recs, int32_t* n_recs, int64_t* n_tok) {
+  if (!e) return fail(SRL_E_INVALID_ARG, "srl_harvest_device: null engine");
+  if (!e->harvest_valid) return fail(SRL_E_STATE, "srl_harvest_device: no harvested group");
+  if (toks) *toks = e->ctl.h_tok;
+  if (logprobs) *logprobs = e->ctl.h_lp;
+  if (versions) *versions = e->ctl.h_ver;
+  if (recs) *recs = e->ctl.h_rec;
+  if (n_recs) *n_recs = e->last_harvest_n;
+  if (n_tok) *n_tok = e->last_harvest_tok;
   return SRL_OK;
 }
 

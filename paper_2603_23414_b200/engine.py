@@ -190,6 +190,26 @@ class RolloutEngine:
         """Order the engine stream after work torch queued on the current stream."""
         self.stream.wait_stream(self.torch.cuda.current_stream(self.dev))
 
+    def harvest_device(self):
+        """Device views (torch tensors, no copy) of the last harvested group: tokens,
+        behaviour logprobs, generating versions (srl_harvest_device), the record
+        count and the token count; the records' tok_offset / len (from the host
+        harvest of the same group) give the ragged offsets."""
+        import torch
+        t, lp, ver, recs = C.c_void_p(), C.c_void_p(), C.c_void_p(), C.c_void_p()
+        n, ntok = C.c_int32(), C.c_int64()
+        check(self.lib.srl_harvest_device(self.h, C.byref(t), C.byref(lp), C.byref(ver), C.byref(recs), C.byref(n),
+                                          C.byref(ntok)), "srl_harvest_device")
+
+        class _View:
+            def __init__(self, ptr, typestr, count, dev):
+                self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr, "data": (ptr, False),
+                                                 "version": 3, "strides": None}
+        dev = self.dev
+        mk = lambda ptr, ts: torch.as_tensor(_View(ptr.value or 0, ts, ntok.value, dev), device=dev)  # noqa: E731
+        return dict(tokens=mk(t, "<i4"), logprobs=mk(lp, "<f4"), versions=mk(ver, "<i4"), n_records=n.value,
+                    n_tokens=ntok.value)
+
     def load_policy_weights(self, version: int, flat=None):
         self._sync_in()
         ptr = C.c_void_p(flat.data_ptr()) if flat is not None else None
