@@ -188,3 +188,50 @@ def test_sampler_ties_lowest_index():
         tok, _, s = sample_row(z, np.float32(1.0), 3, 0, 0, 0)
         assert s[i] == s[j] == s.max()
         assert tok == i
+
+
+# ------------------------------------------------------------------ top-k / top-p (N4)
+def test_truncation_set_definitions():
+    """top-k keeps the k best by (logit desc, index asc); top-p the shortest ranked
+    prefix reaching mass p under the (top-k) softmax, including the crossing token."""
+    from oracle.sampler import truncation_set
+    z = np.log(np.array([0.1, 0.4, 0.2, 0.2, 0.05, 0.05])).astype(np.float32)
+    m, _, _ = truncation_set(z, top_k=3)
+    assert m.tolist() == [False, True, True, True, False, False]          # ties 0.2/0.2 both in, 0.1 out
+    m, _, _ = truncation_set(z, top_k=2)
+    assert m.tolist() == [False, True, True, False, False, False]         # tie broken by the lower index
+    m, lo, hi = truncation_set(z, top_p=0.5)
+    assert m.tolist() == [False, True, True, False, False, False] and abs(hi - 0.6) < 1e-6
+    m, lo, hi = truncation_set(z, top_p=0.39)
+    assert m.tolist() == [False, True, False, False, False, False]        # the first token already reaches p
+    m, lo, hi = truncation_set(z, top_p=0.41)
+    assert m.tolist() == [False, True, True, False, False, False]         # the crossing token is included
+    m, _, _ = truncation_set(z, top_k=3, top_p=0.55)                      # renormalised over top-3: .5 .25 .25
+    assert m.tolist() == [False, True, True, False, False, False]
+    m, _, _ = truncation_set(z, top_k=3, top_p=0.45)
+    assert m.tolist() == [False, True, False, False, False, False]
+    m, _, _ = truncation_set(z, top_k=0, top_p=1.0)
+    assert m.all()
+
+
+def test_top_k_one_is_greedy_and_logprob_zero():
+    z = np.random.default_rng(4).normal(size=1000).astype(np.float32)
+    for n in range(5):
+        tok, lp, _ = sample_row(z, np.float32(1.0), 3, n, 7, 0, top_k=1)
+        assert tok == int(np.argmax(z)) and lp == 0.0
+
+
+def test_top_p_draws_follow_the_renormalised_distribution():
+    """Gumbel-max over the truncation set samples softmax restricted to it (chi-square),
+    and the returned logprob is the log of that renormalised probability."""
+    from scipy.stats import chisquare
+    p = np.array([0.3, 0.25, 0.2, 0.15, 0.06, 0.04])
+    z = np.log(p).astype(np.float32)
+    q = p[:3] / p[:3].sum()                       # top_p 0.7 keeps 0.3 + 0.25 + 0.2 = 0.75
+    counts = np.zeros(6)
+    for n in range(12000):
+        tok, lp, _ = sample_row(z, np.float32(1.0), 5, n, 1, 0, top_p=0.7)
+        counts[tok] += 1
+        assert abs(lp - np.log(q[tok])) < 1e-6
+    assert counts[3:].sum() == 0
+    assert chisquare(counts[:3], q * counts.sum()).pvalue > 1e-3
