@@ -89,6 +89,12 @@ typedef struct srl_sched_cfg {
   float temperature;
   uint64_t sample_seed;
   int32_t max_traj, max_prompt, prefill_chunk;
+  /* N4 truncated sampling: top_k > 0 draws from the k best tokens (logit desc,
+   * index asc); top_p < 1 then from the shortest ranked prefix of the top-k
+   * softmax whose mass reaches top_p.  The cached behaviour logprob is that of
+   * the truncated, renormalised distribution.  0 / 1 = off (R14). */
+  int32_t top_k;
+  float top_p;
 } srl_sched_cfg;
 
 /* Data-parallel replicas (rows a14, a17).  R = world engines run

@@ -79,6 +79,17 @@ int32_t srl_op_sample(const float* logits, int32_t M, int32_t V, const int32_t* 
                       const int32_t* row_restarts, float temperature, uint64_t seed, const int32_t* row_active,
                       int32_t* tok_out, float* lp_out, void* stream);
 
+/* The same with truncated sampling (srl_sched_cfg.top_k / top_p):
+ * the argmax runs over the truncation set only -- the top_k best tokens by
+ * (z/T desc, index asc) (0 = all), then the shortest ranked prefix whose mass
+ * under their softmax reaches top_p (1 = all; the crossing token included) --
+ * and lp_out is the log-probability under that truncated, renormalised
+ * distribution.  The set is found by radix selection with integer fixed-point
+ * masses (deterministic).  Errors: -1 for top_k < 0 or top_p outside (0, 1]. */
+int32_t srl_op_sample_trunc(const float* logits, int32_t M, int32_t V, const int32_t* row_n, const int32_t* row_traj,
+                            const int32_t* row_restarts, float temperature, uint64_t seed, int32_t top_k, float top_p,
+                            const int32_t* row_active, int32_t* tok_out, float* lp_out, void* stream);
+
 /* Thread-local description of the last error (never NULL). */
 const char* srl_last_error(void);
 

@@ -180,9 +180,10 @@ class ModelRunner:
     own logits / sample for comparison in `self.log`)."""
 
     def __init__(self, m: ModelShape, weights_for, prompts, seed: int, temperature: float = 1.0,
-                 teacher=None, record_logits=False):
+                 teacher=None, record_logits=False, top_k: int = 0, top_p: float = 1.0):
         from .sampler import inv_temperature
         self.m = m
+        self.top_k, self.top_p = top_k, top_p
         self.weights_for = weights_for
         self.prompts = prompts          # traj -> prompt token list  (callable)
         self.seed = seed
@@ -221,7 +222,7 @@ class ModelRunner:
             pos = len(prompt) + n - 1
             x = mdl.decode_token(tok_in, pos, self.kv[t.tid])
             z = mdl.logits(x).astype(np.float32)
-            tok, lp, s = sample_row(z, self.invT, self.seed, n, t.tid, t.restarts)
+            tok, lp, s = sample_row(z, self.invT, self.seed, n, t.tid, t.restarts, self.top_k, self.top_p)
             if self.record_logits:
                 self.log.append(dict(k=self.k, g=g, tid=t.tid, n=n, restarts=t.restarts, logits=z, tok=tok, lp=lp,
                                      scores=s))

@@ -14,6 +14,8 @@ TEST INFRASTRUCTURE ONLY (oracle/__init__.py).  Written from PAPER.md:
   P:353 §4.4.3    group size n: pool of n*b prompts, no reload until every sample
                   of the current buffer has been fed to the trainer
   P:338–342       Eq. (bubble) trace records (k, r_k)
+  P:235, P:387    G > 1 responses per prompt; RadixAttention-style sharing of the
+                  prompt's KV pages among them (`share_prefix`)
 and the DESIGN.md readings R1–R28 (SURVEY §8(c) O-C pseudo-code).  The two
 paper modes are the cache bound K (policy versions) at its extremes: K = 0 is
 fully on-policy, K = inf is partial mode; intermediate K generalises them.
@@ -59,6 +61,7 @@ class Traj:
     state: str = "stream"       # stream | pending | running | ready | emitted
     slot: int = -1
     pages: int = 0
+    shared: int = 0             # prompt-prefix pages held through the replica's shared entry
     fresh: bool = True
 
 
@@ -113,6 +116,10 @@ class Controller:
         self.emitted = 0
         self.work_conserving: List[bool] = []
         self._page_blocked = False
+        # N4 prompt-prefix sharing: per (replica, prompt index) the shared entry's
+        # holder count and the policy version its KV was computed under
+        self.pfx_ref = {}
+        self.pfx_tag = {}
 
     # ------------------------------------------------------------ submission
     def submit_prompts(self, prompt_ids, prompt_lens, forced_len=None):
@@ -176,9 +183,28 @@ class Controller:
         P = self.cfg.page_tokens
         return (t.prompt_len + len(t.tokens) + P - 1) // P
 
+    def _prefix_pages(self, t: Traj) -> int:
+        """N4 (P:387 RadixAttention, within an epoch): with share_prefix and G > 1 the
+        full pages of prompt positions that every sample prefills -- [0, prompt_len - 1),
+        the last prompt token being each sample's own first decode row -- are held
+        once per replica and prompt, refcounted.  A new holder shares them only if
+        they were computed under the current policy version (weights shift after
+        every update); otherwise it keeps a private copy of the whole prompt."""
+        cfg = self.cfg
+        if not cfg.share_prefix or cfg.G <= 1:
+            return 0
+        return (t.prompt_len - 1) // cfg.page_tokens
+
     def _free_slot(self, g: int):
         t = self.slots[g]
-        self.free_pages[g % self.cfg.R] += t.pages
+        r = g % self.cfg.R
+        self.free_pages[r] += t.pages
+        if t.shared:
+            key = (r, t.tid // self.cfg.G)
+            self.pfx_ref[key] -= 1
+            if self.pfx_ref[key] == 0:
+                self.free_pages[r] += t.shared
+            t.shared = 0
         t.pages = 0
         t.slot = -1
         self.slots[g] = None
@@ -234,12 +260,22 @@ class Controller:
             t = self._peek_pending()
             need = self._pages_needed(t)
             r = g % cfg.R
-            if self.free_pages[r] < need:
+            S = self._prefix_pages(t)
+            key = (r, t.tid // cfg.G)
+            ref = self.pfx_ref.get(key, 0)
+            share = S > 0 and (ref == 0 or self.pfx_tag[key] == self.v)
+            cost = need - S if (share and ref > 0) else need
+            if self.free_pages[r] < cost:
                 self._page_blocked = True
                 break
             self._pop_pending()
-            self.free_pages[r] -= need
-            t.pages = need
+            self.free_pages[r] -= cost
+            t.pages = need - S if share else need
+            t.shared = S if share else 0
+            if share:
+                if ref == 0:
+                    self.pfx_tag[key] = self.v
+                self.pfx_ref[key] = ref + 1
             t.slot = g
             t.state = "running"
             t.fresh = False
@@ -268,7 +304,7 @@ class Controller:
             t = self.slots[g]
             if t is None:
                 continue
-            need = self._pages_needed(t)
+            need = self._pages_needed(t) - t.shared
             r = g % cfg.R
             while t.pages < need and self.slots[g] is t:
                 if self.free_pages[r] > 0:

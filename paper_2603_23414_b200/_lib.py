@@ -26,7 +26,8 @@ class SchedCfg(C.Structure):
     _fields_ = [("Q_g", _I32), ("U", _I32), ("K", _I32), ("pool_prompts", _I32), ("G", _I32), ("cap", _I32),
                 ("page_tokens", _I32), ("kv_pages", _I32), ("mode", _I32), ("resume", _I32), ("barrier", _I32),
                 ("stop", _I32), ("eos_id", _I32), ("kv_dtype", _I32), ("temperature", C.c_float),
-                ("sample_seed", _U64), ("max_traj", _I32), ("max_prompt", _I32), ("prefill_chunk", _I32)]
+                ("sample_seed", _U64), ("max_traj", _I32), ("max_prompt", _I32), ("prefill_chunk", _I32),
+                ("top_k", _I32), ("top_p", C.c_float)]
 
 
 COMM_NCCL, COMM_LOCAL, COMM_HOST = 0, 1, 2   # srl.h SRL_COMM_*
@@ -90,6 +91,7 @@ SIGNATURES = {
     "srl_op_attention_workspace": (_I64, [_I32, _I32, _I32, _I32, _I32]),
     "srl_op_attention": (_I32, [_P, _P, _P, _I32, _P, _I32, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P, _P, _P]),
     "srl_op_sample": (_I32, [_P, _I32, _I32, _P, _P, _P, C.c_float, _U64, _P, _P, _P, _P]),
+    "srl_op_sample_trunc": (_I32, [_P, _I32, _I32, _P, _P, _P, C.c_float, _U64, _I32, C.c_float, _P, _P, _P, _P]),
     "srl_arena_sizes": (_I32, [_MP, _SP, _I32, _U64P, _U64P, _U64P]),
     "srl_weight_offset": (_I64, [_MP, C.c_char_p, _I64P]),
     "srl_weight_layout": (_I32, [_MP, C.c_char_p, _I64P, _I64P, _I64P, _I64P, _I64P]),

@@ -183,6 +183,7 @@ int validate(const srl_model_cfg* m, const srl_sched_cfg* s, int world, std::str
   if (s->temperature <= 0.f) return why = "temperature must be > 0", -1;
   if (s->max_traj <= 0 || s->max_prompt <= 0 || s->prefill_chunk <= 0) return why = "max_traj, max_prompt, prefill_chunk must be positive", -1;
   if (s->kv_dtype != SRL_KV_BF16 && s->kv_dtype != SRL_KV_FP32) return why = "kv_dtype", -1;
+  if (s->top_k < 0 || !(s->top_p > 0.f && s->top_p <= 1.f)) return why = "top_k must be >= 0 and top_p in (0, 1]", -1;
   return 0;
 }
 
@@ -609,7 +610,7 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
     fe.ldo = m.V;
     fe.w_packed = 1;
     fe.ws = e->gemm_ws;
-    if (fused_sample()) {  // the sampler's Gumbel-max rides on the LM head's epilogue
+    if (fused_sample() && e->s.top_k == 0 && e->s.top_p >= 1.f) {  // Gumbel-max in the LM head's epilogue
       const Ctl& c = e->ctl;
       fe.kind = EPI_SAMPLE;
       fe.s_row_pos = row_pos;
@@ -663,11 +664,13 @@ void decode_tail(srl_engine* e, bool with_end, int M, int M_pre = 0) {
   sa.row_restarts = c.row_restarts;
   sa.invT = 1.0f / e->s.temperature;
   sa.seed = e->s.sample_seed;
+  sa.top_k = e->s.top_k;
+  sa.top_p = e->s.top_p;
   sa.tok_out = c.samp + (size_t)e->rank * 2 * e->s.Q_g;
   sa.lp_out = (float*)(c.samp + (size_t)e->rank * 2 * e->s.Q_g + e->s.Q_g);
   {
     Prof p(e, SRL_K_SAMPLE);
-    if (fused_sample())
+    if (fused_sample() && sa.top_k == 0 && sa.top_p >= 1.f)
       sample_reduce(sa, e->samp_part, e->samp_part_j, (e->m.V + 127) / 128, st);
     else
       sample(sa, st);

@@ -83,7 +83,10 @@ struct SampleArgs {
   uint64_t seed;
   int* tok_out;          // [M]
   float* lp_out;         // [M]
+  int top_k;             // > 0: draw from the k best (logit desc, index asc) only
+  float top_p;           // < 1: then from the shortest ranked prefix of mass >= top_p
 };
+// top_k > 0 or top_p < 1 runs sample_trunc_kernel (truncation set by radix select).
 void sample(const SampleArgs& a, cudaStream_t st);
 // Finish the rows whose Gumbel-max partials the LM-head GEMM produced (EPI_SAMPLE):
 // part / part_j [M][nblk] in vocab-block order -> token and behaviour logprob.

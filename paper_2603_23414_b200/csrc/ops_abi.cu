@@ -248,9 +248,41 @@ extern "C" int32_t srl_op_sample(const float* logits, int32_t M, int32_t V, cons
   a.seed = seed;
   a.tok_out = tok_out;
   a.lp_out = lp_out;
+  a.top_k = 0;
+  a.top_p = 1.f;
   sample(a, reinterpret_cast<cudaStream_t>(stream));
   if (cudaGetLastError() != cudaSuccess) {
     set_error("srl_op_sample: %s", "launch failure", 0);
+    return -3;
+  }
+  return 0;
+}
+
+extern "C" int32_t srl_op_sample_trunc(const float* logits, int32_t M, int32_t V, const int32_t* row_n,
+                                       const int32_t* row_traj, const int32_t* row_restarts, float temperature,
+                                       uint64_t seed, int32_t top_k, float top_p, const int32_t* row_active,
+                                       int32_t* tok_out, float* lp_out, void* stream) {
+  if (M < 0 || V <= 0 || !(temperature > 0.f) || top_k < 0 || !(top_p > 0.f && top_p <= 1.f)) {
+    set_error("srl_op_sample_trunc: %s", "bad arguments", 0);
+    return -1;
+  }
+  SampleArgs a{};
+  a.logits = logits;
+  a.M = M;
+  a.V = V;
+  a.row_pos = row_active;
+  a.row_n = row_n;
+  a.row_traj = row_traj;
+  a.row_restarts = row_restarts;
+  a.invT = 1.0f / temperature;
+  a.seed = seed;
+  a.tok_out = tok_out;
+  a.lp_out = lp_out;
+  a.top_k = top_k;
+  a.top_p = top_p;
+  sample(a, reinterpret_cast<cudaStream_t>(stream));
+  if (cudaGetLastError() != cudaSuccess) {
+    set_error("srl_op_sample_trunc: %s", "launch failure", 0);
     return -3;
   }
   return 0;

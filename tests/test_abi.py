@@ -62,7 +62,7 @@ def test_arena_sizes_and_validation_on_cpu(lib):
     from workload.configs import LLAMA8B, TINY
     L = _lib.load()
     m = _lib.ModelCfg(TINY.L, TINY.d, TINY.Hq, TINY.Hkv, TINY.dh, TINY.ff, TINY.V, 1e4, 1e-5, 0)
-    s = _lib.SchedCfg(16, 4, -1, 16, 1, 64, 64, 64, 0, 0, 0, 0, -1, 1, 1.0, 3, 64, 16, 256)
+    s = _lib.SchedCfg(16, 4, -1, 16, 1, 64, 64, 64, 0, 0, 0, 0, -1, 1, 1.0, 3, 64, 16, 256, 0, 1.0)
     w, k, sc = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
     assert L.srl_arena_sizes(ctypes.byref(m), ctypes.byref(s), 1, ctypes.byref(w), ctypes.byref(k), ctypes.byref(sc)) == 0
     assert k.value == 2 * TINY.L * 64 * TINY.Hkv * 64 * TINY.dh * 4
@@ -75,7 +75,7 @@ def test_arena_sizes_and_validation_on_cpu(lib):
     assert L.srl_arena_sizes(ctypes.byref(m), ctypes.byref(s), 1, None, None, None) == -1
     assert b"pool" in L.srl_last_error()
     m8 = _lib.ModelCfg(LLAMA8B.L, LLAMA8B.d, LLAMA8B.Hq, LLAMA8B.Hkv, LLAMA8B.dh, LLAMA8B.ff, LLAMA8B.V, 5e5, 1e-5, 0)
-    s8 = _lib.SchedCfg(256, 64, -1, 1024, 1, 8192, 64, 12000, 0, 0, 0, 0, -1, 0, 1.0, 3, 2048, 256, 4096)
+    s8 = _lib.SchedCfg(256, 64, -1, 1024, 1, 8192, 64, 12000, 0, 0, 0, 0, -1, 0, 1.0, 3, 2048, 256, 4096, 0, 1.0)
     assert L.srl_arena_sizes(ctypes.byref(m8), ctypes.byref(s8), 1, ctypes.byref(w), ctypes.byref(k), ctypes.byref(sc)) == 0
     # bf16 LLaMA-3.1-8B weights (staging image) + packed copies of the projection matrices
     mats = LLAMA8B.L * ((LLAMA8B.Hq + 2 * LLAMA8B.Hkv) * LLAMA8B.dh * 4096 + 4096 * 4096 + 2 * 14336 * 4096
@@ -89,7 +89,7 @@ def test_compact_weights_sizing_on_cpu(lib):
     from paper_2603_23414_b200 import _lib
     from workload.configs import QWEN32B, TINY
     L = _lib.load()
-    s = _lib.SchedCfg(64, 64, -1, 256, 1, 16384, 64, 5000, 0, 0, 0, 0, -1, 0, 1.0, 3, 1024, 256, 4096)
+    s = _lib.SchedCfg(64, 64, -1, 256, 1, 16384, 64, 5000, 0, 0, 0, 0, -1, 0, 1.0, 3, 1024, 256, 4096, 0, 1.0)
     sizes = []
     for compact in (0, 1):
         m = _lib.ModelCfg(QWEN32B.L, QWEN32B.d, QWEN32B.Hq, QWEN32B.Hkv, QWEN32B.dh, QWEN32B.ff, QWEN32B.V, 1e6,
@@ -116,7 +116,7 @@ def test_emission_sort_capacity_is_validated(lib):
     m = _lib.ModelCfg(TINY.L, TINY.d, TINY.Hq, TINY.Hkv, TINY.dh, TINY.ff, TINY.V, 1e4, 1e-5, 0)
 
     def ok(Q_g, U, pool, mode, world=1):
-        s = _lib.SchedCfg(Q_g, U, -1, pool, 1, 64, 64, 64, mode, 0, 0, 0, -1, 1, 1.0, 3, 64, 16, 256)
+        s = _lib.SchedCfg(Q_g, U, -1, pool, 1, 64, 64, 64, mode, 0, 0, 0, -1, 1, 1.0, 3, 64, 16, 256, 0, 1.0)
         return L.srl_arena_sizes(ctypes.byref(m), ctypes.byref(s), world, None, None, None) == 0
     assert ok(4096, 2048, 8192, 0)                      # U-1+Q_tot = 6143 <= 16384
     assert ok(512, 64, 8192, 2, world=8)                # bench --mode posthoc --gpus 8: pool 8192

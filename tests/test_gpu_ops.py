@@ -310,3 +310,56 @@ def test_sampler_temperature_and_inactive(lib):
     invT = np.float32(1.0) / np.float32(T)
     for r in (0, 2):
         assert tok[r] == sample_row(z[r], invT, 3, 0, 0, 0)[0]
+
+
+# ------------------------------------------------------------------ truncated sampling (N4)
+TRUNC = [(512, 1.0, 10, 1.0), (512, 2.0, 0, 0.9), (128256, 3.0, 50, 0.95), (128256, 1.0, 0, 0.5),
+         (152064, 1.0, 1000, 0.8), (1000, 0.2, 7, 0.3), (4096, 1.0, 5000, 1.0), (4096, 4.0, 0, 1e-6)]
+
+
+@pytest.mark.parametrize("V,scale,top_k,top_p", TRUNC)
+def test_sampler_truncated_matches_oracle(lib, V, scale, top_k, top_p):
+    """srl_op_sample_trunc vs oracle.sampler (truncation_set + Gumbel-max over it).
+    Token ids are equal except where the oracle's top-p cut lies within 1e-7 of
+    top_p (fp64 cumulative sum vs the kernel's fixed-point mass: both decisions are
+    valid there, and the GPU's token must then be drawable under one of them);
+    logprobs (of the truncated distribution) within 2e-5 relative.  Ties at the
+    threshold are injected (duplicated logits)."""
+    from oracle.sampler import truncation_set
+    M = 12
+    rng = np.random.default_rng(V + top_k)
+    z = (rng.normal(size=(M, V)) * scale).astype(np.float32)
+    z[1, :V // 2] = z[1, V // 2:2 * (V // 2)]                       # every value twice
+    z[2, :] = np.float32(0.5)                                      # all equal
+    z[3, rng.integers(0, V, size=V // 8)] = z[3].max()             # many ties at the top
+    n = rng.integers(0, 5000, size=M).astype(np.int32)
+    traj = rng.integers(0, 1 << 20, size=M).astype(np.int32)
+    rs = rng.integers(0, 3, size=M).astype(np.int32)
+    act = np.zeros(M, dtype=np.int32)
+    seed = 0xBEEF
+    tz, tn, tt, tr, ta = (torch.from_numpy(x).cuda() for x in (z, n, traj, rs, act))
+    tok = torch.empty(M, dtype=torch.int32, device="cuda")
+    lp = torch.empty(M, dtype=torch.float32, device="cuda")
+    assert lib.srl_op_sample_trunc(tz.data_ptr(), M, V, tn.data_ptr(), tt.data_ptr(), tr.data_ptr(), 1.0, seed, top_k,
+                                   top_p, ta.data_ptr(), tok.data_ptr(), lp.data_ptr(), _stream()) == 0
+    torch.cuda.synchronize()
+    tok, lp = tok.cpu().numpy(), lp.cpu().numpy()
+    amb = 0
+    for r in range(M):
+        t_ref, lp_ref, _ = sample_row(z[r], np.float32(1.0), seed, int(n[r]), int(traj[r]), int(rs[r]), top_k, top_p)
+        _, lo, hi = truncation_set(z[r], top_k, top_p)
+        if tok[r] != t_ref:
+            assert top_p < 1.0 and (abs(lo - top_p) < 1e-7 or abs(hi - top_p) < 1e-7), (r, tok[r], t_ref, lo, hi)
+            alt = [sample_row(z[r], np.float32(1.0), seed, int(n[r]), int(traj[r]), int(rs[r]), top_k, p)[0]
+                   for p in (top_p - 1e-7, top_p + 1e-7)]
+            assert tok[r] in alt
+            amb += 1
+            continue
+        assert abs(lp[r] - lp_ref) <= 2e-5 * max(1.0, abs(lp_ref)) + 1e-5, (r, lp[r], lp_ref)
+    assert amb <= 1
+
+
+def test_sampler_truncated_rejects_bad_args(lib):
+    assert lib.srl_op_sample_trunc(0, 1, 16, 0, 0, 0, 1.0, 3, -1, 1.0, 0, 0, 0, _stream()) < 0
+    assert lib.srl_op_sample_trunc(0, 1, 16, 0, 0, 0, 1.0, 3, 0, 0.0, 0, 0, 0, _stream()) < 0
+    assert lib.srl_op_sample_trunc(0, 1, 16, 0, 0, 0, 1.0, 3, 0, 1.5, 0, 0, 0, _stream()) < 0

@@ -249,7 +249,8 @@ def _random_cfg(rng):
                 page_tokens=rng.choice([2, 4, 64]), kv_pages=rng.choice([4, 8, 16, 1 << 20]),
                 resume=rng.choice([RESUME_KEEP_KV, RESUME_REPREFILL]),
                 barrier=rng.choice([BARRIER_TRAINED, BARRIER_ADMITTED]),
-                mode=rng.choice([MODE_SORTED, MODE_SORTED, MODE_SYNC, MODE_POSTHOC]))
+                mode=rng.choice([MODE_SORTED, MODE_SORTED, MODE_SYNC, MODE_POSTHOC]),
+                share_prefix=rng.choice([0, 1]))
 
 
 @pytest.mark.parametrize("seed", range(500))
@@ -260,7 +261,7 @@ def test_invariants_random_runs(seed):
     n_prompts = rng.randint(1, 16)
     N = n_prompts * cfg.G
     L = [rng.randint(1, cfg.cap) for _ in range(N)]
-    plen = [rng.randint(1, 6) for _ in range(n_prompts)]
+    plen = [rng.randint(1, 6) if rng.random() < 0.5 else rng.randint(1, 20) for _ in range(n_prompts)]
     if cfg.mode in (MODE_SORTED, MODE_POSTHOC) and cfg.U > cfg.pool_prompts * cfg.G:
         with pytest.raises(SchedError):
             Controller(cfg)
@@ -300,6 +301,8 @@ def test_invariants_random_runs(seed):
             assert r["len"] == L[r["traj_id"]]                   # FORCED stop exact
             assert r["vers"] == sorted(r["vers"])                  # segment versions nondecreasing
             assert r["vers"][0] == r["v_first"]
+    # page conservation (incl. shared prompt prefixes, N4): every page back at DONE
+    assert c.free_pages == [cfg.kv_pages] * cfg.R and all(v == 0 for v in c.pfx_ref.values())
     # token conservation: raw = emitted + discarded (nothing in flight at DONE)
     assert c.raw_tokens == sum(L) + c.discarded_tokens
     # lifecycle counts interruptions: events PREEMPT + DISCARD + SCAVENGE per traj
@@ -431,3 +434,72 @@ def test_throughput_function_identity():
     assert throughput(c.raw_tokens, Fraction(len(c.trace))) == 4 * (1 - B)
     with pytest.raises(ValueError):
         throughput(5, 0)
+
+
+# ---------------------------------------------------------------- N4: shared prompt prefixes
+def _pfx_run(kv_pages, share, L=(5, 5, 5, 5), plen=200, **kw):
+    cfg = SchedConfig(Q_g=4, U=2, pool_prompts=1, G=4, cap=16, kv_pages=kv_pages, share_prefix=share, **kw)
+    c = Controller(cfg)
+    c.submit_prompts([7], [plen], list(L))
+    c.load_policy_weights(0)
+    return c
+
+
+def test_prefix_sharing_page_accounting_hand_example():
+    """One prompt of 200 tokens, G = 4 samples, 64-token pages: positions [0, 199) are
+    prefilled by every sample, so floor(199 / 64) = 3 full pages are shareable; each
+    sample needs ceil((200 + 1) / 64) = 4 pages after its first token.  Shared: 3 + 4 x 1
+    = 7 pages; unshared: 16."""
+    for share, used in ((1, 7), (0, 16)):
+        c = _pfx_run(100, share)
+        c.decode_step()
+        assert c.free_pages == [100 - used]
+        assert [t.shared for t in c.stream] == ([3] * 4 if share else [0] * 4)
+
+
+def test_prefix_sharing_admits_more_when_page_limited():
+    """kv_pages = 10: unshared, two 4-page samples fit (8) and the third blocks; shared,
+    all four fit (7 pages).  Hand-derived r_0 = 2 vs 4."""
+    c0 = _pfx_run(10, 0)
+    c0.decode_step()
+    c1 = _pfx_run(10, 1)
+    c1.decode_step()
+    assert c0.trace[0] == (0, 2) and c1.trace[0] == (0, 4)
+
+
+def test_prefix_sharing_only_within_a_policy_version():
+    """After a version bump a newly admitted sample does not share the prefix computed
+    under the old weights: it holds a private copy of its whole prompt, and the
+    old entry is freed when its last holder finishes."""
+    cfg = SchedConfig(Q_g=2, U=1, pool_prompts=1, G=3, cap=16, kv_pages=100, share_prefix=1)
+    c = Controller(cfg)
+    c.submit_prompts([7], [200], [2, 6, 6])
+    c.load_policy_weights(0)
+    st = c.decode_step()                      # samples 0, 1 admitted, sharing 3 pages
+    assert st == 0 and [t.shared for t in c.stream[:2]] == [3, 3] and c.free_pages == [100 - 3 - 2]
+    assert c.decode_step() == GROUP_READY     # sample 0 (length 2) finishes and is emitted
+    c.harvest()
+    c.load_policy_weights(1)
+    c.decode_step()                           # sample 2 admitted under version 1
+    t2 = c.stream[2]
+    assert t2.shared == 0 and t2.pages == 4   # its own copy of the prompt (4 pages)
+    assert c.free_pages == [100 - (3 + 1) - 4]
+
+
+def test_prefix_sharing_same_schedule_with_ample_pages():
+    """With pages to spare sharing changes no scheduling decision: identical event logs."""
+    rng = random.Random(9)
+    for _ in range(40):
+        G = rng.choice([2, 4, 8])
+        n = rng.randint(1, 6)
+        L = [rng.randint(1, 30) for _ in range(n * G)]
+        plen = [rng.randint(1, 300) for _ in range(n)]
+        kw = dict(Q_g=rng.randint(2, 8), U=rng.randint(1, 4), pool_prompts=rng.randint(1, 4), G=G, cap=30,
+                  K=rng.choice([K_INF, 0, 1]), resume=rng.choice([RESUME_KEEP_KV, RESUME_REPREFILL]))
+        ev = []
+        for share in (0, 1):
+            c = Controller(SchedConfig(share_prefix=share, **kw))
+            c.submit_prompts(range(n), plen, L)
+            c.run()
+            ev.append(c.events)
+        assert ev[0] == ev[1]

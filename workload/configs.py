@@ -86,6 +86,9 @@ class SchedConfig:
     kv_dtype: int = KV_FP32
     temperature: float = 1.0
     sample_seed: int = 3
+    top_k: int = 0                   # N4: 0 = no top-k truncation
+    top_p: float = 1.0               # N4: 1 = no nucleus truncation
+    share_prefix: int = 0            # N4: G > 1 samples of a prompt share its prompt-prefix KV pages
 
     @property
     def Q_tot(self) -> int:
