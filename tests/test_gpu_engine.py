@@ -197,7 +197,7 @@ def test_api_state_errors():
                                                    (KV_BF16, RESUME_KEEP_KV, 256, (0, 1.0)),
                                                    (KV_BF16, RESUME_REPREFILL, 256, (0, 1.0)),
                                                    (KV_BF16, RESUME_KEEP_KV, 24, (0, 1.0)),
-                                                   (KV_BF16, RESUME_KEEP_KV, 256, (40, 0.9))],
+                                                   (KV_BF16, RESUME_KEEP_KV, 256, (40, float(np.float32(0.9))))],
                          ids=["f32", "bf16", "bf16-reprefill", "bf16-separate-prefill", "bf16-topk40-topp0.9"])
 def test_model_parity_teacher_forced(kv, resume, chunk, trunc):
     """chunk = prefill_chunk: 256 lets every step's admitted prompts join the decode
