@@ -201,12 +201,18 @@ class ModelRunner:
         return self._models[version]
 
     def admit(self, t, version):
+        self.kv[t.tid] = self.model(version).new_kv()
+
+    def prefill(self, t, a, b, version):
+        """KV of positions [.., b) of prompt ++ kept tokens under `version` (the
+        controller's chunked prefill, reading R30).  Positions below `a` not yet held
+        -- a sample starting after its shared prompt pages (N4) -- are computed here
+        too: the shared entry holds the same prompt under the same version."""
         mdl = self.model(version)
-        kv = mdl.new_kv()
+        kv = self.kv[t.tid]
         seq = list(self.prompts(t)) + list(t.tokens)
-        for pos, tok in enumerate(seq[:-1]):
-            mdl.decode_token(tok, pos, kv)
-        self.kv[t.tid] = kv
+        for pos in range(len(kv[0][0]), b):
+            mdl.decode_token(seq[pos], pos, kv)
 
     def release(self, t):
         self.kv.pop(t.tid, None)

@@ -16,6 +16,10 @@ TEST INFRASTRUCTURE ONLY (oracle/__init__.py).  Written from PAPER.md:
   P:338–342       Eq. (bubble) trace records (k, r_k)
   P:235, P:387    G > 1 responses per prompt; RadixAttention-style sharing of the
                   prompt's KV pages among them (`share_prefix`)
+  P:32, P:180     chunked prefill (Sarathi) of admitted prompts (+ the kept
+                  tokens a resumed trajectory re-feeds) under a per-step,
+                  per-replica token budget (`prefill_budget`,
+                  reading R30)
 and the DESIGN.md readings R1–R28 (SURVEY §8(c) O-C pseudo-code).  The two
 paper modes are the cache bound K (policy versions) at its extremes: K = 0 is
 fully on-policy, K = inf is partial mode; intermediate K generalises them.
@@ -63,12 +67,17 @@ class Traj:
     pages: int = 0
     shared: int = 0             # prompt-prefix pages held through the replica's shared entry
     fresh: bool = True
+    pre_next: int = -1          # N1: next prefill position (-1: prefill not started since admission)
+    pre_end: int = 0            # N1: prefill positions [.., pre_end) = prompt ++ kept tokens minus the last
 
 
 class DummyRunner:
     """Token source for pure scheduling runs: token 0, logprob 0."""
 
     def admit(self, t: Traj, version: int):
+        pass
+
+    def prefill(self, t: Traj, a: int, b: int, version: int):
         pass
 
     def release(self, t: Traj):
@@ -88,6 +97,11 @@ class Controller:
             raise SchedError("INVALID_ARG", "U larger than the prompt pool (S:252)")
         if cfg.stop == STOP_EOS and cfg.eos_id < 0:
             raise SchedError("INVALID_ARG", "EOS stop needs eos_id")
+        if cfg.prefill_budget < 0:
+            raise SchedError("INVALID_ARG", "prefill_budget must be >= 0 (0 = unlimited)")
+        if cfg.prefill_budget > 0 and cfg.share_prefix and cfg.G > 1:
+            # a shared prefix prefilled across a version bump would mix versions (R30)
+            raise SchedError("INVALID_ARG", "prefill_budget and share_prefix are exclusive")
         self.cfg = cfg
         self.runner = runner or DummyRunner()
         Q = cfg.Q_tot
@@ -120,6 +134,8 @@ class Controller:
         # holder count and the policy version its KV was computed under
         self.pfx_ref = {}
         self.pfx_tag = {}
+        self.pfx_done = {}               # the entry's shared positions have been prefilled
+        self.prefill_trace: List[tuple] = []   # (k, per-replica prefill tokens of step k)
 
     # ------------------------------------------------------------ submission
     def submit_prompts(self, prompt_ids, prompt_lens, forced_len=None):
@@ -275,7 +291,10 @@ class Controller:
             if share:
                 if ref == 0:
                     self.pfx_tag[key] = self.v
+                    self.pfx_done[key] = False
                 self.pfx_ref[key] = ref + 1
+            t.pre_next = -1
+            t.pre_end = t.prompt_len + len(t.tokens) - 1
             t.slot = g
             t.state = "running"
             t.fresh = False
@@ -318,6 +337,39 @@ class Controller:
                     raise SchedError("CAPACITY", "a trajectory outgrows its replica's KV pool")
                 victim = max(cands, key=lambda h: (self.slots[h].admit_step, h))
                 self._preempt(victim)
+
+    def _prefill(self):
+        """N1 (reading R30): each replica prefills its admitted slots strictly in
+        admission order (admit_step, then global slot), at most `prefill_budget`
+        positions per step (0 = unlimited: every admission is prefilled in its own
+        step, R13).  A slot starts at position 0, or -- N4 -- after its shared prompt
+        pages when the entry's first holder has already prefilled them; a slot that is
+        still short of its prefill after the budget stops the walk (later ones wait).
+        A slot decodes in a step only once its prefill is complete (in that step or
+        an earlier one).  Returns the per-replica prefill tokens of this step."""
+        cfg = self.cfg
+        C = cfg.prefill_budget if cfg.prefill_budget > 0 else None
+        used = [0] * cfg.R
+        for r in range(cfg.R):
+            slots = sorted((self.slots[g].admit_step, g) for g in range(r, cfg.Q_tot, cfg.R)
+                           if self.slots[g] is not None and self.slots[g].pre_next < self.slots[g].pre_end)
+            for _, g in slots:
+                t = self.slots[g]
+                key = (r, t.tid // cfg.G)
+                if t.pre_next < 0:
+                    t.pre_next = t.shared * cfg.page_tokens if (t.shared and self.pfx_done[key]) else 0
+                n = t.pre_end - t.pre_next
+                if C is not None:
+                    n = min(n, C - used[r])
+                if n > 0:
+                    self.runner.prefill(t, t.pre_next, t.pre_next + n, self.v)
+                    t.pre_next += n
+                    used[r] += n
+                if t.shared and t.pre_next >= t.shared * cfg.page_tokens:
+                    self.pfx_done[key] = True
+                if t.pre_next < t.pre_end:
+                    break
+        return used
 
     def _emission_check(self) -> bool:
         cfg = self.cfg
@@ -366,6 +418,7 @@ class Controller:
         self._maybe_load()
         self._refill()
         self._grow_pages()
+        pre = self._prefill()
         occ = self._occupied()
         # work conservation record: a free slot only if nothing is admissible
         self.work_conserving.append(len(occ) == cfg.Q_tot or self._pending_empty() or self._page_blocked)
@@ -375,8 +428,11 @@ class Controller:
             if not self.stream:
                 raise SchedError("EMPTY", "nothing submitted (S:124)")
             return DONE
-        r_k = len(occ)
-        batch = [(g, self.slots[g]) for g in occ]
+        # decode rows: the occupied slots whose prefill is complete (N1; all of them
+        # without a budget)
+        batch = [(g, self.slots[g]) for g in occ if self.slots[g].pre_next >= self.slots[g].pre_end]
+        r_k = len(batch)
+        self.prefill_trace.append((self.k, tuple(pre)))
         outs = self.runner.step(batch, self.v)
         finished = []
         for (g, t), (tok, lp) in zip(batch, outs):

@@ -128,6 +128,9 @@ def test_replicas_schedule_bit_exact(name, over):
             def admit(self, t, v):
                 pass
 
+            def prefill(self, t, a, b, v):
+                pass
+
             def release(self, t):
                 pass
 

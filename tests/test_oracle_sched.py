@@ -250,13 +250,17 @@ def _random_cfg(rng):
                 resume=rng.choice([RESUME_KEEP_KV, RESUME_REPREFILL]),
                 barrier=rng.choice([BARRIER_TRAINED, BARRIER_ADMITTED]),
                 mode=rng.choice([MODE_SORTED, MODE_SORTED, MODE_SYNC, MODE_POSTHOC]),
-                share_prefix=rng.choice([0, 1]))
+                share_prefix=rng.choice([0, 1]), prefill_budget=rng.choice([0, 0, 1, 3, 8]))
 
 
 @pytest.mark.parametrize("seed", range(500))
 def test_invariants_random_runs(seed):
     rng = random.Random(seed)
     kw = _random_cfg(rng)
+    if kw["share_prefix"] and kw["G"] > 1 and kw["prefill_budget"]:
+        with pytest.raises(SchedError):
+            Controller(SchedConfig(**kw))
+        kw["prefill_budget"] = 0
     cfg = SchedConfig(**kw)
     n_prompts = rng.randint(1, 16)
     N = n_prompts * cfg.G
@@ -300,7 +304,16 @@ def test_invariants_random_runs(seed):
             assert r["len"] == len(r["tokens"]) == len(r["lps"]) == len(r["vers"])
             assert r["len"] == L[r["traj_id"]]                   # FORCED stop exact
             assert r["vers"] == sorted(r["vers"])                  # segment versions nondecreasing
-            assert r["vers"][0] == r["v_first"]
+            # v_first is stamped at admission (R30): with a prefill budget the first token
+            # may come after a version bump
+            assert r["vers"][0] == r["v_first"] if not cfg.prefill_budget else r["vers"][0] >= r["v_first"]
+    # N1: the per-replica budget holds every step; with no interruption and no
+    # sharing every admission prefills exactly prompt_len - 1 positions
+    assert len(c.prefill_trace) == len(c.trace)
+    if cfg.prefill_budget:
+        assert all(x <= cfg.prefill_budget for _, pre in c.prefill_trace for x in pre)
+    if not any(e[0] in ("PREEMPT", "DISCARD", "SCAVENGE") for e in c.events) and not (cfg.share_prefix and cfg.G > 1):
+        assert sum(sum(pre) for _, pre in c.prefill_trace) == sum(plen[i // cfg.G] - 1 for i in range(N))
     # page conservation (incl. shared prompt prefixes, N4): every page back at DONE
     assert c.free_pages == [cfg.kv_pages] * cfg.R and all(v == 0 for v in c.pfx_ref.values())
     # token conservation: raw = emitted + discarded (nothing in flight at DONE)
@@ -503,3 +516,94 @@ def test_prefix_sharing_same_schedule_with_ample_pages():
             c.run()
             ev.append(c.events)
         assert ev[0] == ev[1]
+
+
+# ---------------------------------------------------------------- N1: per-step prefill budget
+def test_prefill_budget_worked_example():
+    """Hand-derived (reading R30).  Prompts of 100, 50, 30, 10 tokens need 99, 49, 29, 9
+    prefill positions; budget 64 per step, served strictly in admission order:
+      k=0: slot 0 gets 64 (35 left)                          -> prefill 64, no decode row
+      k=1: slot 0 35 (done), slot 1 29 (20 left)              -> prefill 64, decode {0}
+      k=2: slot 1 20, slot 2 29, slot 3 9 (all done)          -> prefill 58, decode {0,1,2,3}
+      k=3: slot 0 emits its 3rd token and finishes            -> decode 4
+      k=4: slots 1, 2, 3 finish                               -> decode 3, group of 4."""
+    cfg = SchedConfig(Q_g=4, U=4, pool_prompts=4, cap=8, prefill_budget=64)
+    c = Controller(cfg)
+    c.submit_prompts([1, 2, 3, 4], [100, 50, 30, 10], [3, 3, 3, 3])
+    c.load_policy_weights(0)
+    st = [c.decode_step() for _ in range(5)]
+    assert st == [0, 0, 0, 0, GROUP_READY]
+    assert c.trace == [(0, 0), (1, 1), (2, 4), (3, 4), (4, 3)]
+    assert c.prefill_trace == [(0, (64,)), (1, (64,)), (2, (58,)), (3, (0,)), (4, (0,))]
+    fin = [(e[1], e[2]) for e in c.events if e[0] == "FINISH"]
+    assert fin == [(3, 0), (4, 1), (4, 2), (4, 3)]
+    # unlimited: every prompt prefilled in step 0, all four finish at step 2 (R13)
+    c0 = Controller(SchedConfig(Q_g=4, U=4, pool_prompts=4, cap=8))
+    c0.submit_prompts([1, 2, 3, 4], [100, 50, 30, 10], [3, 3, 3, 3])
+    c0.load_policy_weights(0)
+    while c0.decode_step() != GROUP_READY:
+        pass
+    assert c0.trace == [(0, 4), (1, 4), (2, 4)] and c0.prefill_trace[0] == (0, (99 + 49 + 29 + 9,))
+
+
+def test_prefill_budget_large_equals_unlimited():
+    """A budget no step can exhaust reproduces the unlimited schedule exactly (R13 is the
+    budget's limit), on random instances incl. preemption, discards and REPREFILL."""
+    for seed in range(60):
+        rng = random.Random(7000 + seed)
+        kw = _random_cfg(rng)
+        kw["share_prefix"] = 0
+        kw["mode"] = rng.choice([MODE_SORTED, MODE_SYNC])
+        kw["U"] = min(kw["U"], kw["pool_prompts"] * kw["G"])
+        n = rng.randint(1, 12)
+        L = [rng.randint(1, kw["cap"]) for _ in range(n * kw["G"])]
+        plen = [rng.randint(1, 20) for _ in range(n)]
+        runs = []
+        for C in (0, 10 ** 6):
+            c = Controller(SchedConfig(**dict(kw, prefill_budget=C)))
+            c.submit_prompts(range(n), plen, L)
+            try:
+                c.run()
+            except SchedError as e:
+                assert e.code == "CAPACITY"
+                c = None
+            runs.append(c)
+        if runs[0] is None:
+            assert runs[1] is None
+            continue
+        assert runs[0].events == runs[1].events and runs[0].trace == runs[1].trace
+        assert runs[0].prefill_trace == runs[1].prefill_trace
+
+
+def test_prefill_budget_fifo_and_first_token():
+    """Without interruptions: prefills complete in admission order per replica, and a
+    trajectory admitted at step a whose prefill needs P positions emits its first token
+    no earlier than step a + ceil(P / C) - 1 (the budget is the only limit)."""
+    for seed in range(40):
+        rng = random.Random(9100 + seed)
+        C = rng.choice([1, 5, 16, 40])
+        R = rng.choice([1, 2])
+        cfg = SchedConfig(Q_g=rng.randint(1, 6), R=R, U=2, pool_prompts=8, cap=20, prefill_budget=C)
+        n = 8
+        plen = [rng.randint(1, 60) for _ in range(n)]
+        L = [rng.randint(1, 20) for _ in range(n)]
+        c = Controller(cfg)
+        c.submit_prompts(range(n), plen, L)
+        c.run()
+        admit = {e[3]: (e[1], e[2]) for e in c.events if e[0] == "ADMIT"}
+        fin = {e[3]: e[1] for e in c.events if e[0] == "FINISH"}
+        first = {t: fin[t] - L[t] + 1 for t in fin}          # FORCED: one token per step once decoding
+        for t, (a, g) in admit.items():
+            P = plen[t] - 1
+            assert first[t] >= a + max(0, -(-P // C) - 1), (t, a, P, C, first[t])
+        for r in range(R):
+            order = sorted((a, g, t) for t, (a, g) in admit.items() if g % R == r)
+            starts = [first[t] for _, _, t in order]
+            assert starts == sorted(starts)
+
+
+def test_prefill_budget_rejected_with_sharing():
+    with pytest.raises(SchedError):
+        Controller(SchedConfig(G=2, share_prefix=1, prefill_budget=64))
+    with pytest.raises(SchedError):
+        Controller(SchedConfig(prefill_budget=-1))

@@ -82,6 +82,9 @@ class _GlobalRunner:
     def admit(self, t, v):
         pass
 
+    def prefill(self, t, a, b, v):
+        pass
+
     def release(self, t):
         pass
 

@@ -89,6 +89,7 @@ class SchedConfig:
     top_k: int = 0                   # N4: 0 = no top-k truncation
     top_p: float = 1.0               # N4: 1 = no nucleus truncation
     share_prefix: int = 0            # N4: G > 1 samples of a prompt share its prompt-prefix KV pages
+    prefill_budget: int = 0          # N1: prefill tokens per replica per step (0 = unlimited)
 
     @property
     def Q_tot(self) -> int:
