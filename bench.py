@@ -71,12 +71,14 @@ def cfg2_sched(world=1, Q_g=256, cap=8192, pool=N_PROMPTS_PER_EPOCH, kv_pages=11
                        stop=STOP_FORCED, kv_dtype=KV_BF16, temperature=1.0, sample_seed=3)
 
 
-def workload_inputs(world=1, epochs=2, pool=N_PROMPTS_PER_EPOCH, V=LLAMA8B.V, cap=8192):
+def workload_inputs(world=1, epochs=2, pool=N_PROMPTS_PER_EPOCH, V=LLAMA8B.V, cap=8192, G=1):
     """The prompt stream every replica submits (identical on all ranks; the replicated
-    pending queue shards it over the global slots)."""
-    n = pool * world * epochs
+    pending queue shards it over the global slots).  `pool` counts trajectories per
+    GPU per epoch: pool / G prompts of G responses each (G = 8: LogicRL's 128 x 8,
+    P:235)."""
+    n = pool * world * epochs // G
     off, toks = make_prompts(1, n, V, PROMPT_LEN)
-    L = sample_lengths(LengthModel(median=1600, sigma=0.55, tail=0.03, floor=1, cap=cap), 0, n)
+    L = sample_lengths(LengthModel(median=1600, sigma=0.55, tail=0.03, floor=1, cap=cap), 0, n * G)
     return off, toks, L
 
 
@@ -166,9 +168,9 @@ class PromptStream:
     load it -- so prompts are copied host -> device inside the round that consumes
     them.  ADMITTED barrier: one epoch is kept queued ahead of the controller."""
 
-    def __init__(self, eng, off, toks, L, ids, per_epoch, trained, torch):
+    def __init__(self, eng, off, toks, L, ids, per_epoch, trained, torch, G=1):
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
-        self.eng, self.off = eng, off
+        self.eng, self.off, self.G = eng, off, G
         self.toks, self.L, self.ids = pin(toks), pin(L), pin(ids)
         self.per_epoch, self.trained = per_epoch, trained
         self.next = 0            # prompts submitted
@@ -193,8 +195,9 @@ class PromptStream:
         if hi <= lo:
             return 0
         o = self.off[lo:hi + 1]
-        self.eng.submit_prompts(self.ids[lo:hi], (o - o[0]).astype(np.int32), self.toks[o[0]:o[-1]], self.L[lo:hi])
-        self.h2d += int((o[-1] - o[0]) * 4 + (hi - lo) * (8 + 4 + 4) + 4)
+        self.eng.submit_prompts(self.ids[lo:hi], (o - o[0]).astype(np.int32), self.toks[o[0]:o[-1]],
+                               self.L[lo * self.G:hi * self.G])
+        self.h2d += int((o[-1] - o[0]) * 4 + (hi - lo) * (8 + 4 + 4 * self.G) + 4)
         self.submits.append((lo, hi - lo))
         self.next = hi
         return hi - lo
@@ -211,6 +214,9 @@ class PromptStream:
 
 def run_gpu(args, rank, world, dist):
     import torch
+    if args.tuning:
+        from paper_2603_23414_b200 import _lib
+        _lib.set_tuning(**{k: int(v) for k, v in (kv.split("=") for kv in args.tuning.split(","))})
     from paper_2603_23414_b200.engine import DONE, GROUP_READY, RolloutEngine
     from workload.weights import fill_engine_weights
     torch.cuda.set_device(rank % max(1, torch.cuda.device_count()))
@@ -222,8 +228,10 @@ def run_gpu(args, rank, world, dist):
     sched = dataclasses.replace(sched, mode={"sorted": MODE_SORTED, "sync": MODE_SYNC, "posthoc": MODE_POSTHOC}[args.mode],
                                 K=args.K, U=args.U,
                                 barrier={"trained": BARRIER_TRAINED, "admitted": BARRIER_ADMITTED}[args.barrier],
-                                resume={"keep_kv": RESUME_KEEP_KV, "reprefill": RESUME_REPREFILL}[args.resume])
-    off, toks, L = workload_inputs(world, epochs=EPOCHS, pool=pool, V=model.V, cap=cap)
+                                resume={"keep_kv": RESUME_KEEP_KV, "reprefill": RESUME_REPREFILL}[args.resume],
+                                G=args.G, pool_prompts=pool * world // args.G, share_prefix=int(args.share_prefix),
+                                prefill_budget=args.prefill_budget)
+    off, toks, L = workload_inputs(world, epochs=EPOCHS, pool=pool, V=model.V, cap=cap, G=args.G)
     ids = np.arange(len(off) - 1, dtype=np.uint64) + 1
     max_traj = EPOCHS * pool * world
     rep = {}
@@ -238,9 +246,9 @@ def run_gpu(args, rank, world, dist):
     eng.load_policy_weights(0)
     torch.cuda.synchronize()
     stream = eng.stream              # the stream every engine kernel is launched on
-    per_epoch = pool * world
+    per_epoch = pool * world // sched.G      # prompts per epoch
     trained = sched.barrier == BARRIER_TRAINED or sched.mode != MODE_SORTED
-    loader = PromptStream(eng, off, toks, L, ids, per_epoch if sched.mode != MODE_SYNC else per_epoch, trained, torch)
+    loader = PromptStream(eng, off, toks, L, ids, per_epoch, trained, torch, G=sched.G)
     st = {"v": 0, "useful": 0, "d2h": 0, "done": False, "emitted": 0, "steps": 0}
     trace = []                       # every decode step: (r_k, sum_ctx, dt_ms, prefill_tokens, n_fin, r_local)
     ATT = ["attention"]
@@ -551,6 +559,10 @@ def main():
     ap.add_argument("--K", type=int, default=K_INF, help="cache bound in policy versions (-1 = inf, 0 = on-policy)")
     ap.add_argument("--U", type=int, default=64, help="update group size")
     ap.add_argument("--barrier", default="trained", choices=["trained", "admitted"], help="cache-aware loading barrier")
+    ap.add_argument("--tuning", default="", help="srl_tuning overrides for measurement, e.g. fuse_mlp=0,mlp_splits=4")
+    ap.add_argument("--G", type=int, default=1, help="responses per prompt (trajectories per epoch unchanged)")
+    ap.add_argument("--share-prefix", action="store_true", help="N4: G samples share their prompt-prefix KV pages")
+    ap.add_argument("--prefill-budget", type=int, default=0, help="N1: prefill tokens per GPU per step (0 = unlimited)")
     ap.add_argument("--resume", default="keep_kv", choices=["keep_kv", "reprefill"],
                     help="how kept partial trajectories resume (reading R10): keep their KV (default) or re-prefill "
                          "prompt + generated tokens (P:180 literal)")
@@ -654,7 +666,8 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": MODELS[args.model][7] or WORKLOAD,
                    "scheduler": {"mode": args.mode, "K": args.K, "U": args.U, "barrier": args.barrier,
-                                 "resume": args.resume},
+                                 "resume": args.resume, "G": args.G, "share_prefix": bool(args.share_prefix),
+                                 "prefill_budget": args.prefill_budget},
                    "step": "one early-update round: decode steps (refill, prefill, decode GEMMs, paged attention, "
                            "Philox sampling, stop detection, compaction) until the length-sorted update group of "
                            f"U={args.U} is ready, its harvest, and the policy refresh (load_policy_weights, K bound)",
@@ -663,7 +676,8 @@ def main():
                               f"epoch drain + next epoch's prefill burst inside), {n_dec} decode steps; "
                               f"{r.get('warmup_rounds')} untimed rounds before"),
                    "l2": "no flush needed: every decode step streams 15 GB of weights + the KV cache (>> 126 MB L2)",
-                   "parallelism": f"dp{world} lockstep replicas (NCCL)" if world > 1 else "dp1"},
+                   "parallelism": f"dp{world} lockstep replicas (NCCL)" if world > 1 else "dp1",
+                   **({"tuning": args.tuning} if args.tuning else {})},
         "decode_steps": n_dec,
         "ms_per_decode_step": ms / max(1, n_dec),
         "useful_tokens_per_s": useful_s,

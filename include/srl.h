@@ -95,6 +95,19 @@ typedef struct srl_sched_cfg {
    * the truncated, renormalised distribution.  0 / 1 = off (R14). */
   int32_t top_k;
   float top_p;
+  /* N4 prompt-prefix KV sharing (G > 1; P:235 several responses per prompt, P:387
+   * RadixAttention): the full KV pages of prompt positions [0, prompt_len - 1) --
+   * what every sample of a prompt prefills -- are held once per replica and
+   * prompt, refcounted, and only shared with samples admitted under the policy
+   * version they were computed with; a later sample prefills from the first
+   * unshared position.  Page accounting = oracle/sched.py _prefix_pages.  0 / 1. */
+  int32_t share_prefix;
+  /* N1 chunked prefill (Sarathi; prompt ++ kept tokens on resume):
+   * at most prefill_budget prefill positions per replica per step, served strictly
+   * in admission order; a slot decodes from the step its prefill completes (reading
+   * R30; oracle/sched.py _prefill).  0 = unlimited (every admission is prefilled in
+   * its own step, R13).  Exclusive with share_prefix. */
+  int32_t prefill_budget;
 } srl_sched_cfg;
 
 /* Data-parallel replicas (rows a14, a17).  R = world engines run
@@ -355,6 +368,8 @@ typedef struct srl_tuning {
   int32_t graphs;          /* 1: replay the decode tail from CUDA graphs */
   int32_t mixed_prefill;   /* 1: admitted prompts ride in the decode pass when they fit one chunk */
   int32_t verbose;         /* 1: print GEMM plans to stderr */
+  int32_t fuse_mlp;        /* 1: gate/up and down GEMMs as one persistent kernel (128 <= M <= 256) */
+  int32_t mlp_splits;      /* k-splits of the fused down GEMM (its partials go to the next RMSNorm), 1..8 */
 } srl_tuning;
 void srl_default_tuning(srl_tuning* t);
 int32_t srl_get_tuning(srl_tuning* t);

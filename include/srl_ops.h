@@ -44,6 +44,24 @@ int64_t srl_op_gemm_workspace(int32_t M, int32_t N, int32_t K, int32_t epi);
 int32_t srl_op_gemm_bf16(const void* X, int32_t M, const void* W, int32_t N, int32_t K, int32_t epi, void* out,
                          void* workspace, void* stream);
 
+/* The decode MLP (SURVEY §8(a) a8 + a9) as ONE persistent tcgen05 kernel, the
+ * engine's path for 128 <= M <= 256 decode rows (srl_tuning.fuse_mlp):
+ *   act  [M, ff] bf16 = silu(X Wg^T) * (X Wu^T)      (a8: the gate/up GEMM + SiLU-mul)
+ *   part [splits][M, d] fp32, part[s] = act[:, ks] Wd[:, ks]^T over the s-th of
+ *        `splits` equal k-ranges ks of ff               (a9: the down GEMM, k-split)
+ * so that sum_s part[s] (in s order) = act Wd^T; the engine's next RMSNorm sums
+ * them and adds the residual.  X [M, d] bf16 row-major; Wgu_packed = the packed
+ * image (srl_op_pack_weight) of the interleaved [2ff, d] gate/up matrix (64 gate
+ * rows then the matching 64 up rows per 128-row block, as epi 2 above); Wd_packed
+ * = the packed image of Wd [d, ff].  workspace as srl_op_gemm_workspace (zeroed
+ * before first use, left zeroed).  The down k-split s starts as soon as the
+ * gate/up tiles producing its act columns are stored (device-scope counters).
+ * Requires 128 <= M <= 256, d % 256 == 0, ff % (128 * splits) == 0, 1 <= splits
+ * <= 8.  Returns 0, 1 (shape not supported by the fused kernel: nothing written)
+ * or -1 (bad arguments / launch failure, srl_last_error()). */
+int32_t srl_op_mlp_bf16(const void* X, int32_t M, const void* Wgu_packed, const void* Wd_packed, int32_t d, int32_t ff,
+                        int32_t splits, void* act_out, float* part_out, void* workspace, void* stream);
+
 /* Packed weight layout for srl_op_gemm_bf16 (and the engine's internal copy
  * of its projection weights; written by srl_load_policy_weights).  W [N, K] bf16
  * row-major -> dst of srl_op_packed_weight_bytes(N, K) bytes: blocks of 16 KB

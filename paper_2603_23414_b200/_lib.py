@@ -27,7 +27,7 @@ class SchedCfg(C.Structure):
                 ("page_tokens", _I32), ("kv_pages", _I32), ("mode", _I32), ("resume", _I32), ("barrier", _I32),
                 ("stop", _I32), ("eos_id", _I32), ("kv_dtype", _I32), ("temperature", C.c_float),
                 ("sample_seed", _U64), ("max_traj", _I32), ("max_prompt", _I32), ("prefill_chunk", _I32),
-                ("top_k", _I32), ("top_p", C.c_float)]
+                ("top_k", _I32), ("top_p", C.c_float), ("share_prefix", _I32), ("prefill_budget", _I32)]
 
 
 COMM_NCCL, COMM_LOCAL, COMM_HOST = 0, 1, 2   # srl.h SRL_COMM_*
@@ -75,7 +75,7 @@ class Tuning(C.Structure):
     _fields_ = [(n, _I32) for n in ("gemm_split", "gemm_pair", "gemm_h", "gemm_stages", "gemm_xstages",
                                     "partial_norm", "partial_small_m", "qkv_finish", "fused_sample",
                                     "attn_min_items", "attn_target_items", "attn_l2_prefetch", "pdl", "graphs",
-                                    "mixed_prefill", "verbose")]
+                                    "mixed_prefill", "verbose", "fuse_mlp", "mlp_splits")]
 
 
 _MP, _SP, _AP, _CP = C.POINTER(ModelCfg), C.POINTER(SchedCfg), C.POINTER(Arena), C.POINTER(Comm)
@@ -87,6 +87,7 @@ SIGNATURES = {
     "srl_op_gemm_bf16": (_I32, [_P, _I32, _P, _I32, _I32, _I32, _P, _P, _P]),
     "srl_op_gemm_workspace": (_I64, [_I32, _I32, _I32, _I32]),
     "srl_op_packed_weight_bytes": (_I64, [_I32, _I32]),
+    "srl_op_mlp_bf16": (_I32, [_P, _I32, _P, _P, _I32, _I32, _I32, _P, _P, _P, _P]),
     "srl_op_pack_weight": (_I32, [_P, _I32, _I32, _P, _P]),
     "srl_op_attention_workspace": (_I64, [_I32, _I32, _I32, _I32, _I32]),
     "srl_op_attention": (_I32, [_P, _P, _P, _I32, _P, _I32, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P, _P, _P]),

@@ -147,10 +147,22 @@ __device__ void free_slot(const Ctl& c, int g) {
   DevTraj& t = c.traj[tid];
   const int r = g % c.R;
   if (r == c.rank) {
-    const int* row = c.page_table + (size_t)(g / c.R) * c.max_pages;
+    const int* row = c.page_table + (size_t)(g / c.R) * c.max_pages + t.shared;
     for (int i = t.pages - 1; i >= 0; --i) c.page_stack[s->own_top++] = row[i];
   }
   s->free_pages[r] += t.pages;
+  if (t.shared) {  // N4: release the prompt-prefix entry; its last holder frees its pages
+    const int key = r * c.max_prompts + t.prompt_idx;
+    if (--c.pfx_ref[key] == 0) {
+      s->free_pages[r] += t.shared;
+      c.pfx_valid[key] = 0;
+      if (r == c.rank) {
+        const int* pp = c.pfx_pages + (size_t)t.prompt_idx * c.pfx_max;
+        for (int i = t.shared - 1; i >= 0; --i) c.page_stack[s->own_top++] = pp[i];
+      }
+    }
+    t.shared = 0;
+  }
   t.pages = 0;
   t.slot = -1;
   c.slot_traj[g] = -1;
@@ -333,14 +345,32 @@ __global__ void __launch_bounds__(kCtlThreads, 1) ctl_begin_kernel(Ctl c) {
         DevTraj& t = c.traj[tid];
         const int need = (t.prompt_len + t.n_tok + kPage - 1) / kPage;
         const int r = gg % c.R;
-        if (s->free_pages[r] < need || need > c.max_pages) {
+        // N4 (oracle/sched.py _prefix_pages): the full pages of prompt positions
+        // [0, prompt_len - 1) are shareable; a new holder shares an existing entry
+        // only if it was computed under the current version
+        const int S = c.share_prefix ? (t.prompt_len - 1) / kPage : 0;
+        const int key = r * c.max_prompts + t.prompt_idx;
+        const int ref = S > 0 ? c.pfx_ref[key] : 0;
+        const bool share = S > 0 && (ref == 0 || c.pfx_tag[key] == s->v);
+        const int cost = (share && ref > 0) ? need - S : need;
+        if (s->free_pages[r] < cost || need > c.max_pages) {
           s->page_blocked = 1;
           sh_stop = 1;
           break;
         }
         pending_pop(c);
-        s->free_pages[r] -= need;
-        t.pages = need;
+        s->free_pages[r] -= cost;
+        t.pages = share ? need - S : need;
+        t.shared = share ? S : 0;
+        if (share) {
+          if (ref == 0) {
+            c.pfx_tag[key] = s->v;
+            c.pfx_valid[key] = 0;  // computed by the first holder whose prefill reaches it
+          }
+          c.pfx_ref[key] = ref + 1;
+        }
+        t.pre_next = -1;
+        t.pre_end = t.prompt_len + t.n_tok - 1;
         t.slot = gg;
         t.state = TS_RUNNING;
         t.fresh = 0;
@@ -351,7 +381,13 @@ __global__ void __launch_bounds__(kCtlThreads, 1) ctl_begin_kernel(Ctl c) {
         s->st.n_admit++;
         if (r == c.rank) {
           int* row = c.page_table + (size_t)(gg / c.R) * c.max_pages;
-          for (int p = 0; p < need; ++p) row[p] = c.page_stack[--s->own_top];
+          if (share) {
+            int* pp = c.pfx_pages + (size_t)t.prompt_idx * c.pfx_max;
+            if (ref == 0)  // a new entry: its pages are computed by the first surviving holder's prefill
+              for (int p = 0; p < S; ++p) pp[p] = c.page_stack[--s->own_top];
+            for (int p = 0; p < S; ++p) row[p] = pp[p];
+          }
+          for (int p = t.shared; p < need; ++p) row[p] = c.page_stack[--s->own_top];
           c.admit_local[s->st.n_admit_local++] = gg / c.R;
         }
       }
@@ -368,7 +404,7 @@ __global__ void __launch_bounds__(kCtlThreads, 1) ctl_begin_kernel(Ctl c) {
       const int tid = c.slot_traj[g];
       if (tid >= 0) {
         const DevTraj& t = c.traj[tid];
-        f = t.pages * kPage < t.prompt_len + t.n_tok;
+        f = (t.shared + t.pages) * kPage < t.prompt_len + t.n_tok;
       }
     }
     int tot;
@@ -382,12 +418,13 @@ __global__ void __launch_bounds__(kCtlThreads, 1) ctl_begin_kernel(Ctl c) {
         const int tid = c.slot_traj[gg];
         if (tid < 0) continue;  // preempted earlier in this loop
         DevTraj& t = c.traj[tid];
-        const int need = (t.prompt_len + t.n_tok + kPage - 1) / kPage;
+        const int need = (t.prompt_len + t.n_tok + kPage - 1) / kPage - t.shared;  // private pages
         const int r = gg % c.R;
         while (t.pages < need && c.slot_traj[gg] == tid) {
-          if (s->free_pages[r] > 0 && t.pages < c.max_pages) {
+          if (s->free_pages[r] > 0 && t.shared + t.pages < c.max_pages) {
             s->free_pages[r]--;
-            if (r == c.rank) c.page_table[(size_t)(gg / c.R) * c.max_pages + t.pages] = c.page_stack[--s->own_top];
+            if (r == c.rank)
+              c.page_table[(size_t)(gg / c.R) * c.max_pages + t.shared + t.pages] = c.page_stack[--s->own_top];
             t.pages++;
             continue;
           }
@@ -439,17 +476,77 @@ __global__ void __launch_bounds__(kCtlThreads, 1) ctl_begin_kernel(Ctl c) {
     }
     return;
   }
-  // decode rows: this rank's running slots compacted in ascending slot order (row i
-  // -> slot row_slot[i]), so the decode forward runs over the first r_local rows only
-  // (the host picks a graph whose M covers them); rows past them are inactive
+  // N1 prefill allocation (reading R30, oracle/sched.py _prefill), replicated over
+  // every replica's slots: each replica serves its prefilling slots strictly in
+  // admission order (admit_step, global slot) with at most prefill_budget positions
+  // per step (0 = unlimited); a slot short of its prefill stops its replica's walk.
+  // N4: a slot starts after its shared prompt pages when the entry is already valid.
+  __shared__ int sh_npf, sh_nalloc, sh_used[kMaxR], sh_blk[kMaxR];
+  if (threadIdx.x == 0) sh_npf = 0;
+  __syncthreads();
+  for (int base = 0; base < c.Q_tot; base += blockDim.x) {
+    const int g = base + threadIdx.x;
+    int f = 0;
+    if (g < c.Q_tot) {
+      const int tid = c.slot_traj[g];
+      f = tid >= 0 && c.traj[tid].pre_next < c.traj[tid].pre_end;
+    }
+    int tot;
+    const int pos = block_scan(f, &tot);
+    if (f) keys[sh_npf + pos] = ((long long)c.traj[c.slot_traj[g]].admit_step << 32) | (unsigned)g;
+    __syncthreads();
+    if (threadIdx.x == 0) sh_npf += tot;
+    __syncthreads();
+  }
+  const int npf = sh_npf;
+  if (npf > 0) bitonic_sort(keys, npf);
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < c.R; ++r) sh_used[r] = sh_blk[r] = 0;
+    int na = 0, off = 0;
+    for (int i = 0; i < npf; ++i) {
+      const int g = (int)(keys[i] & 0xffffffffLL), r = g % c.R;
+      if (sh_blk[r]) continue;
+      DevTraj& t = c.traj[c.slot_traj[g]];
+      const int key = r * c.max_prompts + t.prompt_idx;
+      if (t.pre_next < 0) t.pre_next = (t.shared > 0 && c.pfx_valid[key]) ? t.shared * kPage : 0;
+      int n = t.pre_end - t.pre_next;
+      if (c.prefill_budget > 0 && n > c.prefill_budget - sh_used[r]) n = c.prefill_budget - sh_used[r];
+      if (n > 0) {
+        if (r == c.rank) {
+          c.pre_list[3 * na] = g / c.R;
+          c.pre_list[3 * na + 1] = t.pre_next;
+          c.pre_list[3 * na + 2] = off;
+          ++na;
+          off += n;
+        }
+        t.pre_next += n;
+        sh_used[r] += n;
+      }
+      if (t.shared > 0 && t.pre_next >= t.shared * kPage) c.pfx_valid[key] = 1;
+      if (t.pre_next < t.pre_end) sh_blk[r] = 1;
+    }
+    sh_nalloc = na;
+    c.pre_list[3 * na + 2] = off;  // sentinel: total rows (pre_list has room for Q_g + 1 entries)
+  }
+  __syncthreads();
+  // decode rows: this rank's running slots whose prefill is complete, compacted in
+  // ascending slot order (row i -> slot row_slot[i]), so the decode forward runs over
+  // the first r_local rows only (the host picks a graph whose M covers them); rows
+  // past them are inactive
   long long my_ctx = 0;
-  int my_rows = 0;
+  int my_rows = 0, dec = 0;
+  for (int g = threadIdx.x; g < c.Q_tot; g += blockDim.x) {
+    const int tid = c.slot_traj[g];
+    dec += tid >= 0 && c.traj[tid].pre_next >= c.traj[tid].pre_end;
+  }
+  dec = block_sum(dec);
   __shared__ int sh_rbase;
   if (threadIdx.x == 0) sh_rbase = 0;
   __syncthreads();
   for (int base = 0; base < c.Q_g; base += blockDim.x) {
     const int sl = base + threadIdx.x;
-    const int tid = sl < c.Q_g ? c.slot_traj[sl * c.R + c.rank] : -1;
+    int tid = sl < c.Q_g ? c.slot_traj[sl * c.R + c.rank] : -1;
+    if (tid >= 0 && c.traj[tid].pre_next < c.traj[tid].pre_end) tid = -1;  // still prefilling
     int tot;
     const int rank_in = block_scan(tid >= 0 ? 1 : 0, &tot);
     if (tid >= 0) {
@@ -478,13 +575,9 @@ __global__ void __launch_bounds__(kCtlThreads, 1) ctl_begin_kernel(Ctl c) {
     c.row_restarts[i] = 0;
     c.row_slot[i] = -1;
   }
-  // prefill rows of local admissions still running (prompt ++ kept[:-1])
-  __shared__ int sh_off;
+  // prefill rows of this rank's allocations, in allocation order (prompt ++ kept[:-1])
   __shared__ unsigned long long sh_ctx;
-  if (threadIdx.x == 0) {
-    sh_off = 0;
-    sh_ctx = 0;
-  }
+  if (threadIdx.x == 0) sh_ctx = 0;
   __syncthreads();
   atomicAdd(&sh_ctx, (unsigned long long)my_ctx);
   my_rows = block_sum(my_rows);
@@ -492,33 +585,27 @@ __global__ void __launch_bounds__(kCtlThreads, 1) ctl_begin_kernel(Ctl c) {
     s->st.sum_ctx = (long long)sh_ctx;
     s->st.r_local = my_rows;
   }
-  const int na = s->st.n_admit_local;
-  for (int a = 0; a < na; ++a) {
-    const int sl = c.admit_local[a];
-    const int g = sl * c.R + c.rank;
-    const int tid = c.slot_traj[g];
-    const int off = sh_off;
-    if (tid >= 0 && c.traj[tid].admit_step == s->k) {
-      const DevTraj& t = c.traj[tid];
-      const int cnt = t.prompt_len + t.n_tok - 1;
-      if (off + cnt <= c.prefill_rows_max) {
-        const int* pt = c.prompt_tok + c.prompt_off[t.prompt_idx];
-        const int* kt = c.tokens + (size_t)tid * c.cap;
-        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-          c.pre_tok[off + i] = i < t.prompt_len ? pt[i] : kt[i - t.prompt_len];
-          c.pre_pos[off + i] = i;
-          c.pre_slot[off + i] = sl;
-        }
+  const int na = sh_nalloc;
+  const int m_pre = c.pre_list[3 * na + 2];
+  if (m_pre <= c.prefill_rows_max) {
+    for (int a = 0; a < na; ++a) {
+      const int sl = c.pre_list[3 * a], p0 = c.pre_list[3 * a + 1], off = c.pre_list[3 * a + 2];
+      const int cnt = c.pre_list[3 * a + 5] - off;
+      const DevTraj& t = c.traj[c.slot_traj[sl * c.R + c.rank]];
+      const int* pt = c.prompt_tok + c.prompt_off[t.prompt_idx];
+      const int* kt = c.tokens + (size_t)c.slot_traj[sl * c.R + c.rank] * c.cap;
+      for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+        const int q = p0 + i;
+        c.pre_tok[off + i] = q < t.prompt_len ? pt[q] : kt[q - t.prompt_len];
+        c.pre_pos[off + i] = q;
+        c.pre_slot[off + i] = sl;
       }
-      __syncthreads();
-      if (threadIdx.x == 0) sh_off = off + cnt;
     }
-    __syncthreads();
   }
   if (threadIdx.x == 0) {
-    s->st.r_k = occ;
-    s->st.m_pre = sh_off;
-    fill_status(c, sh_off > c.prefill_rows_max ? SRL_E_CAPACITY : ST_CONTINUE);
+    s->st.r_k = dec;
+    s->st.m_pre = m_pre;
+    fill_status(c, m_pre > c.prefill_rows_max ? SRL_E_CAPACITY : ST_CONTINUE);
   }
 }
 
@@ -538,7 +625,7 @@ __global__ void __launch_bounds__(kCtlThreads, 1) ctl_end_kernel(Ctl c) {
     int fin = 0;
     if (g < c.Q_tot) {
       const int tid = c.slot_traj[g];
-      if (tid >= 0) {
+      if (tid >= 0 && c.traj[tid].pre_next >= c.traj[tid].pre_end) {  // decoded this step (N1: prefill complete)
         occ++;
         DevTraj& t = c.traj[tid];
         const int n = t.n_tok;
@@ -731,6 +818,8 @@ __global__ void ctl_init_kernel(Ctl c, int K) {
   CtlState* s = c.s;
   for (int g = threadIdx.x; g < c.Q_tot; g += blockDim.x) c.slot_traj[g] = -1;
   for (int p = threadIdx.x; p < c.kv_pages; p += blockDim.x) c.page_stack[p] = c.kv_pages - 1 - p;
+  for (int i = threadIdx.x; i < c.R * c.max_prompts; i += blockDim.x) c.pfx_ref[i] = c.pfx_tag[i] = 0;
+  for (int i = threadIdx.x; i < c.R * c.max_prompts; i += blockDim.x) c.pfx_valid[i] = 0;
   if (threadIdx.x == 0) {
     memset(s, 0, sizeof(CtlState));
     s->K = K;

@@ -150,6 +150,7 @@ struct ScratchPlan {
 
 struct Sizes {
   int Q_g, R, Q_tot, max_pages, max_ctx, max_prompts, mmax, prefill_rows_max, max_items, G;
+  int pfx_max;  // N4: shared prompt-prefix pages per (replica, prompt) entry
   long long ev_cap, h_cap_tok;
   size_t qkv_n;
 };
@@ -184,6 +185,10 @@ int validate(const srl_model_cfg* m, const srl_sched_cfg* s, int world, std::str
   if (s->max_traj <= 0 || s->max_prompt <= 0 || s->prefill_chunk <= 0) return why = "max_traj, max_prompt, prefill_chunk must be positive", -1;
   if (s->kv_dtype != SRL_KV_BF16 && s->kv_dtype != SRL_KV_FP32) return why = "kv_dtype", -1;
   if (s->top_k < 0 || !(s->top_p > 0.f && s->top_p <= 1.f)) return why = "top_k must be >= 0 and top_p in (0, 1]", -1;
+  if (s->share_prefix != 0 && s->share_prefix != 1) return why = "share_prefix must be 0 or 1", -1;
+  if (s->prefill_budget < 0) return why = "prefill_budget must be >= 0 (0 = unlimited)", -1;
+  if (s->prefill_budget > 0 && s->share_prefix && s->G > 1)
+    return why = "prefill_budget and share_prefix are exclusive (reading R30)", -1;
   return 0;
 }
 
@@ -195,6 +200,8 @@ Sizes compute_sizes(const srl_model_cfg* m, const srl_sched_cfg* s, int world) {
   z.max_ctx = s->max_prompt + s->cap;
   z.max_pages = (z.max_ctx + kPage - 1) / kPage;
   z.max_prompts = (s->max_traj + s->G - 1) / s->G + 1;
+  z.pfx_max = s->max_prompt > 1 ? (s->max_prompt - 1) / kPage : 0;
+  if (z.pfx_max < 1) z.pfx_max = 1;
   z.prefill_rows_max = s->Q_g * (z.max_ctx);
   z.mmax = s->Q_g + s->prefill_chunk;  // a mixed pass: Q_g decode rows + up to prefill_chunk prompt rows
   z.G = m->Hq / m->Hkv;
@@ -389,6 +396,11 @@ void plan_scratch(srl_engine* e, ScratchPlan& p, bool assign) {
   c.prompt_off = (int*)P(4ull * (z.max_prompts + 1));
   c.prompt_tok = (int*)P(4ull * z.max_prompts * s.max_prompt);
   c.events = (int*)P(24ull * z.ev_cap);
+  c.pfx_ref = (int*)P(4ull * z.R * z.max_prompts);
+  c.pfx_tag = (int*)P(4ull * z.R * z.max_prompts);
+  c.pfx_pages = (int*)P(4ull * z.max_prompts * z.pfx_max);
+  c.pfx_valid = (int*)P(4ull * z.R * z.max_prompts);
+  c.pre_list = (int*)P(12ull * (z.Q_g + 1));
   // decode rows [0, Q_g) and prefill rows [Q_g, ...) are one array each, so one
   // forward can run both (the mixed pass of a step with admissions)
   c.row_tok = (int*)P(4ull * (z.Q_g + z.prefill_rows_max));
@@ -406,7 +418,8 @@ void plan_scratch(srl_engine* e, ScratchPlan& p, bool assign) {
   c.h_lp = (float*)P(4ull * z.h_cap_tok);
   c.h_ver = (int*)P(4ull * z.h_cap_tok);
   c.h_rec = (srl_traj*)P(sizeof(srl_traj) * kMaxGroup);
-  e->norm_part_floats = 4ull * (z.Q_g > 512 ? z.Q_g : 512) * m.d;  // S <= 4 splits of <= 512 rows (gemm_partial_split)
+  // S <= 4 splits of <= 512 rows (gemm_partial_split), <= kNormMaxSplits of <= 256 rows (fused MLP)
+  e->norm_part_floats = std::max(4ull * (z.Q_g > 512 ? z.Q_g : 512), (unsigned long long)kNormMaxSplits * 256) * m.d;
   e->norm_part = (float*)P(4ull * e->norm_part_floats);
   e->qkv_part_floats = 4ull * (z.Q_g > 512 ? z.Q_g : 512) * z.qkv_n;
   e->qkv_part = (float*)P(4ull * e->qkv_part_floats);
@@ -524,6 +537,9 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
   int S_o = gemm_partial_split(M, d, qd, e->num_sms), S_d = gemm_partial_split(M, d, m.ff, e->num_sms);
   if ((size_t)S_o * M * d > e->norm_part_floats || S_o > 4) S_o = 1;  // rmsnorm sums <= 4 splits
   if ((size_t)S_d * M * d > e->norm_part_floats || S_d > 4) S_d = 1;
+  // fused MLP (decode rows 128..256 on the pair kernel): down k-splits for the RMSNorm
+  int mlp_S = tuning().fuse_mlp ? tuning().mlp_splits : 0;
+  if (mlp_S > kNormMaxSplits || (size_t)mlp_S * M * d > e->norm_part_floats) mlp_S = 0;
   // the QKV projection can likewise leave its partials to qkv_finish (bias, RoPE, KV
   // append) -- opt-in (srl_tuning.qkv_finish): measured r01 even with the in-GEMM
   // reduction (QKV class -0.02 ms, attention +0.1 ms per step)
@@ -593,15 +609,28 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
       rmsnorm(e->x_res, row_tok, row_pos, M, d, nullptr, w.mlp_norm, m.rms_eps, e->xn, st,
               S_o > 1 ? e->norm_part : nullptr, S_o, (size_t)M * d);
     }
-    run_gemm(e, D + SRL_K_GEMM_GU, e->xn, M, (const __nv_bfloat16*)w.pgu, 2 * m.ff, d, se);  // interleaved gate/up
-    run_gemm(e, D + SRL_K_GEMM_DOWN, e->act, M, (const __nv_bfloat16*)w.pd, d, m.ff, S_d > 1 ? pe : re);
+    // gate/up (SiLU-mul) and down: one persistent kernel whose down k-splits fill the
+    // gate/up tail (gemm_pair.cuh SPLIT 3), else two GEMMs
+    int S_dn = S_d, fused = 1;
+    if (mlp_S > 1) {
+      Prof p(e, D + SRL_K_GEMM_GU);
+      fused = gemm_mlp_fused(e->xn, M, w.pgu, m.ff, d, e->act, w.pd, e->norm_part, (size_t)M * d, mlp_S, e->gemm_ws,
+                             e->num_sms, st);
+      if (fused < 0) note_launch(e, "fused MLP launch", fused);
+      if (fused == 0) S_dn = mlp_S;
+      e->launches += fused == 0;
+    }
+    if (fused != 0) {
+      run_gemm(e, D + SRL_K_GEMM_GU, e->xn, M, (const __nv_bfloat16*)w.pgu, 2 * m.ff, d, se);  // interleaved gate/up
+      run_gemm(e, D + SRL_K_GEMM_DOWN, e->act, M, (const __nv_bfloat16*)w.pd, d, m.ff, S_d > 1 ? pe : re);
+    }
     {
       Prof p(e, D + SRL_K_ELEMWISE);
       const __nv_bfloat16* next = l + 1 < m.L ? e->lw[l + 1].attn_norm : e->final_norm;
       rmsnorm(e->x_res, row_tok, row_pos, M, d, nullptr, next, m.rms_eps, e->xn, st,
-              S_d > 1 ? e->norm_part : nullptr, S_d, (size_t)M * d);
+              S_dn > 1 ? e->norm_part : nullptr, S_dn, (size_t)M * d);
     }
-    e->launches += 4;
+    e->launches += 4;  // attention (2 launches) + the two RMSNorms
   }
   if (decode) {
     GemmEpi fe{};
@@ -929,6 +958,10 @@ int32_t srl_create(const srl_model_cfg* m, const srl_sched_cfg* s, int32_t devic
   c.max_traj = s->max_traj;
   c.max_prompt = s->max_prompt;
   c.prefill_rows_max = e->z.prefill_rows_max;
+  c.share_prefix = s->share_prefix && s->G > 1;
+  c.prefill_budget = s->prefill_budget;
+  c.max_prompts = e->z.max_prompts;
+  c.pfx_max = e->z.pfx_max;
   c.ev_cap = e->z.ev_cap;
   c.h_cap_tok = e->z.h_cap_tok;
   e->prompt_tok_cap = (long long)e->z.max_prompts * s->max_prompt;
@@ -1058,6 +1091,24 @@ int32_t srl_decode_step(srl_engine* e, srl_step_info* info) {
     return b.status;
   }
   const Ctl& c = e->ctl;
+  if (b.r_local == 0) {
+    // N1 (prefill budget): every running slot of this GPU is still prefilling -- the
+    // step is its prefill rows only, then the (replicated) controller END
+    for (int r0 = 0; r0 < b.m_pre; r0 += e->s.prefill_chunk) {
+      const int mc = b.m_pre - r0 < e->s.prefill_chunk ? b.m_pre - r0 : e->s.prefill_chunk;
+      Prof p(e, SRL_K_PREFILL, 2 + 8 * e->m.L);
+      forward(e, mc, c.pre_tok + r0, c.pre_pos + r0, c.pre_slot + r0, false);
+    }
+    e->last_m = 0;
+    if (e->comm) {
+      if (int rc = exchange_and_end(e)) return rc;
+    } else {
+      Prof p(e, SRL_K_CTL);
+      ctl_end(c, st);
+      e->launches++;
+    }
+    return finish_step(e, b, info, nullptr);
+  }
   if (e->mixed_ok && b.m_pre > 0 && b.m_pre <= e->s.prefill_chunk) {
     // steady state: the few admitted prompts join the decode pass (direct launches:
     // the row count varies)

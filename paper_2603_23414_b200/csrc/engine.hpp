@@ -26,7 +26,11 @@ struct DevTraj {
   int prompt_idx, prompt_len, forced_len, epoch;
   int n_tok, v_first, lifecycle, restarts;
   int admit_step, finish_step, state, slot;
-  int fresh, pages, sample, pad;
+  int fresh, pages, sample;
+  int shared;  // N4: prompt-prefix pages held through the replica's shared entry (page-table
+               // entries [0, shared)); the private pages are entries [shared, shared + pages)
+  int pre_next, pre_end;  // N1: next prefill position (-1: not started since admission) and the
+                          //     end of the prefill range (prompt ++ kept tokens minus the last)
 };
 
 // Host-visible status block (mirrored to pinned memory after each phase).
@@ -66,6 +70,8 @@ struct Ctl {
   // config
   int Q_g, R, rank, Q_tot, U, pool_traj, G, cap, kv_pages, max_pages;
   int mode, resume, barrier, stop, eos_id, max_traj, max_prompt, prefill_rows_max;
+  int share_prefix, max_prompts, pfx_max;  // N4: sharing on, prompt-table size, shared pages per entry
+  int prefill_budget;                      // N1: prefill positions per replica per step (0 = unlimited)
   long long ev_cap;
   // state
   CtlState* s;
@@ -82,6 +88,13 @@ struct Ctl {
   int* prompt_off;     // [max_prompts+1]
   int* prompt_tok;     // prompt token storage
   int* events;         // [ev_cap][6]
+  // N4 prompt-prefix sharing (oracle/sched.py _prefix_pages), one entry per (replica, prompt)
+  int* pfx_ref;        // [R][max_prompts] holders of the entry (replicated accounting)
+  int* pfx_tag;        // [R][max_prompts] policy version the entry's KV was computed under
+  int* pfx_pages;      // [max_prompts][pfx_max] page ids of this rank's entries
+  int* pfx_valid;      // [R][max_prompts] the entry's shared positions have been prefilled (in an
+                       //   earlier step or earlier in this step's rows) -- later holders skip them
+  int* pre_list;       // [Q_g][3] this step's own prefill allocations (local slot, first position, count)
   // per-step rows (this rank)
   int* row_tok;        // [Q_g]
   int* row_pos;        // [Q_g]  (-1 = inactive)

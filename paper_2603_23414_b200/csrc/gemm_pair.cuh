@@ -24,6 +24,17 @@
 //     shared memory of the CTA (same row half) that owns the chunk
 //     (st.shared::cluster, fire-and-forget), and the owner sums the S partials
 //     in pair (= k) order from local memory -- deterministic;
+//  3  fused MLP (gemm_pair_mlp_kernel): the gate/up GEMM (EPI_SILU, whole units,
+//     phase A) and the down GEMM (EPI_PARTIAL, S2 k-splits per tile, phase B) as
+//     ONE persistent work list per pair (FuseArgs, a host-built static schedule).
+//     A down k-split s reads act columns produced by a fixed range of gate/up units;
+//     each of their CTAs bumps done[s] after its act stores (release), and the X
+//     producer of a phase-B item waits for done[s] (acquire) before its first TMA of
+//     act.  Phase-A items precede phase-B items on every pair and phase-A items never
+//     wait, so with all CTAs co-resident (grid = 2 x pairs) nothing can deadlock.
+//     The weight producer streams phase-B weights ahead regardless (they are
+//     constant), so the down GEMM fills the gate/up GEMM's last partial wave instead
+//     of starting after it (r02: 112 gate/up units on 74 pairs = 1.51 waves).
 //  2  stream-K (opt-in, srl_tuning.gemm_split = 2): the flattened (unit, k-block) space
 //     is cut into #pairs equal ranges; a unit cut between pairs is finished by
 //     its LAST arriving piece: every piece stores its fp32 partial to an
@@ -117,10 +128,32 @@ __device__ __forceinline__ void sk_unit_pairs(const GemmParams& p, int u, int* q
 }
 __device__ __forceinline__ float4 ldcg_f4(const float4* a) { return __ldcg(a); }
 
+// Fused MLP work list (SPLIT 3).  Item ids < nA: phase-A unit; else j = id - nA:
+// phase-B k-split j / p2.n_tiles of tile j % p2.n_tiles (m_blocks == 1).
+constexpr int kFuseMaxPairs = 80, kFuseMaxItems = 8;
+struct FuseArgs {
+  CUtensorMap tmW2, tmX2;  // phase B: down weights (packed), act [M][ff]
+  GemmParams p2;
+  int nA;                  // phase-A units
+  int S2;                  // phase-B k-splits per tile
+  int a_per_split;         // phase-A units whose act columns one k-split reads
+  int* done;               // [S2] CTA completions of each split's phase-A units (self-resetting)
+  int* exit_ctr;
+  uint8_t n_items[kFuseMaxPairs];
+  uint8_t items[kFuseMaxPairs][kFuseMaxItems];
+};
+
+SRL_DEV int ld_acquire_gpu(const int* a) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+SRL_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
 // pair unit u -> (pair tile, batch block); pair tile t covers weight rows 256t..256t+255
 template <int SPLIT>
-__global__ void __launch_bounds__(kGemmThreads, 1)
-    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GemmParams p) {
+__device__ __forceinline__ void gemm_pair_body(const CUtensorMap& tmW, const CUtensorMap& tmX, const GemmParams& p,
+                                               const FuseArgs* fz) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int stage_b = (p.m_blk >> 1) * 128;  // this CTA's half of the activation slice
@@ -153,13 +186,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   int nseg;
   if (SPLIT == 1) nseg = 1;
   else if (SPLIT == 2) sk_piece(p, pid, -1, &nseg);
+  else if (SPLIT == 3) nseg = fz->n_items[pid];
   else nseg = pid < p.units ? (p.units - pid + npairs - 1) / npairs : 0;
-  // piece i of this pair: (unit, k-block range)
+  // piece i of this pair: (unit, k-block range[, phase])
   auto piece = [&](int i) -> Seg {
     if (SPLIT == 2) return sk_piece(p, pid, i);
     if (SPLIT == 1) return Seg{cl, pi * p.kb / p.S, (pi + 1) * p.kb / p.S};
+    if (SPLIT == 3) {
+      const int it = fz->items[pid][i];
+      if (it < fz->nA) return Seg{it, 0, p.kb, 0};
+      const int j = it - fz->nA, sp = j / fz->p2.n_tiles;
+      return Seg{j % fz->p2.n_tiles, sp * fz->p2.kb / fz->S2, (sp + 1) * fz->p2.kb / fz->S2, 1};
+    }
     return Seg{pid + i * npairs, 0, p.kb};
   };
+  // the GEMM (and its tensor maps) a piece belongs to
+  auto gp = [&](const Seg& sg) -> const GemmParams& { return (SPLIT == 3 && sg.ph) ? fz->p2 : p; };
   pdl_trigger();
 
   if (threadIdx.x == 0) {
@@ -179,6 +221,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     fence_barrier_init();
     tma_prefetch(&tmW);
     tma_prefetch(&tmX);
+    if (SPLIT == 3) {
+      tma_prefetch(&fz->tmW2);
+      tma_prefetch(&fz->tmX2);
+    }
   }
   if (w == 1) tmem_alloc_pair(tholder, p.tmem_cols);
   tc_fence_before();
@@ -197,14 +243,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       bool first = true;
       for (int i = 0; i < nseg; ++i) {
         const Seg sg = piece(i);
+        const GemmParams& q = gp(sg);
+        const CUtensorMap* tw = (SPLIT == 3 && sg.ph) ? &fz->tmW2 : &tmW;
         const int u = sg.u;
-        const int t128 = (u % p.n_tiles) * 2 + (int)r2;  // this CTA's 128-row tile
+        const int t128 = (u % q.n_tiles) * 2 + (int)r2;  // this CTA's 128-row tile
         for (int k = sg.k0; k < sg.k1; ++k) {
           mbar_wait(&empty[s], ph);
           if (is_leader) mbar_arrive_expect_tx(&full[s], 2 * kStageA);  // both CTAs' halves
-          const int c1 = p.wp ? (t128 * p.kb + k) * 128 : t128 * 128;
-          const int c0 = p.wp ? 0 : k * 64;
-          tma_load_2d_pair(sA + s * kStageA, &tmW, full_l + 8u * s, c0, c1, pol_w);
+          const int c1 = q.wp ? (t128 * q.kb + k) * 128 : t128 * 128;
+          const int c0 = q.wp ? 0 : k * 64;
+          tma_load_2d_pair(sA + s * kStageA, tw, full_l + 8u * s, c0, c1, pol_w);
           if (first) {
             DBG(2);
             first = false;
@@ -221,17 +269,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       const uint64_t pol_x = policy_evict_last();
       const uint32_t xfull_l = mapa_u32(smem_u32(xfull), leader);
+      bool xw = false;  // (profiling stamps of the first phase-B wait)
       int s = 0;
       uint32_t ph = 1;
       for (int i = 0; i < nseg; ++i) {
         const Seg sg = piece(i);
+        const GemmParams& q = gp(sg);
+        const CUtensorMap* tx = (SPLIT == 3 && sg.ph) ? &fz->tmX2 : &tmX;
         const int u = sg.u;
-        const int ncol = unit_cols(p, u);
-        const int mrow = (u / p.n_tiles) * p.m_blk + (int)r2 * (ncol >> 1);
+        const int ncol = unit_cols(q, u);
+        const int mrow = (u / q.n_tiles) * q.m_blk + (int)r2 * (ncol >> 1);
+        if (SPLIT == 3 && sg.ph) {
+          // phase B reads act columns [k0, k1) * 64: wait for the phase-A CTAs that
+          // write them (acquire), then order the async-proxy (TMA) reads after it
+          const int sp = sg.k0 * fz->S2 / q.kb;
+          if (!xw) DBG(13);
+          while (ld_acquire_gpu(fz->done + sp) < 2 * fz->a_per_split) __nanosleep(64);
+          fence_proxy_async_global();
+          if (!xw) DBG(15);
+          xw = true;
+        }
         for (int k = sg.k0; k < sg.k1; ++k) {
           mbar_wait(&xempty[s], ph);
           if (is_leader) mbar_arrive_expect_tx(&xfull[s], 2 * stage_b);
-          tma_load_2d_pair(sB + s * stage_b, &tmX, xfull_l + 8u * s, k * 64, mrow, pol_x);
+          tma_load_2d_pair(sB + s * stage_b, tx, xfull_l + 8u * s, k * 64, mrow, pol_x);
           if (++s == p.xstages) {
             s = 0;
             ph ^= 1;
@@ -249,7 +310,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int i = 0; i < nseg; ++i) {
         const Seg sg = piece(i);
         const int u = sg.u;
-        const uint32_t idesc = umma_idesc_bf16(256, unit_cols(p, u));
+        const uint32_t idesc = umma_idesc_bf16(256, unit_cols(gp(sg), u));
         const int a = i % p.acc_stages;
         mbar_wait(&tempty[a], ((i / p.acc_stages) & 1) ^ 1);
         tc_fence_after();
@@ -294,17 +355,35 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int cmax = p.m_blk >> 4;
     for (int i = 0; i < nseg; ++i) {
       const Seg sg = piece(i);
+      const GemmParams& q = gp(sg);
       const int u = sg.u;
-      const int unit_n0 = (u % p.n_tiles) * 256 + (int)r2 * 128, m_base = (u / p.n_tiles) * p.m_blk;
-      const int ncol = unit_cols(p, u), nchunk = ncol >> 4;
+      const int unit_n0 = (u % q.n_tiles) * 256 + (int)r2 * 128, m_base = (u / q.n_tiles) * q.m_blk;
+      const int ncol = unit_cols(q, u), nchunk = ncol >> 4;
       const int a = i % p.acc_stages;
-      const bool whole = sg.k0 == 0 && sg.k1 == p.kb;
-      fill_row_table(p, m_base, ncol, rtab, (int)threadIdx.x - 64);  // overlaps the MMAs
+      const bool whole = sg.k0 == 0 && sg.k1 == q.kb;
+      fill_row_table(q, m_base, ncol, rtab, (int)threadIdx.x - 64);  // overlaps the MMAs
       mbar_wait(&tfull[a], (i / p.acc_stages) & 1);
       tc_fence_after();
       if (lane == 0 && qw == 0 && i < 3) DBG(6 + i);
       const uint32_t tl = tbase + ((uint32_t)(qw * 32) << 16) + (uint32_t)(a * p.m_blk);
-      if (whole) {
+      if (SPLIT == 3 && sg.ph) {
+        // phase B: this k-split's fp32 partial of the down projection -> the next
+        // RMSNorm (sums the S2 splits in order + residual), as EPI_PARTIAL
+        const int sp = sg.k0 * fz->S2 / q.kb;
+        if (unit_n0 < q.N) {
+          float* dst = q.epi.part + (size_t)sp * q.epi.part_stride + unit_n0 + n;
+          const bool rok = unit_n0 + n < q.N;
+          for (int c = eg; c < nchunk; c += 2) {
+            float v[16];
+            tmem_ld16(tl + (uint32_t)(c * 16), v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int m = m_base + c * 16 + j;
+              if (rok && m < q.M) dst[(size_t)m * q.epi.ldo] = v[j];  // a warp writes 128 contiguous bytes
+            }
+          }
+        }
+      } else if (whole) {
         if (unit_n0 < p.N) {
           for (int cc = eg * 16; cc < ncol; cc += 32) {
             float v[16];
@@ -340,7 +419,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_l + 8u * a);  // TMEM buffer free: the next piece may accumulate
       if (lane == 0 && qw == 0 && i < 3) DBG(9 + i);
-      if (!whole) {
+      if (SPLIT == 3 && !sg.ph) {
+        // phase A: this CTA's act columns of unit u are stored -- count them into the
+        // k-split of the down GEMM that reads them (release after a CTA barrier)
+        fence_proxy_async_global();
+        asm volatile("bar.sync 4, 256;" ::: "memory");
+        if (w == 2 && lane == 0) {
+          __threadfence();
+          atomicAdd(fz->done + u / fz->a_per_split, 1);
+        }
+      }
+      if (SPLIT == 2 && !whole) {
         // count the piece in; the CTA completing the count reduces the unit (this row half)
         int q0, q1;
         sk_unit_pairs(p, u, &q0, &q1);
@@ -490,4 +579,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   cluster_sync_all();  // both CTAs done with the pair's TMEM before it is freed
   if (threadIdx.x == 0) DBG(12);
   if (w == 1) tmem_dealloc_pair(tbase, p.tmem_cols);
+  if (SPLIT == 3 && threadIdx.x == 0) {
+    // the last CTA out re-arms the split counters for the next launch (nobody waits
+    // on them any more: every phase-B item of every CTA has been loaded)
+    __threadfence();
+    if (atomicAdd(fz->exit_ctr, 1) == (int)gridDim.x - 1) {
+      for (int i = 0; i < fz->S2; ++i) fz->done[i] = 0;
+      *fz->exit_ctr = 0;
+      __threadfence();
+    }
+  }
+}
+
+template <int SPLIT>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GemmParams p) {
+  gemm_pair_body<SPLIT>(tmW, tmX, p, nullptr);
+}
+
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_pair_mlp_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, GemmParams p,
+                         const __grid_constant__ FuseArgs f) {
+  gemm_pair_body<3>(tmW, tmX, p, &f);
 }

@@ -37,6 +37,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
+#include <vector>
 
 #include "common.cuh"
 #include "gumbel.cuh"
@@ -107,6 +109,7 @@ SRL_DEV float4 ld_dsmem_f4(uint32_t local_addr, uint32_t rank) {
 // segment i of this CTA: unit and k-block range
 struct Seg {
   int u, k0, k1;
+  int ph = 0;  // fused MLP kernel: 0 = phase A (gate/up) unit, 1 = phase B (down) k-split
 };
 template <int SPLIT>
 __device__ __forceinline__ int seg_count(const GemmParams& p) {
@@ -512,9 +515,11 @@ static int single_partial_split(int units, int kb, int num_sms) {
   return S;
 }
 
-size_t gemm_workspace_bytes(int num_sms) {
+// fused-MLP split counters + exit counter, after the stream-K slots and counters
+static size_t fuse_ctr_offset(int num_sms) {
   return (size_t)num_sms * 2 * kSkSlotBytes + (size_t)kSkMaxUnits * 2 * sizeof(int);
 }
+size_t gemm_workspace_bytes(int num_sms) { return fuse_ctr_offset(num_sms) + 64 * sizeof(int); }
 
 static int gemm_pair_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N, int K, const GemmEpi& epi,
                            int num_sms, cudaStream_t stream, int* plan_s = nullptr) {
@@ -630,6 +635,141 @@ static int gemm_pair_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W
   } else {
     rc = launch_cluster(gemm_pair_kernel<1>, p.units * 2 * S, p.split_pairs ? 2 : 2 * S, smem, stream, tmW, tmX, p);
   }
+  if (rc) cudaGetLastError();
+  return rc;
+}
+
+// ---------------------------------------------------------------- fused MLP (SPLIT 3)
+// Static per-pair work list: phase-A (gate/up) units round-robin, then every
+// phase-B (down) k-split item, in split order, to the pair where it can start first
+// (the later of the pair's finish time and the time its split's act columns are
+// complete), costs in k-blocks -- a list-scheduling makespan model of the tensor /
+// weight-stream-bound items.  Cached per shape.
+struct FuseSched {
+  bool ok = false;
+  uint8_t n_items[kFuseMaxPairs];
+  uint8_t items[kFuseMaxPairs][kFuseMaxItems];
+};
+static const FuseSched& fuse_schedule(int P, int nA, int nt2, int S2, int kbA, int kbB) {
+  static std::vector<std::pair<std::vector<int>, FuseSched>> cache;
+  const std::vector<int> key{P, nA, nt2, S2, kbA, kbB};
+  for (const auto& c : cache)
+    if (c.first == key) return c.second;
+  FuseSched f;
+  memset(f.n_items, 0, sizeof(f.n_items));
+  bool ok = P <= kFuseMaxPairs && nA % S2 == 0 && nA + S2 * nt2 <= 255;
+  std::vector<long long> t(P, 0), avail(S2, 0);
+  const int apS = ok ? nA / S2 : 1;
+  for (int u = 0; ok && u < nA; ++u) {
+    const int q = u % P;
+    if (f.n_items[q] >= kFuseMaxItems) ok = false;
+    else f.items[q][f.n_items[q]++] = (uint8_t)u;
+    t[q] += kbA;
+    avail[u / apS] = std::max(avail[u / apS], (long long)(u / P + 1) * kbA);
+  }
+  const int cB = kbB / S2;
+  for (int j = 0; ok && j < S2 * nt2; ++j) {
+    const long long av = avail[j / nt2];
+    int best = -1;
+    long long bs = 0;
+    for (int q = 0; q < P; ++q) {
+      if (f.n_items[q] >= kFuseMaxItems) continue;
+      const long long st = std::max(t[q], av);
+      if (best < 0 || st < bs) {
+        best = q;
+        bs = st;
+      }
+    }
+    if (best < 0) {
+      ok = false;
+      break;
+    }
+    f.items[best][f.n_items[best]++] = (uint8_t)(nA + j);
+    t[best] = bs + cB;
+  }
+  f.ok = ok;
+  cache.emplace_back(key, f);
+  return cache.back().second;
+}
+
+int gemm_mlp_fused(const __nv_bfloat16* X, int M, const void* Wgu, int ff, int d, __nv_bfloat16* act, const void* Wd,
+                   float* part, size_t part_stride, int S2, void* ws, int num_sms, cudaStream_t stream) {
+  const int pairs = num_sms / 2;
+  if (M < 128 || M > 256 || !ws || S2 < 1 || ff % (S2 * 128) || (2 * ff) % 256 || d % 256 || d % 64 || ff % 64 ||
+      pairs > kFuseMaxPairs)
+    return 1;
+  GemmParams p;
+  memset(&p, 0, sizeof(p));
+  p.M = M;
+  p.N = 2 * ff;
+  p.K = d;
+  p.m_blk = pick_mblk(M);
+  p.m_blocks = 1;
+  p.H = 1;
+  p.kb = d / 64;
+  p.n_tiles = p.N / 256;
+  p.units = p.n_tiles;
+  p.S = 1;
+  p.epi.kind = EPI_SILU;
+  p.epi.w_packed = 1;
+  p.epi.act = act;
+  p.epi.ldo = ff;
+  p.wp = reinterpret_cast<const uint8_t*>(Wgu);
+  p.dbg = (g_dbg && g_dbg_count++ == g_dbg_target) ? g_dbg : nullptr;
+  static FuseArgs f;  // host staging of the grid-constant argument (1.6 KB)
+  memset(&f, 0, sizeof(f));
+  GemmParams& q = f.p2;
+  q = p;
+  q.N = d;
+  q.K = ff;
+  q.kb = ff / 64;
+  q.n_tiles = d / 256;
+  q.units = q.n_tiles;
+  q.epi = GemmEpi{};
+  q.epi.kind = EPI_PARTIAL;
+  q.epi.w_packed = 1;
+  q.epi.part = part;
+  q.epi.part_stride = part_stride;
+  q.epi.ldo = d;
+  q.wp = reinterpret_cast<const uint8_t*>(Wd);
+  q.dbg = nullptr;
+  const FuseSched& fs = fuse_schedule(pairs, p.units, q.n_tiles, S2, p.kb, q.kb);
+  if (!fs.ok) return 1;
+  memcpy(f.n_items, fs.n_items, sizeof(f.n_items));
+  memcpy(f.items, fs.items, sizeof(f.items));
+  f.nA = p.units;
+  f.S2 = S2;
+  f.a_per_split = p.units / S2;
+  f.done = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + fuse_ctr_offset(num_sms));
+  f.exit_ctr = f.done + 32;
+  const int stage_b = (p.m_blk >> 1) * 128;
+  const int budget = 200 * 1024;
+  const int xstages = stage_b <= 4096 ? 8 : (stage_b <= 8192 ? 6 : 4);
+  int stages = (budget - xstages * stage_b) / kStageA;
+  if (stages > 12) stages = 12;
+  p.stages = q.stages = stages;
+  p.xstages = q.xstages = xstages;
+  p.acc_stages = q.acc_stages = 2;
+  int tc = 32;
+  while (tc < p.m_blk * 2) tc <<= 1;
+  p.tmem_cols = q.tmem_cols = tc;
+  CUtensorMap tmW, tmX;
+  const uint64_t rowsA = (uint64_t)(p.N / 128) * p.kb * 128, rowsB = (uint64_t)(q.N / 128) * q.kb * 128;
+  if (tma_encode_2d(&tmW, Wgu, rowsA, 64, 128, 128, 64, 2, false)) return -2;
+  if (tma_encode_2d(&f.tmW2, Wd, rowsB, 64, 128, 128, 64, 2, false)) return -2;
+  if (tma_encode_2d(&tmX, X, M, d, (uint64_t)d * 2, p.m_blk >> 1, 64, 2, true)) return -2;
+  if (tma_encode_2d(&f.tmX2, act, M, ff, (uint64_t)ff * 2, p.m_blk >> 1, 64, 2, true)) return -2;
+  const size_t rings = (size_t)stages * kStageA + (size_t)xstages * stage_b;
+  const size_t smem = 1024 + rings + (2 * stages + 2 * xstages + 4) * 8 + 16 + 2 * kXchFloats * 4 + kRowTab * 4;
+  if (once_per_device(kOnceGemmMlp))
+    cudaFuncSetAttribute(gemm_pair_mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (tuning().verbose)
+    fprintf(stderr, "gemm(mlp) M=%d ff=%d d=%d unitsA=%d itemsB=%d S2=%d stages=%d/%d smem=%zu\n", M, ff, d, p.units,
+            S2 * q.n_tiles, S2, stages, xstages, smem);
+  const int rc = launch_k(gemm_pair_mlp_kernel, dim3(2 * pairs), dim3(kGemmThreads), smem, stream, 2, tmW, tmX, p, f) ==
+                         cudaSuccess
+                     ? 0
+                     : -3;
   if (rc) cudaGetLastError();
   return rc;
 }

@@ -66,6 +66,14 @@ int gemm_partial_split(int M, int N, int K, int num_sms);
 int gemm_bf16_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N, int K, const GemmEpi& epi,
                     int num_sms, cudaStream_t stream);
 void gemm_set_debug(unsigned long long* buf, int target);
+// The decode MLP as one persistent tcgen05 kernel (gemm_pair.cuh SPLIT 3): act =
+// silu(X Wg^T) * (X Wu^T) (EPI_SILU, interleaved packed gate/up weights Wgu [2ff, d])
+// and the S2 k-split fp32 partials of act Wd^T (packed Wd [d, ff]) written to
+// part + s * part_stride as [M][d] (the next RMSNorm sums them in split order).
+// ws: the GEMM workspace (zero-filled once; left zeroed).  Returns 0, 1 (not
+// applicable: the caller runs the two GEMMs) or < 0 (encode / launch failure).
+int gemm_mlp_fused(const __nv_bfloat16* X, int M, const void* Wgu, int ff, int d, __nv_bfloat16* act, const void* Wd,
+                   float* part, size_t part_stride, int S2, void* ws, int num_sms, cudaStream_t stream);
 
 // Packed weight layout for the GEMM's weight stream: [ceil(N/128)][K/64] blocks of
 // 16 KB, block (t, k) = rows 128t..128t+127 x cols 64k..64k+63 stored exactly as

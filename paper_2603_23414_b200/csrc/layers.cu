@@ -61,15 +61,15 @@ __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(float* __restrict
         if (part) {
           // the previous split-K GEMM's partials: summed in split (= k) order, then
           // added to the residual -- the same fp32 operations its own epilogue did
-          // (up to 4 splits, all loads in flight before the adds)
-          float4 q[4];
+          // (up to kNormMaxSplits splits, all loads in flight before the adds)
+          float4 q[kNormMaxSplits];
 #pragma unroll
-          for (int sp = 0; sp < 4; ++sp)
+          for (int sp = 0; sp < kNormMaxSplits; ++sp)
             q[sp] = sp < nsplit ? __ldcg(reinterpret_cast<const float4*>(part + sp * part_stride + (size_t)m * d) + i)
                                 : make_float4(0.f, 0.f, 0.f, 0.f);
           float4 acc = q[0];
 #pragma unroll
-          for (int sp = 1; sp < 4; ++sp)
+          for (int sp = 1; sp < kNormMaxSplits; ++sp)
             if (sp < nsplit) {
               acc.x += q[sp].x;
               acc.y += q[sp].y;

@@ -7,6 +7,7 @@
 namespace srl {
 
 void rope_table(float* cos_t, float* sin_t, int max_pos, int dh, double theta, cudaStream_t st);
+constexpr int kNormMaxSplits = 8;  // split-K partials one RMSNorm can sum
 // RMSNorm of the fp32 residual rows into the bf16 GEMM operand; with `embed`
 // non-null the residual row is first set to the embedding of row_tok[m].
 // part (optional): nsplit fp32 partials [M][d] (part_stride floats apart) of the

@@ -22,11 +22,12 @@ extern "C" const char* srl_last_error(void) { return g_last_error.c_str(); }
 
 // ------------------------------------------------------------------ tuning
 namespace srl {
-srl_tuning g_tuning = {
+static const srl_tuning kDefaultTuning = {
     /*gemm_split*/ 1, /*gemm_pair*/ -1, /*gemm_h*/ 0, /*gemm_stages*/ 0, /*gemm_xstages*/ 0,
     /*partial_norm*/ 1, /*partial_small_m*/ 0, /*qkv_finish*/ 0, /*fused_sample*/ 0,
     /*attn_min_items*/ 0, /*attn_target_items*/ 0, /*attn_l2_prefetch*/ 0,
-    /*pdl*/ 1, /*graphs*/ 1, /*mixed_prefill*/ 1, /*verbose*/ 0};
+    /*pdl*/ 1, /*graphs*/ 1, /*mixed_prefill*/ 1, /*verbose*/ 0, /*fuse_mlp*/ 1, /*mlp_splits*/ 8};
+srl_tuning g_tuning = kDefaultTuning;
 
 bool once_per_device(int slot) {
   static std::atomic<unsigned long long> done[kOnceSlots];
@@ -40,8 +41,7 @@ bool once_per_device(int slot) {
 
 extern "C" void srl_default_tuning(srl_tuning* t) {
   if (!t) return;
-  srl_tuning d = {1, -1, 0, 0, 0, 1, 0, 0, 0, 0, 0, 0, 1, 1, 1, 0};
-  *t = d;
+  *t = srl::kDefaultTuning;
 }
 
 extern "C" int32_t srl_get_tuning(srl_tuning* t) {
@@ -60,7 +60,8 @@ extern "C" int32_t srl_set_tuning(const srl_tuning* t) {
   }
   if (t->gemm_split < 0 || t->gemm_split > 3 || t->gemm_pair < -1 || t->gemm_pair > 1 || t->gemm_h < 0 ||
       t->gemm_h > 2 || t->gemm_stages < 0 || t->gemm_xstages < 0 || t->attn_min_items < 0 ||
-      t->attn_target_items < 0 || t->attn_l2_prefetch < 0 || t->attn_l2_prefetch > 16) {
+      t->attn_target_items < 0 || t->attn_l2_prefetch < 0 || t->attn_l2_prefetch > 16 || t->mlp_splits < 1 ||
+      t->mlp_splits > 8) {
     set_error("srl_set_tuning: %s", "field out of range", 0);
     return -1;
   }
@@ -113,6 +114,24 @@ extern "C" int32_t srl_op_gemm_bf16(const void* X, int32_t M, const void* W, int
   int r = gemm_bf16_fused(reinterpret_cast<const __nv_bfloat16*>(X), M, reinterpret_cast<const __nv_bfloat16*>(W),
                           rows, K, e, sms, st);
   if (r) set_error("srl_op_gemm_bf16: %s (code %ld)", r == -1 ? "bad shape" : "launch/tma failure", r);
+  return r;
+}
+
+extern "C" int32_t srl_op_mlp_bf16(const void* X, int32_t M, const void* Wgu_packed, const void* Wd_packed, int32_t d,
+                                   int32_t ff, int32_t splits, void* act_out, float* part_out, void* workspace,
+                                   void* stream) {
+  if (!X || !Wgu_packed || !Wd_packed || !act_out || !part_out || !workspace || M <= 0 || d <= 0 || ff <= 0 ||
+      splits < 1 || splits > 8) {
+    set_error("srl_op_mlp_bf16: %s", "bad arguments", 0);
+    return -1;
+  }
+  const int r = gemm_mlp_fused(reinterpret_cast<const __nv_bfloat16*>(X), M, Wgu_packed, ff, d,
+                               reinterpret_cast<__nv_bfloat16*>(act_out), Wd_packed, part_out, (size_t)M * d, splits,
+                               workspace, op_sms(), reinterpret_cast<cudaStream_t>(stream));
+  if (r < 0) {
+    set_error("srl_op_mlp_bf16: %s (code %ld)", "launch/tma failure", r);
+    return -1;
+  }
   return r;
 }
 

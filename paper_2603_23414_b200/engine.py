@@ -130,7 +130,8 @@ class RolloutEngine:
         self.s = SchedCfg(sched.Q_g, sched.U, sched.K, sched.pool_prompts, sched.G, sched.cap, sched.page_tokens,
                           sched.kv_pages, sched.mode, sched.resume, sched.barrier, sched.stop, sched.eos_id,
                           sched.kv_dtype, float(sched.temperature), int(sched.sample_seed), max_traj, max_prompt,
-                          prefill_chunk, int(getattr(sched, "top_k", 0)), float(getattr(sched, "top_p", 1.0)))
+                          prefill_chunk, int(getattr(sched, "top_k", 0)), float(getattr(sched, "top_p", 1.0)),
+                          int(getattr(sched, "share_prefix", 0)), int(getattr(sched, "prefill_budget", 0)))
         wb, kb, sb = C.c_uint64(), C.c_uint64(), C.c_uint64()
         check(self.lib.srl_arena_sizes(C.byref(self.m), C.byref(self.s), world, C.byref(wb), C.byref(kb),
                                        C.byref(sb)), "srl_arena_sizes")

@@ -121,6 +121,64 @@ def test_gemm_silu_mul_epilogue(lib, M, N, K, packed):
     assert ((out.double() - ref).abs() <= 2.0 ** -8 * ref.abs() + 1e-4).all()
 
 
+# ------------------------------------------------------------------ fused MLP (gate/up + down, one kernel)
+@pytest.mark.parametrize("M,d,ff,splits", [(256, 4096, 14336, 8), (256, 4096, 14336, 4), (128, 4096, 14336, 8),
+                                           (208, 4096, 14336, 8), (144, 512, 2048, 2), (256, 1024, 3072, 3)])
+def test_mlp_fused_matches_unfused_and_fp64(lib, M, d, ff, splits):
+    """srl_op_mlp_bf16: act within the bf16 rounding of the fp64 SiLU-mul and, at the
+    LLaMA width, bit-identical to the separate SiLU-mul GEMM (same whole-unit MMA order);
+    the down projection (sum of the k-split partials in split order) within
+    the fp32-accumulation bound of the fp64 product of that act with Wd; two launches
+    bit-identical (split counters re-armed by the kernel)."""
+    g = torch.Generator(device="cuda").manual_seed(M + d + ff)
+    X = (torch.randn(M, d, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    Wg = (torch.randn(ff, d, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    Wu = (torch.randn(ff, d, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    Wd = (torch.randn(d, ff, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    W = torch.stack([Wg.view(ff // 64, 64, d), Wu.view(ff // 64, 64, d)], dim=1).reshape(2 * ff, d).contiguous()
+    Wgu_p, Wd_p = _pack(lib, W), _pack(lib, Wd)
+    ws = torch.zeros(lib.srl_op_gemm_workspace(M, d, ff, 1), dtype=torch.uint8, device="cuda")
+    outs = []
+    for _ in range(2):
+        act = torch.full((M, ff), float("nan"), dtype=torch.bfloat16, device="cuda")
+        part = torch.full((splits, M, d), float("nan"), dtype=torch.float32, device="cuda")
+        rc = lib.srl_op_mlp_bf16(X.data_ptr(), M, Wgu_p.data_ptr(), Wd_p.data_ptr(), d, ff, splits, act.data_ptr(),
+                                 part.data_ptr(), ws.data_ptr(), _stream())
+        torch.cuda.synchronize()
+        assert rc == 0
+        outs.append((act, part))
+    assert torch.equal(outs[0][0].view(torch.int16), outs[1][0].view(torch.int16))
+    assert torch.equal(outs[0][1].view(torch.int32), outs[1][1].view(torch.int32))
+    assert torch.count_nonzero(ws).item() == 0                  # workspace left zeroed
+    act, part = outs[0]
+    gte, up = X.double() @ Wg.double().t(), X.double() @ Wu.double().t()
+    ref_a = gte / (1 + torch.exp(-gte)) * up
+    assert ((act.double() - ref_a).abs() <= 2.0 ** -8 * ref_a.abs() + 1e-4).all()
+    if 2 * ff // 256 >= 74:
+        # the separate SiLU-mul GEMM runs the same whole units (no split-K) at this width
+        ref_act = torch.empty(M, ff, dtype=torch.bfloat16, device="cuda")
+        assert _gemm(lib, X, W, ff, 2, ref_act, packed=True) == 0
+        assert torch.equal(act.view(torch.int16), ref_act.view(torch.int16))
+    y = part[0].clone()
+    for s_ in range(1, splits):
+        y += part[s_]
+    ref = act.double() @ Wd.double().t()
+    assert ((y.double() - ref).abs() <= _bound(act, Wd)).all()
+    # each partial is its own k-range's product
+    ks = ff // splits
+    ref1 = act[:, ks:2 * ks].double() @ Wd[:, ks:2 * ks].double().t() if splits > 1 else ref
+    assert ((part[min(1, splits - 1)].double() - ref1).abs() <= _bound(act[:, ks:2 * ks] if splits > 1 else act,
+                                                                       Wd[:, ks:2 * ks] if splits > 1 else Wd)).all()
+
+
+def test_mlp_fused_unsupported_shapes(lib):
+    dummy = torch.zeros(16, dtype=torch.uint8, device="cuda")
+    p = dummy.data_ptr()
+    assert lib.srl_op_mlp_bf16(p, 64, p, p, 4096, 14336, 8, p, p, p, _stream()) == 1       # M < 128
+    assert lib.srl_op_mlp_bf16(p, 256, p, p, 4096, 14336 + 64, 8, p, p, p, _stream()) == 1  # ff % (128 splits)
+    assert lib.srl_op_mlp_bf16(p, 256, p, p, 4096, 14336, 9, p, p, p, _stream()) == -1      # splits > 8
+
+
 def test_gemm_rejects_bad_shapes(lib):
     assert lib.srl_op_gemm_bf16(0, 16, 0, 128, 100, 0, 0, 0, _stream()) < 0      # K % 64
     assert lib.srl_op_gemm_bf16(0, 16, 0, 100, 128, 2, 0, 0, _stream()) < 0      # silu needs N % 64

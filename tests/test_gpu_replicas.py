@@ -44,7 +44,7 @@ def _oracle(cfg, off, toks, L, runner=None):
     return c, groups
 
 
-def _run_replicas(cfg, off, toks, L, *, record_logits=False, max_traj=64):
+def _run_replicas(cfg, off, toks, L, *, record_logits=False, max_traj=64, max_prompt=16):
     """R engines on cuda:0, one thread each, in-process exchange."""
     from paper_2603_23414_b200.engine import LocalGroup
     R = cfg.R
@@ -54,7 +54,7 @@ def _run_replicas(cfg, off, toks, L, *, record_logits=False, max_traj=64):
     def work(r):
         try:
             torch.cuda.set_device(0)
-            eng = make_engine(TINY, cfg, max_traj=max_traj, max_prompt=16, rank=r, world=R, local_group=grp)
+            eng = make_engine(TINY, cfg, max_traj=max_traj, max_prompt=max_prompt, rank=r, world=R, local_group=grp)
             out[r] = run_engine(eng, TINY, off, toks, L, record_logits=record_logits)
             out[r]["counters"] = eng.counters()
             eng.close()

@@ -16,7 +16,7 @@ from paper_2603_23414_b200 import _lib
 lib = _lib.load()
 lib.srl_debug_gemm_timestamps.argtypes = [ctypes.c_void_p, ctypes.c_int32]
 NAMES = ["start", "setup", "tma0", "tma_done", "mma0", "mma_done", "e_full0", "e_full1", "e_full2", "e_done0",
-         "e_done1", "e_done2", "end", "csync1", "pushed", "reduced"]
+         "e_done1", "e_done2", "end", "csync1/xwait0", "pushed/epi_end", "reduced/xwait1"]
 
 
 def report(title, dbg):
@@ -94,8 +94,34 @@ def engine(L):
     print({k: round(v[0] / 5 / (L if k.startswith("gemm") else 1), 4) for k, v in eng.profile().items()})
 
 
+def mlp(M, S2, d=4096, ff=14336):
+    """one srl_op_mlp_bf16 launch (fused gate/up + down)"""
+    def pack(W):
+        dst = torch.empty(lib.srl_op_packed_weight_bytes(W.shape[0], W.shape[1]), dtype=torch.uint8, device="cuda")
+        lib.srl_op_pack_weight(W.data_ptr(), W.shape[0], W.shape[1], dst.data_ptr(), s)
+        return dst
+    s = torch.cuda.current_stream().cuda_stream
+    gu = [pack((torch.randn(2 * ff, d, device="cuda") * 0.02).to(torch.bfloat16)) for _ in range(3)]
+    dn = [pack((torch.randn(d, ff, device="cuda") * 0.02).to(torch.bfloat16)) for _ in range(3)]
+    X = torch.randn(M, d, device="cuda").to(torch.bfloat16)
+    act = torch.empty(M, ff, dtype=torch.bfloat16, device="cuda")
+    part = torch.empty(8, M, d, dtype=torch.float32, device="cuda")
+    ws = torch.zeros(lib.srl_op_gemm_workspace(M, d, ff, 1), dtype=torch.uint8, device="cuda")
+    dbg = torch.zeros(200 * 16, dtype=torch.int64, device="cuda")
+    for i in range(5):
+        if i == 4:
+            lib.srl_debug_gemm_timestamps(dbg.data_ptr(), 0)
+        lib.srl_op_mlp_bf16(X.data_ptr(), M, gu[i % 3].data_ptr(), dn[i % 3].data_ptr(), d, ff, S2, act.data_ptr(),
+                            part.data_ptr(), ws.data_ptr(), s)
+        torch.cuda.synchronize()
+    lib.srl_debug_gemm_timestamps(None, 0)
+    report(f"mlp M={M} S2={S2}", dbg)
+
+
 if __name__ == "__main__":
-    if sys.argv[1] == "op":
+    if sys.argv[1] == "mlp":
+        mlp(int(sys.argv[2]), int(sys.argv[3]))
+    elif sys.argv[1] == "op":
         op(*map(int, sys.argv[2:6]))
     else:
         engine(int(sys.argv[2]) if len(sys.argv) > 2 else 4)
