@@ -368,8 +368,12 @@ typedef struct srl_tuning {
   int32_t graphs;          /* 1: replay the decode tail from CUDA graphs */
   int32_t mixed_prefill;   /* 1: admitted prompts ride in the decode pass when they fit one chunk */
   int32_t verbose;         /* 1: print GEMM plans to stderr */
-  int32_t fuse_mlp;        /* 1: gate/up and down GEMMs as one persistent kernel (128 <= M <= 256) */
+  int32_t fuse_mlp;        /* 1: gate/up and down GEMMs as one persistent kernel (128 <= M <= 256);
+                              measured r02 equal to the two PDL-chained GEMMs, off */
   int32_t mlp_splits;      /* k-splits of the fused down GEMM (its partials go to the next RMSNorm), 1..8 */
+  int32_t qkv_attn;        /* 1 (default): pure decode passes leave QKV split-K partials to the attention
+                              kernel, whose finish warp completes q / k / v per item (bias, RoPE, KV
+                              append) ahead of its TMA producer */
 } srl_tuning;
 void srl_default_tuning(srl_tuning* t);
 int32_t srl_get_tuning(srl_tuning* t);

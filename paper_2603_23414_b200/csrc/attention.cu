@@ -316,7 +316,9 @@ __global__ void __launch_bounds__(kF32Threads) attn_f32_kernel(AttnArgs a) {
 // ---------------------------------------------------------------- bf16 KV (TMA + mma.sync)
 constexpr int kStages = 4;
 constexpr int kConsumerWarps = 4;
-constexpr int kAttnThreads = (kConsumerWarps + 1) * 32;
+constexpr int kFinishWarp = kConsumerWarps + 1;          // fused QKV finish (idle otherwise)
+constexpr int kAttnThreads = (kConsumerWarps + 2) * 32;
+constexpr int kFQ = 2;  // finished items handed from the finish warp to the producer
 
 template <int DH>
 struct AttnCfg {
@@ -360,6 +362,76 @@ __device__ __forceinline__ ItemInfo item_info(const AttnArgs& a, int it) {
   return r;
 }
 
+// Fused QKV finish for one item (the whole producer warp): q of the item's G query
+// heads and, for the item holding the row's last page, the new token's k / v --
+// sum of the qkv_S partials in split order, + bias, RoPE on q / k (rotate-half pairs
+// (i, i + dh/2), the EPI_QKV epilogue's arithmetic), stored as bf16.
+template <int DH>
+__device__ __forceinline__ void qkv_finish_item(const AttnArgs& a, const ItemInfo& ii, int G, bool last, int lane) {
+  constexpr int HALF = DH / 2;
+  const int pos = ii.ctx - 1;
+  const float* cs = a.rope_cos + (size_t)pos * HALF;
+  const float* sn = a.rope_sin + (size_t)pos * HALF;
+  const size_t rowoff = (size_t)ii.m * a.Nqkv;
+  // heads of this item: G query heads, then (last) the k and v head
+  const int nh = G + (last ? 2 : 0);
+  for (int t = lane; t < nh * (HALF / 4); t += 32) {
+    const int hh = t / (HALF / 4), i = (t % (HALF / 4)) * 4;
+    int col;  // first column of the head in the QKV output
+    if (hh < G) col = (ii.kvh * G + hh) * DH;
+    else if (hh == G) col = (a.Hq + ii.kvh) * DH;
+    else col = (a.Hq + a.Hkv + ii.kvh) * DH;
+    float x0[4] = {0.f, 0.f, 0.f, 0.f}, x1[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int sp = 0; sp < a.qkv_S; ++sp) {  // split (= k) order
+      const float* pp = a.qkv_part + sp * a.qkv_part_stride + rowoff + col;
+      const float4 u0 = __ldcg(reinterpret_cast<const float4*>(pp + i));
+      const float4 u1 = __ldcg(reinterpret_cast<const float4*>(pp + i + HALF));
+      x0[0] += u0.x; x0[1] += u0.y; x0[2] += u0.z; x0[3] += u0.w;
+      x1[0] += u1.x; x1[1] += u1.y; x1[2] += u1.z; x1[3] += u1.w;
+    }
+    if (a.qkv_bias) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        x0[k] += __bfloat162float(a.qkv_bias[col + i + k]);
+        x1[k] += __bfloat162float(a.qkv_bias[col + i + HALF + k]);
+      }
+    }
+    float y0[4], y1[4];
+    if (hh <= G) {  // q and k heads are rotated
+      const float4 c = __ldg(reinterpret_cast<const float4*>(cs + i));
+      const float4 s = __ldg(reinterpret_cast<const float4*>(sn + i));
+      const float cc[4] = {c.x, c.y, c.z, c.w}, ss[4] = {s.x, s.y, s.z, s.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        y0[k] = x0[k] * cc[k] - x1[k] * ss[k];
+        y1[k] = x1[k] * cc[k] + x0[k] * ss[k];
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        y0[k] = x0[k];
+        y1[k] = x1[k];
+      }
+    }
+    __nv_bfloat16* dst;
+    if (hh < G) {
+      dst = const_cast<__nv_bfloat16*>(reinterpret_cast<const __nv_bfloat16*>(a.q)) +
+            ((size_t)ii.m * a.Hq + ii.kvh * G + hh) * DH;
+    } else {
+      const int page = a.page_table[(size_t)ii.slot * a.max_pages + pos / 64];
+      const size_t off = (((size_t)page * a.Hkv + ii.kvh) * 64 + pos % 64) * DH;
+      dst = const_cast<__nv_bfloat16*>(reinterpret_cast<const __nv_bfloat16*>(hh == G ? a.k_pool : a.v_pool)) + off;
+    }
+    *reinterpret_cast<uint2*>(dst + i) = make_uint2(pack_bf16(y0[0], y0[1]), pack_bf16(y0[2], y0[3]));
+    *reinterpret_cast<uint2*>(dst + i + HALF) = make_uint2(pack_bf16(y1[0], y1[1]), pack_bf16(y1[2], y1[3]));
+  }
+  // the new k / v are read back by this CTA's TMA (async proxy) and q by its
+  // consumer warps: order the generic stores before both (the hand-off to the
+  // producer is a release / acquire on an mbarrier)
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  __syncwarp();
+}
+
 template <int DH>
 __global__ void __launch_bounds__(kAttnThreads, 1)
     attn_bf16_kernel(AttnArgs a, const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV) {
@@ -376,30 +448,75 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   volatile int* hdr = reinterpret_cast<volatile int*>(empty + kStages);  // [kStages] item of each staged page
   volatile int* merge_flag = hdr + kStages;
 
+  __shared__ uint64_t fq_full[kFQ], fq_empty[kFQ];
+  __shared__ int fq_item[kFQ];
+
   const int G = a.Hq / a.Hkv;
   const int w = warp_id(), lane = lane_id();
   const int n_items = *a.n_items;
+  const bool fin = a.qkv_part != nullptr;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumerWarps);
     }
+    for (int s = 0; s < kFQ; ++s) {
+      mbar_init(&fq_full[s], 1);
+      mbar_init(&fq_empty[s], 1);
+    }
     fence_barrier_init();
   }
   __syncthreads();
 
+  if (w == kFinishWarp) {
+    // ---------------- fused QKV finish warp: takes the items (longest first) and
+    // finishes each one's q / k / v kFQ items ahead of the producer, so the partial
+    // reads and stores stay off the TMA issue path
+    if (!fin) return;
+    for (int n = 0;; ++n) {
+      const int s = n % kFQ;
+      mbar_wait(&fq_empty[s], ((n / kFQ) & 1) ^ 1);
+      int j = 0;
+      if (lane == 0) j = atomicAdd(a.work_ctr, 1);
+      j = __shfl_sync(0xffffffffu, j, 0);
+      const int it = j < n_items ? a.order[j] : -1;
+      if (it >= 0) {
+        const ItemInfo ii = item_info(a, it);
+        qkv_finish_item<DH>(a, ii, G, ii.p1 == (ii.ctx + 63) / 64, lane);
+      }
+      if (lane == 0) {
+        fq_item[s] = it;
+        mbar_arrive(&fq_full[s]);  // release: the item's q / k / v stores before the hand-off
+      }
+      if (it < 0) break;
+    }
+    return;
+  }
+
   if (w == kConsumerWarps) {
-    // ---------------- producer warp
-    if (lane == 0) {
-      tma_prefetch(&tmK);
-      tma_prefetch(&tmV);
+    // ---------------- producer warp (lane 0 issues the TMA loads)
+    {
+      if (lane == 0) {
+        tma_prefetch(&tmK);
+        tma_prefetch(&tmV);
+      }
       const uint64_t pol = policy_evict_first();
       int q = 0;
-      for (;;) {
-        // longest remaining item first, pulled dynamically (balances the tail)
-        const int j = atomicAdd(a.work_ctr, 1);
-        if (j >= n_items) break;
-        const int it = a.order[j];
+      for (int nf = 0; lane == 0; ++nf) {
+        // longest remaining item first, pulled dynamically (balances the tail) -- from
+        // the finish warp's hand-off queue when it runs
+        int it;
+        if (fin) {
+          const int s = nf % kFQ;
+          mbar_wait(&fq_full[s], (nf / kFQ) & 1);
+          it = fq_item[s];
+          mbar_arrive(&fq_empty[s]);
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // the finished k / v, read by TMA below
+        } else {
+          const int j = atomicAdd(a.work_ctr, 1);
+          it = j < n_items ? a.order[j] : -1;
+        }
+        if (it < 0) break;
         const ItemInfo ii = item_info(a, it);
         for (int p = ii.p0; p < ii.p1; ++p, ++q) {
           const int s = q % kStages;
@@ -428,10 +545,12 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         }
       }
       // end of work: a stage with no data and item -1
-      const int s = q % kStages;
-      mbar_wait(&empty[s], ((q / kStages) & 1) ^ 1);
-      hdr[s] = -1;
-      mbar_arrive(&full[s]);
+      if (lane == 0) {
+        const int s = q % kStages;
+        mbar_wait(&empty[s], ((q / kStages) & 1) ^ 1);
+        hdr[s] = -1;
+        mbar_arrive(&full[s]);
+      }
     }
     return;
   }

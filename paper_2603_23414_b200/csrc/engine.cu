@@ -545,6 +545,18 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
   // reduction (QKV class -0.02 ms, attention +0.1 ms per step)
   int S_q = tuning().qkv_finish ? gemm_partial_split(M, Nqkv, d, e->num_sms) : 1;
   if ((size_t)S_q * M * Nqkv > e->qkv_part_floats) S_q = 1;
+  // ... or to the attention kernel, whose producer warps finish q / k / v per item
+  // (pure decode passes: every row's KV append precedes only its own attention)
+  const bool pure_decode = decode && (m_lm < 0 || m_lm >= M);
+  int S_qa = (pure_decode && !e->kv_f32 && tuning().qkv_attn) ? gemm_partial_split(M, Nqkv, d, e->num_sms) : 1;
+  if ((size_t)S_qa * M * Nqkv > e->qkv_part_floats) S_qa = 1;
+  if (S_qa > 1) S_q = 1;
+  a.qkv_part = nullptr;
+  a.qkv_part_stride = (size_t)M * Nqkv;
+  a.qkv_S = S_qa;
+  a.Nqkv = Nqkv;
+  a.rope_cos = e->rope_cos;
+  a.rope_sin = e->rope_sin;
   GemmEpi pq{};
   pq.kind = EPI_PARTIAL;
   pq.w_packed = 1;
@@ -568,7 +580,12 @@ void forward(srl_engine* e, int M, const int* row_tok, const int* row_pos, const
     qe.bias = m.qkv_bias ? w.bqkv : nullptr;
     qe.k_pool = e->kpool[l];
     qe.v_pool = e->vpool[l];
-    if (S_q > 1) {  // split-K partials, then bias + RoPE + KV append in one elementwise pass
+    a.qkv_part = nullptr;
+    if (S_qa > 1) {  // split-K partials, finished inside the attention kernel
+      run_gemm(e, D + SRL_K_GEMM_QKV, e->xn, M, (const __nv_bfloat16*)w.pqkv, Nqkv, d, pq);
+      a.qkv_part = e->qkv_part;
+      a.qkv_bias = qe.bias;
+    } else if (S_q > 1) {  // split-K partials, then bias + RoPE + KV append in one elementwise pass
       run_gemm(e, D + SRL_K_GEMM_QKV, e->xn, M, (const __nv_bfloat16*)w.pqkv, Nqkv, d, pq);
       {
         Prof p(e, D + SRL_K_GEMM_QKV);

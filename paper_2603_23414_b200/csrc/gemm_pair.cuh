@@ -128,8 +128,9 @@ __device__ __forceinline__ void sk_unit_pairs(const GemmParams& p, int u, int* q
 }
 __device__ __forceinline__ float4 ldcg_f4(const float4* a) { return __ldcg(a); }
 
-// Fused MLP work list (SPLIT 3).  Item ids < nA: phase-A unit; else j = id - nA:
-// phase-B k-split j / p2.n_tiles of tile j % p2.n_tiles (m_blocks == 1).
+// Fused MLP work list (SPLIT 3).  Item ids < nA: phase-A unit (ph 0); else
+// j = id - nA: phase-B k-split j / p2.n_tiles of tile j % p2.n_tiles (ph 1,
+// m_blocks == 1).
 constexpr int kFuseMaxPairs = 80, kFuseMaxItems = 8;
 struct FuseArgs {
   CUtensorMap tmW2, tmX2;  // phase B: down weights (packed), act [M][ff]
@@ -244,7 +245,7 @@ __device__ __forceinline__ void gemm_pair_body(const CUtensorMap& tmW, const CUt
       for (int i = 0; i < nseg; ++i) {
         const Seg sg = piece(i);
         const GemmParams& q = gp(sg);
-        const CUtensorMap* tw = (SPLIT == 3 && sg.ph) ? &fz->tmW2 : &tmW;
+        const CUtensorMap* tw = (SPLIT == 3 && sg.ph == 1) ? &fz->tmW2 : &tmW;
         const int u = sg.u;
         const int t128 = (u % q.n_tiles) * 2 + (int)r2;  // this CTA's 128-row tile
         for (int k = sg.k0; k < sg.k1; ++k) {
@@ -276,10 +277,11 @@ __device__ __forceinline__ void gemm_pair_body(const CUtensorMap& tmW, const CUt
         const Seg sg = piece(i);
         const GemmParams& q = gp(sg);
         const CUtensorMap* tx = (SPLIT == 3 && sg.ph) ? &fz->tmX2 : &tmX;
+        const uint32_t xbytes = 2u * (uint32_t)((q.m_blk >> 1) * 128);  // both CTAs' boxes (slots are stage_b apart)
         const int u = sg.u;
         const int ncol = unit_cols(q, u);
         const int mrow = (u / q.n_tiles) * q.m_blk + (int)r2 * (ncol >> 1);
-        if (SPLIT == 3 && sg.ph) {
+        if (SPLIT == 3 && sg.ph == 1) {
           // phase B reads act columns [k0, k1) * 64: wait for the phase-A CTAs that
           // write them (acquire), then order the async-proxy (TMA) reads after it
           const int sp = sg.k0 * fz->S2 / q.kb;
@@ -291,7 +293,7 @@ __device__ __forceinline__ void gemm_pair_body(const CUtensorMap& tmW, const CUt
         }
         for (int k = sg.k0; k < sg.k1; ++k) {
           mbar_wait(&xempty[s], ph);
-          if (is_leader) mbar_arrive_expect_tx(&xfull[s], 2 * stage_b);
+          if (is_leader) mbar_arrive_expect_tx(&xfull[s], xbytes);
           tma_load_2d_pair(sB + s * stage_b, tx, xfull_l + 8u * s, k * 64, mrow, pol_x);
           if (++s == p.xstages) {
             s = 0;

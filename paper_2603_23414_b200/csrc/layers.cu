@@ -26,12 +26,12 @@ void rope_table(float* cos_t, float* sin_t, int max_pos, int dh, double theta, c
 }
 
 // ---------------------------------------------------------------- RMSNorm: one CTA per row
-// x fp32 [M][d] (d % 4 == 0, d <= 4 * 256 * kNormVec), w bf16 [d] -> y bf16 [M][d];
+// x fp32 [M][d] (d % 4 == 0, d <= 4 * kNormThreads * kNormVec), w bf16 [d] -> y bf16 [M][d];
 // when `embed` is set, x is first overwritten with the fp32 embedding row of
 // row_tok[m] (layer 0).  Every load of the row is issued before the reduction
 // (the kernel is latency-bound otherwise).
-constexpr int kNormThreads = 256;
-constexpr int kNormVec = 8;  // float4 per thread
+constexpr int kNormThreads = 512;
+constexpr int kNormVec = 4;  // float4 per thread (d <= 8192)
 __global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(float* __restrict__ x_res, const int* __restrict__ row_tok,
                                                                 const int* __restrict__ row_pos, int M, int d,
                                                                 const __nv_bfloat16* __restrict__ embed,

@@ -65,6 +65,17 @@ struct AttnArgs {
   int* merge_ctr;        // [M * Hkv] split-KV chunk arrivals (zeroed by the plan kernel, reset by the merger)
   int* chunk_pages;      // device int: split-KV chunk size in pages, chosen by the plan kernel
   int l2_prefetch;       // bf16 kernel: pages of L2 prefetch beyond the smem ring (0 = none)
+  // fused QKV finish (bf16 kernel, pure decode passes): when qkv_part is set, the QKV
+  // projection left its qkv_S split-K fp32 partials [qkv_S][M][Nqkv] and the item's
+  // producer warp sums them (split order) + bias, applies RoPE at the row's position,
+  // writes q (bf16, a.q) and -- the item holding the row's last page -- the new
+  // token's k / v into that page before the page is loaded
+  const float* qkv_part;
+  size_t qkv_part_stride;
+  int qkv_S, Nqkv;
+  const __nv_bfloat16* qkv_bias;  // nullable
+  const float* rope_cos;
+  const float* rope_sin;
 };
 void attn_plan(const AttnArgs& a, int split, cudaStream_t st);
 void attn_run(const AttnArgs& a, bool kv_fp32, const void* tmap_k, const void* tmap_v, cudaStream_t st);

@@ -26,7 +26,8 @@ static const srl_tuning kDefaultTuning = {
     /*gemm_split*/ 1, /*gemm_pair*/ -1, /*gemm_h*/ 0, /*gemm_stages*/ 0, /*gemm_xstages*/ 0,
     /*partial_norm*/ 1, /*partial_small_m*/ 0, /*qkv_finish*/ 0, /*fused_sample*/ 0,
     /*attn_min_items*/ 0, /*attn_target_items*/ 0, /*attn_l2_prefetch*/ 0,
-    /*pdl*/ 1, /*graphs*/ 1, /*mixed_prefill*/ 1, /*verbose*/ 0, /*fuse_mlp*/ 1, /*mlp_splits*/ 8};
+    /*pdl*/ 1, /*graphs*/ 1, /*mixed_prefill*/ 1, /*verbose*/ 0, /*fuse_mlp*/ 0, /*mlp_splits*/ 8,
+    /*qkv_attn*/ 1};
 srl_tuning g_tuning = kDefaultTuning;
 
 bool once_per_device(int slot) {

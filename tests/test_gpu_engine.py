@@ -150,6 +150,23 @@ def test_fused_lm_head_sampling_matches():
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
 
 
+def test_qkv_finish_in_attention_small_m():
+    """The QKV split-K partials finished inside the attention kernel (srl_tuning.qkv_attn,
+    default) on the tiny model (dh = 32): at M < 128 the pair GEMM is not used, so the
+    single-CTA kernel's partial mode is switched on (partial_small_m) -- the teacher-forced
+    parity test (schedule, bit-exact ids on identical logits, logits within 1e-2 per row)
+    must pass unchanged, for the fp32-KV (unfused) and bf16-KV (fused) cases."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SRL_TEST_TUNING="partial_small_m=1,qkv_attn=1")
+    out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                          "tests/test_gpu_engine.py::test_model_parity_teacher_forced"],
+                         cwd=root, capture_output=True, text=True, env=env, timeout=900)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
+
+
 def test_two_epochs_and_counters():
     cfg = SchedConfig(Q_g=8, U=4, K=K_INF, pool_prompts=8, cap=64, kv_pages=128, kv_dtype=KV_BF16)
     off, toks, L = tiny_workload(n_prompts=24)

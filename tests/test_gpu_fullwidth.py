@@ -266,7 +266,23 @@ def test_fullwidth_qkv_finish_path():
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, SRL_TEST_TUNING="qkv_finish=1")
+    env = dict(os.environ, SRL_TEST_TUNING="qkv_finish=1,qkv_attn=0")
+    out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                          "tests/test_gpu_fullwidth.py::test_fullwidth_teacher_forced[llama8b-L2-Q256]"],
+                         cwd=root, capture_output=True, text=True, env=env, timeout=1200)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
+
+
+def test_fullwidth_fused_kernel_paths():
+    """The other kernel chain (srl_tuning qkv_attn = 0: bias, RoPE and the KV append in the
+    QKV GEMM's own epilogue after its cluster split-K reduction; fuse_mlp = 1: gate/up and
+    down as one persistent kernel) passes the same full-width parity test.  Subprocess:
+    settings are applied at session start (tests/conftest.py)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SRL_TEST_TUNING="qkv_attn=0,fuse_mlp=1")
     out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
                           "tests/test_gpu_fullwidth.py::test_fullwidth_teacher_forced[llama8b-L2-Q256]"],
                          cwd=root, capture_output=True, text=True, env=env, timeout=1200)
