@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(kF32Threads) attn_f32_kernel(AttnArgs a) {
 }
 
 // ---------------------------------------------------------------- bf16 KV (TMA + mma.sync)
-constexpr int kStages = 4;
+constexpr int kStagesDefault = 4;  // K/V ring depth (srl_tuning.attn_stages: 4 or 6)
 constexpr int kConsumerWarps = 4;
 constexpr int kFinishWarp = kConsumerWarps + 1;          // fused QKV finish (idle otherwise)
 constexpr int kAttnThreads = (kConsumerWarps + 2) * 32;
@@ -432,7 +432,7 @@ __device__ __forceinline__ void qkv_finish_item(const AttnArgs& a, const ItemInf
   __syncwarp();
 }
 
-template <int DH>
+template <int DH, int kStages>
 __global__ void __launch_bounds__(kAttnThreads, 1)
     attn_bf16_kernel(AttnArgs a, const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV) {
   using C = AttnCfg<DH>;
@@ -757,17 +757,26 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   }
 }
 
-template <int DH>
-static void launch_bf16(const AttnArgs& a, const void* tk, const void* tv, cudaStream_t st) {
+template <int DH, int NS>
+static void launch_bf16_ns(const AttnArgs& a, const void* tk, const void* tv, cudaStream_t st, int once_slot) {
   using C = AttnCfg<DH>;
-  const size_t smem = 1024 + kStages * C::kStageBytes + kConsumerWarps * 8 * (DH + 2) * 4 + 2 * kStages * 8 + 64;
-  if (once_per_device(DH == 128 ? kOnceAttn128 : (DH == 64 ? kOnceAttn64 : kOnceAttn32)))  // per-device attribute
-    cudaFuncSetAttribute(attn_bf16_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem = 1024 + NS * C::kStageBytes + kConsumerWarps * 8 * (DH + 2) * 4 + 2 * NS * 8 + 64;
+  if (once_per_device(once_slot))  // per-device attribute
+    cudaFuncSetAttribute(attn_bf16_kernel<DH, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int grid = 148;
   const int occ = (int)((228 * 1024) / (smem + 1024));
   grid *= occ < 1 ? 1 : occ;
-  launch_k(attn_bf16_kernel<DH>, dim3(grid), dim3(kAttnThreads), smem, st, 1, a, *reinterpret_cast<const CUtensorMap*>(tk),
-           *reinterpret_cast<const CUtensorMap*>(tv));
+  launch_k(attn_bf16_kernel<DH, NS>, dim3(grid), dim3(kAttnThreads), smem, st, 1, a,
+           *reinterpret_cast<const CUtensorMap*>(tk), *reinterpret_cast<const CUtensorMap*>(tv));
+}
+
+template <int DH>
+static void launch_bf16(const AttnArgs& a, const void* tk, const void* tv, cudaStream_t st) {
+  const int slot = DH == 128 ? kOnceAttn128 : (DH == 64 ? kOnceAttn64 : kOnceAttn32);
+  if (tuning().attn_stages == 6 && DH == 128)
+    launch_bf16_ns<DH, 6>(a, tk, tv, st, kOnceAttn128s6);
+  else
+    launch_bf16_ns<DH, kStagesDefault>(a, tk, tv, st, slot);
 }
 
 void attn_plan(const AttnArgs& a, int split, cudaStream_t st) {

@@ -333,7 +333,9 @@ __global__ void __launch_bounds__(kCtlThreads, 1) ctl_begin_kernel(Ctl c) {
     if (f) sh_free[pos] = g;
     if (threadIdx.x == 0) sh_nfree = tot;
     __syncthreads();
-    if (threadIdx.x == 0 && !sh_stop) {
+    // only thread 0 may read sh_stop here (it writes it below): a volatile read is not
+    // speculated past the thread test (compute-sanitizer racecheck)
+    if (threadIdx.x == 0 && !*reinterpret_cast<volatile int*>(&sh_stop)) {
       s->page_blocked = 0;
       for (int i = 0; i < sh_nfree; ++i) {
         const int gg = sh_free[i];

@@ -15,6 +15,8 @@ from paper_2603_23414_b200 import _lib  # noqa: E402
 
 lib = _lib.load()
 st = torch.cuda.current_stream().cuda_stream
+if len(sys.argv) > 1:  # srl_tuning overrides, e.g. attn_stages=6
+    _lib.set_tuning(**{k: int(v) for k, v in (kv.split("=") for kv in sys.argv[1].split(","))})
 
 
 def case(name, M, Hq, Hkv, ctx_mean, sigma=0.5, dh=128, it=20, seed=0):
