@@ -253,10 +253,23 @@ def run_gpu(args, rank, world, dist):
     trace = []                       # every decode step: (r_k, sum_ctx, dt_ms, prefill_tokens, n_fin, r_local)
     ATT = ["attention"]
     prof_all_every = max(1, args.prof_every)
+    att_every = max(1, args.attn_every)
+    att_ctx = []                     # sum_ctx of the decode steps whose attention launches were timed
 
     def step(sample_all=False):
-        if sample_all is not None:   # profiled window: every class on sampled steps, attention on the rest
-            eng.set_profile_mask(None if sample_all else ATT)
+        # profiled window: every class on 1 step in prof_every, attention alone on 1 in
+        # attn_every, nothing on the rest (a bracketed class loses its PDL edges)
+        timed_att = False
+        if sample_all is not None:
+            i = st["steps"]
+            if sample_all:
+                eng.set_profile_mask(None)
+                timed_att = True
+            elif i % att_every == 0:
+                eng.set_profile_mask(ATT)
+                timed_att = True
+            else:
+                eng.set_profile_mask([])
         s_, info = eng.decode_step()
         if s_ == DONE:
             st["done"] = True
@@ -265,6 +278,8 @@ def run_gpu(args, rank, world, dist):
             trace.append((info.r_k, info.sum_ctx, info.dt_ms, info.n_prefill_tokens, info.n_finished,
                           info.r_local))
             st["steps"] += 1
+            if timed_att:
+                att_ctx.append(info.sum_ctx)
         if s_ == GROUP_READY:        # rows a15-a17: sorted group out, refreshed policy in
             h = eng.harvest_finished(cap_recs=U_MAX, cap_toks=U_MAX * sched.cap)
             st["useful"] += sum(r["len"] for r in h.records)
@@ -373,7 +388,7 @@ def run_gpu(args, rank, world, dist):
     del eng
     return dict(ms=ms, ran=ran, raw=raw / world, useful=useful / world, stats=stats, prof=prof, launches=launches,
                 clocks=clk.summary(), e2e=e2e, trace=trace, breakdown=prof, n_break=n_sampled, n_dec=n_dec,
-                warmup_rounds=warm, window=(warm, warm + ran))
+                warmup_rounds=warm, window=(warm, warm + ran), att_ctx=att_ctx)
 
 
 # ------------------------------------------------------------------ CPU oracle (the reference arm)
@@ -559,6 +574,8 @@ def main():
     ap.add_argument("--K", type=int, default=K_INF, help="cache bound in policy versions (-1 = inf, 0 = on-policy)")
     ap.add_argument("--U", type=int, default=64, help="update group size")
     ap.add_argument("--barrier", default="trained", choices=["trained", "admitted"], help="cache-aware loading barrier")
+    ap.add_argument("--attn-every", type=int, default=4,
+                    help="time the attention launches on 1 decode step in N (the roofline's measured kernel)")
     ap.add_argument("--tuning", default="", help="srl_tuning overrides for measurement, e.g. fuse_mlp=0,mlp_splits=4")
     ap.add_argument("--G", type=int, default=1, help="responses per prompt (trajectories per epoch unchanged)")
     ap.add_argument("--share-prefix", action="store_true", help="N4: G samples share their prompt-prefix KV pages")
@@ -606,9 +623,11 @@ def main():
     n_dec = len(stats)
     attn_ms, attn_n = r["prof"]["attention"]
     # dominant kernel: paged attention, bracketed by CUDA events on the engine stream in
-    # every timed decode step (a class's events sit outside its launches, inside the graph)
+    # the sampled decode steps of the timed window (a class's events sit outside its
+    # launches, inside the graph); units = those steps' context tokens per layer
     per_unit = 2 * m.Hkv * m.dh * 2                             # K+V bytes per context token per layer
-    units = sum_ctx                                              # context tokens read per layer, all timed steps
+    att_ctx = r.get("att_ctx") or [x[1] for x in stats]
+    units = sum(att_ctx)                                         # context tokens read per layer, timed launches
     achieved = per_unit * units * m.L / (attn_ms * 1e-3) / 1e9 if attn_ms > 0 else None
     traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")
@@ -622,7 +641,7 @@ def main():
                             "ncu --set full (traffic_capture: its own algorithmic bytes beside it)",
             "traffic_capture": traffic_src,
             "per_unit_bytes": per_unit, "unit_def": "one context token of one layer (K+V, bf16)",
-            "units_per_launch": units / max(1, n_dec), "launches": attn_n,
+            "units_per_launch": units / max(1, len(att_ctx)), "launches": attn_n,
             "peak_source": peak_src + " (MEASURED_PEAKS.json copy bandwidth; a read-only stream may exceed it)"}
     # decode roofline fraction of the whole step
     t_roof = 0.0
@@ -657,8 +676,8 @@ def main():
         return
     nb = max(1, r["n_break"])
     bd = {k: v[0] / nb for k, v in r["breakdown"].items()}
-    if n_dec:
-        bd["attention"] = attn_ms / n_dec                        # attention is bracketed in every step
+    if att_ctx:
+        bd["attention"] = attn_ms / len(att_ctx)                 # per timed step (1 in attn_every + the sampled ones)
     win = r.get("window")
     line = {
         "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": world, "steps": steps,
@@ -691,7 +710,8 @@ def main():
         "kernel_ms_per_decode_step": bd,
         "kernel_breakdown_note": (f"inside the timed window: every class bracketed by CUDA events on 1 decode step in "
                                   f"{args.prof_every} ({r['n_break']} steps; those steps lose their PDL edges), "
-                                  f"attention on every step; prefill passes counted under 'prefill'"),
+                                  f"attention alone on 1 in {args.attn_every} more ({len(r.get('att_ctx') or [])} "
+                                  f"attention-timed steps in all); prefill passes counted under 'prefill'"),
         "paper_context": {"note": "context, not the target: P:336-339, H100/MI300X mix (P:239), GPU type/count, engine "
                                   "capacity and length trace unstated",
                           "bubble": {"sync_baseline": 0.74, "sortedrl_on_policy": 0.0581, "sortedrl_partial": 0.0337},
