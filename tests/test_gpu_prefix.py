@@ -126,3 +126,20 @@ def test_prefix_sharing_teacher_forced_logits(kv, over):
         assert t_same == teacher[e["tid"]][e["n"]]
     assert len(runner.log) > 100
     print(f"worst logits rel-L2 {worst:.2e} over {len(runner.log)} rows")
+
+
+def test_prefix_sharing_replicas_bit_exact():
+    """R = 2 lockstep replicas (in-process transport): every rank keeps every replica's
+    prefix entries (refcounts, version tags) for the page accounting and only its own
+    entries' page ids; schedules bit-exact against the R = 2 oracle on every rank."""
+    from test_gpu_replicas import _run_replicas
+    cfg = SchedConfig(R=2, Q_g=4, U=4, K=1, pool_prompts=4, G=4, cap=96, kv_pages=12, kv_dtype=KV_BF16,
+                      share_prefix=1)
+    off, toks, L = _workload(8, cfg.G, cap=cfg.cap, median=30)
+    outs = _run_replicas(cfg, off, toks, L, max_prompt=MAXP)
+    c, og = _oracle(cfg, off, toks, L)
+    for o in outs:
+        _compare_schedule(o, c, og)
+    import dataclasses
+    c0, _ = _oracle(dataclasses.replace(cfg, share_prefix=0), off, toks, L)
+    assert c0.events != c.events
