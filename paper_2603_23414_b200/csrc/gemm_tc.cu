@@ -38,6 +38,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -650,9 +651,12 @@ struct FuseSched {
   uint8_t n_items[kFuseMaxPairs];
   uint8_t items[kFuseMaxPairs][kFuseMaxItems];
 };
-static const FuseSched& fuse_schedule(int P, int nA, int nt2, int S2, int kbA, int kbB) {
+static FuseSched fuse_schedule(int P, int nA, int nt2, int S2, int kbA, int kbB) {
+  // engines of one process may launch from several host threads (SRL_COMM_LOCAL)
+  static std::mutex mu;
   static std::vector<std::pair<std::vector<int>, FuseSched>> cache;
   const std::vector<int> key{P, nA, nt2, S2, kbA, kbB};
+  std::lock_guard<std::mutex> lock(mu);
   for (const auto& c : cache)
     if (c.first == key) return c.second;
   FuseSched f;
@@ -716,7 +720,7 @@ int gemm_mlp_fused(const __nv_bfloat16* X, int M, const void* Wgu, int ff, int d
   p.epi.ldo = ff;
   p.wp = reinterpret_cast<const uint8_t*>(Wgu);
   p.dbg = (g_dbg && g_dbg_count++ == g_dbg_target) ? g_dbg : nullptr;
-  static FuseArgs f;  // host staging of the grid-constant argument (1.6 KB)
+  FuseArgs f;  // host staging of the grid-constant argument (copied at launch; per call: thread-safe)
   memset(&f, 0, sizeof(f));
   GemmParams& q = f.p2;
   q = p;
@@ -733,7 +737,7 @@ int gemm_mlp_fused(const __nv_bfloat16* X, int M, const void* Wgu, int ff, int d
   q.epi.ldo = d;
   q.wp = reinterpret_cast<const uint8_t*>(Wd);
   q.dbg = nullptr;
-  const FuseSched& fs = fuse_schedule(pairs, p.units, q.n_tiles, S2, p.kb, q.kb);
+  const FuseSched fs = fuse_schedule(pairs, p.units, q.n_tiles, S2, p.kb, q.kb);
   if (!fs.ok) return 1;
   memcpy(f.n_items, fs.n_items, sizeof(f.n_items));
   memcpy(f.items, fs.items, sizeof(f.items));
