@@ -210,3 +210,31 @@ def test_storage_rounding_points_each_act_and_positions_subset():
         assert r.max() < 2e-2, (p, r.max())
     r_all = rel(mdl.full_forward(toks, storage_bf16=True))
     assert 1e-4 < r_all.mean() < 2e-2
+
+
+def test_runner_chunked_prefill_equals_whole_prefill():
+    """oracle.model.ModelRunner under the N1 prefill budget (reading R30): with no policy
+    update in between, a prompt prefilled in budget-sized chunks over several steps gives
+    the same logits, token for token, as the unlimited (whole-prompt) prefill -- the
+    incremental decode's KV is position-wise, so the chunking cannot change it -- and the
+    schedule differs only in when decoding starts (first tokens later)."""
+    import numpy as np
+    from oracle.model import ModelRunner, load_weights
+    from oracle.sched import Controller
+    from workload.configs import TINY, SchedConfig
+    plen, L = [40, 25, 33], [5, 4, 6]
+    toks = [list(np.random.default_rng(i).integers(1, TINY.V, size=n)) for i, n in enumerate(plen)]
+    W = load_weights(TINY)
+    logs = []
+    for C in (0, 7):
+        cfg = SchedConfig(Q_g=3, U=3, pool_prompts=3, cap=8, prefill_budget=C)
+        runner = ModelRunner(TINY, lambda v: W, lambda t: toks[t.tid], cfg.sample_seed, record_logits=True)
+        c = Controller(cfg, runner)
+        c.submit_prompts([1, 2, 3], plen, L)
+        c.run()
+        logs.append(({(e["tid"], e["n"]): e["logits"] for e in runner.log}, c.trace))
+    (a, tr0), (b, tr7) = logs
+    assert a.keys() == b.keys() and len(a) == sum(L)
+    for key in a:
+        assert np.array_equal(a[key], b[key]), key
+    assert len(tr7) > len(tr0)                      # decoding starts later under the budget

@@ -17,6 +17,7 @@ from workload.configs import LLAMA8B  # noqa: E402
 from workload.weights import fill_engine_weights  # noqa: E402
 
 P = int(sys.argv[1]) if len(sys.argv) > 1 else 1500
+MIXED = len(sys.argv) > 2 and sys.argv[2] == "mixed"   # profile a step that admits prompts (mixed pass)
 sched = bench.cfg2_sched(1)
 off, toks, L = bench.workload_inputs(1, epochs=2)
 eng = RolloutEngine(LLAMA8B, sched, max_traj=2048, max_prompt=256, prefill_chunk=4096)
@@ -32,16 +33,22 @@ while k < P:
         eng.harvest_finished(cap_recs=2048)
         v += 1
         eng.load_policy_weights(v)
-while True:   # a step without admissions (pure decode)
+while True:   # a step without admissions (pure decode), or with them (mixed)
+    # advance, unprofiled, to a step of the wanted kind: a decode step admits prompts
+    # iff the previous step finished trajectories (slots free up at its END)
+    st, info = eng.decode_step()
+    if st == GROUP_READY:
+        eng.harvest_finished(cap_recs=2048)
+        v += 1
+        eng.load_policy_weights(v)
+        continue
+    if (info.n_finished > 0) != MIXED:
+        continue
     torch.cuda.synchronize()
     torch.cuda.cudart().cudaProfilerStart()
     st, info = eng.decode_step()
     torch.cuda.synchronize()
     torch.cuda.cudart().cudaProfilerStop()
-    if st == GROUP_READY:
-        eng.harvest_finished(cap_recs=2048)
-        v += 1
-        eng.load_policy_weights(v)
     print("profiled step", info.k, "r_k", info.r_k, "sum_ctx", info.sum_ctx, "prefill", info.n_prefill_tokens,
           "dt_ms", round(info.dt_ms, 3), flush=True)
     break
