@@ -15,19 +15,24 @@ KEYS = ["Kernel Name", "launch__grid_size", "launch__block_size", "launch__regis
 
 
 def summary(path):
+    """one dict per captured kernel launch in the report"""
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
-    h, u, v = rows[0], rows[1], rows[2]
-    d = {}
-    for k in KEYS:
-        if k in h:
-            i = h.index(k)
-            d[k] = (v[i], u[i])
-    return d
+    h, u = rows[0], rows[1]
+    res = []
+    for v in rows[2:]:
+        d = {}
+        for k in KEYS:
+            if k in h:
+                i = h.index(k)
+                d[k] = (v[i], u[i])
+        res.append(d)
+    return res
 
 
 if __name__ == "__main__":
     for p in sys.argv[1:]:
-        print(f"== {p}")
-        for k, (val, unit) in summary(p).items():
-            print(f"  {k:75s} {val} {unit}")
+        for j, d in enumerate(summary(p)):
+            print(f"== {p} [launch {j}]")
+            for k, (val, unit) in d.items():
+                print(f"  {k:75s} {val} {unit}")
