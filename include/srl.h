@@ -375,6 +375,9 @@ typedef struct srl_tuning {
   int32_t qkv_attn;        /* 1 (default): pure decode passes leave QKV split-K partials to the attention
                               kernel, whose finish warp completes q / k / v per item (bias, RoPE, KV
                               append) ahead of its TMA producer */
+  int32_t pair_h2;         /* 1 (default): whole-unit pair GEMMs take 512-row units (two MMAs per
+                              k-step share the activation slice) when that at least halves the
+                              waves of 256-row units (decode gate/up); 0: 256-row units */
 } srl_tuning;
 void srl_default_tuning(srl_tuning* t);
 int32_t srl_get_tuning(srl_tuning* t);

@@ -75,7 +75,8 @@ class Tuning(C.Structure):
     _fields_ = [(n, _I32) for n in ("gemm_split", "gemm_pair", "gemm_h", "gemm_stages", "gemm_xstages",
                                     "partial_norm", "partial_small_m", "qkv_finish", "fused_sample",
                                     "attn_min_items", "attn_target_items", "attn_l2_prefetch", "pdl", "graphs",
-                                    "mixed_prefill", "verbose", "fuse_mlp", "mlp_splits", "attn_stages", "qkv_attn")]
+                                    "mixed_prefill", "verbose", "fuse_mlp", "mlp_splits", "attn_stages", "qkv_attn",
+                                    "pair_h2")]
 
 
 _MP, _SP, _AP, _CP = C.POINTER(ModelCfg), C.POINTER(SchedCfg), C.POINTER(Arena), C.POINTER(Comm)

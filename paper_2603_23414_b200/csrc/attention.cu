@@ -518,11 +518,16 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         }
         if (it < 0) break;
         const ItemInfo ii = item_info(a, it);
+        const int* pt = a.page_table + (size_t)ii.slot * a.max_pages;
+        int page_next = ii.p0 < ii.p1 ? pt[ii.p0] : 0;
         for (int p = ii.p0; p < ii.p1; ++p, ++q) {
           const int s = q % kStages;
           const uint32_t ph = (q / kStages) & 1;
+          // the next page id is loaded one page ahead: its L2 round trip overlaps the
+          // wait for a free stage instead of delaying the TMA issue
+          const int page = page_next;
+          if (p + 1 < ii.p1) page_next = pt[p + 1];
           mbar_wait(&empty[s], ph ^ 1);
-          const int page = a.page_table[(size_t)ii.slot * a.max_pages + p];
           const int row = (page * a.Hkv + ii.kvh) * 64;
           uint8_t* kb = stages + s * C::kStageBytes;
           uint8_t* vb = kb + C::kBlockBytes;

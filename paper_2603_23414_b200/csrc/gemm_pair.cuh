@@ -158,8 +158,14 @@ __device__ __forceinline__ void gemm_pair_body(const CUtensorMap& tmW, const CUt
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int stage_b = (p.m_blk >> 1) * 128;  // this CTA's half of the activation slice
+  // H = 2 (whole units only): a pair unit is 512 weight rows, two M = 256 MMAs per
+  // k-step sharing the activation slice -- per SM 32 KB of weights + 16 KB of
+  // activations per k-block for twice the MACs (H = 1: 16 + 16); TMEM holds both
+  // accumulators (512 columns, no double buffering).  Measured MMA-paced: 0.71 us per
+  // k-block (1024 clk) vs 0.37-0.40 for H = 1; it pays where it halves the waves
+  const int H = SPLIT == 0 ? p.H : 1;
   uint8_t* sA = smem;
-  uint8_t* sB = smem + p.stages * kStageA;
+  uint8_t* sB = smem + p.stages * kStageA * H;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + p.xstages * stage_b);
   uint64_t* empty = full + p.stages;
   uint64_t* xfull = empty + p.stages;
@@ -247,13 +253,15 @@ __device__ __forceinline__ void gemm_pair_body(const CUtensorMap& tmW, const CUt
         const GemmParams& q = gp(sg);
         const CUtensorMap* tw = (SPLIT == 3 && sg.ph == 1) ? &fz->tmW2 : &tmW;
         const int u = sg.u;
-        const int t128 = (u % q.n_tiles) * 2 + (int)r2;  // this CTA's 128-row tile
         for (int k = sg.k0; k < sg.k1; ++k) {
           mbar_wait(&empty[s], ph);
-          if (is_leader) mbar_arrive_expect_tx(&full[s], 2 * kStageA);  // both CTAs' halves
-          const int c1 = q.wp ? (t128 * q.kb + k) * 128 : t128 * 128;
-          const int c0 = q.wp ? 0 : k * 64;
-          tma_load_2d_pair(sA + s * kStageA, tw, full_l + 8u * s, c0, c1, pol_w);
+          if (is_leader) mbar_arrive_expect_tx(&full[s], 2 * kStageA * H);  // both CTAs' halves
+          for (int h = 0; h < H; ++h) {
+            const int t128 = ((u % q.n_tiles) * H + h) * 2 + (int)r2;  // this CTA's 128-row tile of MMA h
+            const int c1 = q.wp ? (t128 * q.kb + k) * 128 : t128 * 128;
+            const int c0 = q.wp ? 0 : k * 64;
+            tma_load_2d_pair(sA + (s * H + h) * kStageA, tw, full_l + 8u * s, c0, c1, pol_w);
+          }
           if (first) {
             DBG(2);
             first = false;
@@ -305,7 +313,7 @@ __device__ __forceinline__ void gemm_pair_body(const CUtensorMap& tmW, const CUt
   } else if (w == 1) {
     if (lane == 0 && is_leader) {
       const uint64_t da0 = umma_desc_sw128(smem_u32(sA)), db0 = umma_desc_sw128(smem_u32(sB));
-      const uint32_t sa16 = (uint32_t)kStageA >> 4, sb16 = (uint32_t)stage_b >> 4;
+      const uint32_t sa16 = (uint32_t)(kStageA * H) >> 4, sb16 = (uint32_t)stage_b >> 4;
       int s = 0, sx = 0;
       uint32_t ph = 0, phx = 0;
       bool first = true;
@@ -316,17 +324,21 @@ __device__ __forceinline__ void gemm_pair_body(const CUtensorMap& tmW, const CUt
         const int a = i % p.acc_stages;
         mbar_wait(&tempty[a], ((i / p.acc_stages) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t tacc = tbase + (uint32_t)(a * p.m_blk);
+        const uint32_t tacc = tbase + (uint32_t)(a * H * p.m_blk);
         uint32_t acc = 0;
         for (int k = sg.k0; k < sg.k1; ++k) {
           mbar_wait(&full[s], ph);
           mbar_wait(&xfull[sx], phx);
           tc_fence_after();
-          const uint64_t da = da0 + (uint64_t)(s * sa16), db = db0 + (uint64_t)(sx * sb16);
-          tc_mma_bf16_pair(tacc, da, db, idesc, acc);
-          tc_mma_bf16_pair(tacc, da + 2, db + 2, idesc, 1u);
-          tc_mma_bf16_pair(tacc, da + 4, db + 4, idesc, 1u);
-          tc_mma_bf16_pair(tacc, da + 6, db + 6, idesc, 1u);
+          const uint64_t db = db0 + (uint64_t)(sx * sb16);
+          for (int h = 0; h < H; ++h) {
+            const uint64_t da = da0 + (uint64_t)(s * sa16 + h * ((uint32_t)kStageA >> 4));
+            const uint32_t th = tacc + (uint32_t)(h * p.m_blk);
+            tc_mma_bf16_pair(th, da, db, idesc, acc);
+            tc_mma_bf16_pair(th, da + 2, db + 2, idesc, 1u);
+            tc_mma_bf16_pair(th, da + 4, db + 4, idesc, 1u);
+            tc_mma_bf16_pair(th, da + 6, db + 6, idesc, 1u);
+          }
           acc = 1;
           tc_commit_pair(&empty[s], pair_mask);  // frees both CTAs' slots once the MMAs retire
           tc_commit_pair(&xempty[sx], pair_mask);
@@ -386,11 +398,14 @@ __device__ __forceinline__ void gemm_pair_body(const CUtensorMap& tmW, const CUt
           }
         }
       } else if (whole) {
-        if (unit_n0 < p.N) {
+        for (int h = 0; h < H; ++h) {  // MMA h's 256 rows (H = 2: unit rows 512 t + 256 h)
+          const int n0 = (u % q.n_tiles) * 256 * H + h * 256 + (int)r2 * 128;
+          if (n0 >= p.N) break;
+          const uint32_t tlh = tbase + ((uint32_t)(qw * 32) << 16) + (uint32_t)((a * H + h) * p.m_blk);
           for (int cc = eg * 16; cc < ncol; cc += 32) {
             float v[16];
-            tmem_ld16(tl + cc, v);
-            apply_epilogue(p, unit_n0, n, m_base + cc, v, xg, 1 + eg, rtab + cc);
+            tmem_ld16(tlh + cc, v);
+            apply_epilogue(p, n0, n, m_base + cc, v, xg, 1 + eg, rtab + cc);
           }
         }
       } else {

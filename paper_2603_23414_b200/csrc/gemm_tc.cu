@@ -587,14 +587,28 @@ static int gemm_pair_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W
     p.sk_ws = reinterpret_cast<float*>(epi.ws);
     p.sk_cnt = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(epi.ws) + (size_t)num_sms * 2 * kSkSlotBytes);
   }
+  // H = 2 (whole units): 512-row pair units, two MMAs per k-step sharing the activation
+  // slice (gemm_pair.cuh) -- when that at least halves the waves of 256-row units (a
+  // 512-row unit takes ~1.8x as long, incl. its un-overlapped epilogue): gate/up's 112
+  // units = 2 waves on 74 pairs -> 56 = 1 wave (measured r02: gate/up 2.41 -> 2.26 ms per
+  // step); not the LM head (501 units = 7 waves -> 251 = 4: measured 0.228 -> 0.238 ms)
+  if (tuning().pair_h2 && !sk && !bsplit && S == 1 && epi.kind != EPI_SAMPLE) {
+    const int units2 = (N + 511) / 512 * p.m_blocks;
+    const int w1 = (p.units + pairs - 1) / pairs, w2 = (units2 + pairs - 1) / pairs;
+    if (w2 * 2 <= w1) {
+      p.H = 2;
+      p.n_tiles = (N + 511) / 512;
+      p.units = units2;
+    }
+  }
   const int stage_b = (p.m_blk >> 1) * 128;
   const int budget = 200 * 1024;
   int xstages = stage_b <= 4096 ? 8 : (stage_b <= 8192 ? 6 : 4);
-  int stages = (budget - xstages * stage_b) / kStageA;
+  int stages = (budget - xstages * stage_b) / (kStageA * p.H);
   if (stages > 12) stages = 12;
   p.stages = stages;
   p.xstages = xstages;
-  const size_t rings = (size_t)stages * kStageA + (size_t)xstages * stage_b;
+  const size_t rings = (size_t)stages * kStageA * p.H + (size_t)xstages * stage_b;
   if (S > 1 && !part) {
     const int cpr = ((p.m_blk >> 4) + S - 1) / S;
     if ((size_t)S * cpr * 8192 > rings) return 1;
@@ -604,9 +618,9 @@ static int gemm_pair_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W
     return 0;
   }
   if (epi.kind == EPI_PARTIAL && !(S > 1 && !sk && !bsplit)) return -1;  // caller must ask gemm_partial_split
-  p.acc_stages = (S == 1 && 2 * p.m_blk <= 512) ? 2 : 1;
+  p.acc_stages = (S == 1 && 2 * p.H * p.m_blk <= 512) ? 2 : 1;
   int tc = 32;
-  while (tc < p.m_blk * p.acc_stages) tc <<= 1;
+  while (tc < p.H * p.m_blk * p.acc_stages) tc <<= 1;
   p.tmem_cols = tc;
   CUtensorMap tmW, tmX;
   if (epi.w_packed) {
@@ -625,8 +639,8 @@ static int gemm_pair_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W
     cudaFuncSetAttribute(gemm_pair_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   }
   if (tuning().verbose)
-    fprintf(stderr, "gemm(pair) M=%d N=%d K=%d units=%d S=%d sk=%d stages=%d/%d smem=%zu\n", M, N, K, p.units, S,
-            (int)sk, stages, xstages, smem);
+    fprintf(stderr, "gemm(pair) M=%d N=%d K=%d H=%d units=%d S=%d sk=%d stages=%d/%d smem=%zu\n", M, N, K, p.H,
+            p.units, S, (int)sk, stages, xstages, smem);
   int rc;
   if (sk) {
     rc = launch_cluster(gemm_pair_kernel<2>, 2 * p.sk_pairs, 2, smem, stream, tmW, tmX, p);

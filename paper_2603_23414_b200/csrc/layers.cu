@@ -7,6 +7,7 @@
 #include "common.cuh"
 #include "launch.hpp"
 #include "layers.hpp"
+#include "norm_row.cuh"
 
 namespace srl {
 
@@ -26,93 +27,18 @@ void rope_table(float* cos_t, float* sin_t, int max_pos, int dh, double theta, c
 }
 
 // ---------------------------------------------------------------- RMSNorm: one CTA per row
-// x fp32 [M][d] (d % 4 == 0, d <= 4 * kNormThreads * kNormVec), w bf16 [d] -> y bf16 [M][d];
-// when `embed` is set, x is first overwritten with the fp32 embedding row of
-// row_tok[m] (layer 0).  Every load of the row is issued before the reduction
+// x fp32 [M][d] (d % 4 == 0, d <= 8192), w bf16 [d] -> y bf16 [M][d]; when `embed` is
+// set, x is first overwritten with the fp32 embedding row of row_tok[m] (layer 0).
+// The row arithmetic (norm_row.cuh) is the one the pair GEMM's norm prologue runs, so
+// both give the same bits.  Every load of the row is issued before the reduction
 // (the kernel is latency-bound otherwise).
-constexpr int kNormThreads = 512;
-constexpr int kNormVec = 4;  // float4 per thread (d <= 8192)
-__global__ void __launch_bounds__(kNormThreads) rmsnorm_kernel(float* __restrict__ x_res, const int* __restrict__ row_tok,
-                                                                const int* __restrict__ row_pos, int M, int d,
-                                                                const __nv_bfloat16* __restrict__ embed,
-                                                                const __nv_bfloat16* __restrict__ w, float eps,
-                                                                __nv_bfloat16* __restrict__ y, const float* __restrict__ part,
-                                                                int nsplit, size_t part_stride) {
-  __shared__ float red[kNormThreads / 32];
+constexpr int kNormThreads = kNormVT;  // one virtual thread per real thread
+template <int VEC, int MAXS>
+__global__ void __launch_bounds__(kNormThreads, 2) rmsnorm_kernel(NormRowArgs a) {
+  __shared__ float red[kNormVT / 32];
   pdl_trigger();
   pdl_wait();
-  const int m = blockIdx.x;
-  float* x = x_res + (size_t)m * d;
-  __nv_bfloat16* out = y + (size_t)m * d;
-  const bool active = row_pos[m] >= 0;
-  const int nv = d >> 2;
-  float4 v[kNormVec];
-  uint2 wr[kNormVec];
-  const __nv_bfloat16* e = embed ? embed + (size_t)(active ? row_tok[m] : 0) * d : nullptr;
-#pragma unroll
-  for (int k = 0; k < kNormVec; ++k) {
-    const int i = threadIdx.x + k * kNormThreads;
-    if (i < nv) {
-      if (e) {
-        const uint2 raw = __ldg(reinterpret_cast<const uint2*>(e) + i);
-        v[k] = make_float4(bf16lo(raw.x), bf16hi(raw.x), bf16lo(raw.y), bf16hi(raw.y));
-      } else {
-        v[k] = reinterpret_cast<const float4*>(x)[i];
-        if (part) {
-          // the previous split-K GEMM's partials: summed in split (= k) order, then
-          // added to the residual -- the same fp32 operations its own epilogue did
-          // (up to kNormMaxSplits splits, all loads in flight before the adds)
-          float4 q[kNormMaxSplits];
-#pragma unroll
-          for (int sp = 0; sp < kNormMaxSplits; ++sp)
-            q[sp] = sp < nsplit ? __ldcg(reinterpret_cast<const float4*>(part + sp * part_stride + (size_t)m * d) + i)
-                                : make_float4(0.f, 0.f, 0.f, 0.f);
-          float4 acc = q[0];
-#pragma unroll
-          for (int sp = 1; sp < kNormMaxSplits; ++sp)
-            if (sp < nsplit) {
-              acc.x += q[sp].x;
-              acc.y += q[sp].y;
-              acc.z += q[sp].z;
-              acc.w += q[sp].w;
-            }
-          v[k].x += acc.x;
-          v[k].y += acc.y;
-          v[k].z += acc.z;
-          v[k].w += acc.w;
-        }
-      }
-      wr[k] = __ldg(reinterpret_cast<const uint2*>(w) + i);
-    }
-  }
-  float ss = 0.f;
-#pragma unroll
-  for (int k = 0; k < kNormVec; ++k) {
-    const int i = threadIdx.x + k * kNormThreads;
-    if (i < nv) {
-      if (!active) v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (e || part) reinterpret_cast<float4*>(x)[i] = v[k];
-      ss += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
-  __syncthreads();
-  float tot = 0.f;
-#pragma unroll
-  for (int i = 0; i < kNormThreads / 32; ++i) tot += red[i];
-  const float inv = active ? rsqrtf(tot / (float)d + eps) : 0.f;
-#pragma unroll
-  for (int k = 0; k < kNormVec; ++k) {
-    const int i = threadIdx.x + k * kNormThreads;
-    if (i < nv) {
-      uint2 o;
-      o.x = pack_bf16(v[k].x * inv * bf16lo(wr[k].x), v[k].y * inv * bf16hi(wr[k].x));
-      o.y = pack_bf16(v[k].z * inv * bf16lo(wr[k].y), v[k].w * inv * bf16hi(wr[k].y));
-      reinterpret_cast<uint2*>(out)[i] = o;
-    }
-  }
+  norm_row<1, VEC, MAXS>(a, blockIdx.x, threadIdx.x, red, [] { __syncthreads(); });
 }
 
 // ---------------------------------------------------------------- QKV finish
@@ -200,9 +126,16 @@ void qkv_finish(const QkvFinishArgs& a, int M, cudaStream_t st) {
 void rmsnorm(float* x_res, const int* row_tok, const int* row_pos, int M, int d, const __nv_bfloat16* embed,
              const __nv_bfloat16* w, float eps, __nv_bfloat16* y, cudaStream_t st, const float* part, int nsplit,
              size_t part_stride) {
-  if (M > 0)
-    launch_k(rmsnorm_kernel, dim3(M), dim3(kNormThreads), 0, st, 1, x_res, row_tok, row_pos, M, d, embed, w, eps, y,
-             part, nsplit, part_stride);
+  rmsnorm(norm_args(x_res, row_tok, row_pos, d, embed, w, eps, y, part, nsplit, part_stride), M, st);
+}
+void rmsnorm(const NormRowArgs& a, int M, cudaStream_t st) {
+  if (M <= 0) return;
+  if (a.d <= 4 * 2 * kNormVT && a.nsplit <= 4)  // the 8B decode shapes
+    launch_k(rmsnorm_kernel<2, 4>, dim3(M), dim3(kNormThreads), 0, st, 1, a);
+  else if (a.d <= 4 * 3 * kNormVT && a.nsplit <= 4)  // the 32B width (d = 5120)
+    launch_k(rmsnorm_kernel<3, 4>, dim3(M), dim3(kNormThreads), 0, st, 1, a);
+  else
+    launch_k(rmsnorm_kernel<kNormVec, kNormMaxSplits>, dim3(M), dim3(kNormThreads), 0, st, 1, a);
 }
 
 }  // namespace srl

@@ -15,6 +15,8 @@ constexpr int kNormMaxSplits = 8;  // split-K partials one RMSNorm can sum
 void rmsnorm(float* x_res, const int* row_tok, const int* row_pos, int M, int d, const __nv_bfloat16* embed,
              const __nv_bfloat16* w, float eps, __nv_bfloat16* y, cudaStream_t st, const float* part = nullptr,
              int nsplit = 0, size_t part_stride = 0);
+struct NormRowArgs;
+void rmsnorm(const NormRowArgs& a, int M, cudaStream_t st);
 
 // QKV projection finish from split-K partials (see layers.cu)
 struct QkvFinishArgs {

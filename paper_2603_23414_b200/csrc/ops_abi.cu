@@ -27,7 +27,7 @@ static const srl_tuning kDefaultTuning = {
     /*partial_norm*/ 1, /*partial_small_m*/ 0, /*qkv_finish*/ 0, /*fused_sample*/ 0,
     /*attn_min_items*/ 0, /*attn_target_items*/ 0, /*attn_l2_prefetch*/ 0,
     /*pdl*/ 1, /*graphs*/ 1, /*mixed_prefill*/ 1, /*verbose*/ 0, /*fuse_mlp*/ 0, /*mlp_splits*/ 8,
-    /*attn_stages*/ 4, /*qkv_attn*/ 1};
+    /*attn_stages*/ 4, /*qkv_attn*/ 1, /*pair_h2*/ 1};
 srl_tuning g_tuning = kDefaultTuning;
 
 bool once_per_device(int slot) {
@@ -62,7 +62,7 @@ extern "C" int32_t srl_set_tuning(const srl_tuning* t) {
   if (t->gemm_split < 0 || t->gemm_split > 3 || t->gemm_pair < -1 || t->gemm_pair > 1 || t->gemm_h < 0 ||
       t->gemm_h > 2 || t->gemm_stages < 0 || t->gemm_xstages < 0 || t->attn_min_items < 0 ||
       t->attn_target_items < 0 || t->attn_l2_prefetch < 0 || t->attn_l2_prefetch > 16 || t->mlp_splits < 1 ||
-      t->mlp_splits > 8 || (t->attn_stages != 4 && t->attn_stages != 6)) {
+      t->mlp_splits > 8 || (t->attn_stages != 4 && t->attn_stages != 6) || t->pair_h2 < 0 || t->pair_h2 > 1) {
     set_error("srl_set_tuning: %s", "field out of range", 0);
     return -1;
   }

@@ -121,6 +121,35 @@ def test_gemm_silu_mul_epilogue(lib, M, N, K, packed):
     assert ((out.double() - ref).abs() <= 2.0 ** -8 * ref.abs() + 1e-4).all()
 
 
+@pytest.mark.parametrize("M,N,K,epi", [(256, 14336, 4096, 2), (256, 128256, 512, 0), (4096, 4096, 256, 0),
+                                       (200, 40064, 128, 1), (144, 14336, 256, 2), (256, 57344, 256, 0)])
+def test_gemm_pair_h2_bit_identical(lib, M, N, K, epi):
+    """srl_tuning.pair_h2: 512-row pair units (two M = 256 MMAs per k-step sharing the
+    activation slice; gate/up 112 -> 56 units, LM head 501 -> 251 with a half-empty last
+    unit) give the same bits as 256-row units -- each output element is the same k-ordered
+    MMA chain -- and stay within the fp32-accumulation bound of the fp64 product."""
+    from paper_2603_23414_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(M + N + K + epi)
+    X = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    rows = 2 * N if epi == 2 else N
+    W = (torch.randn(rows, K, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    dt = torch.bfloat16 if epi == 2 else torch.float32
+    base = torch.randn(M, N, device="cuda", generator=g)
+    outs = []
+    for h2 in (1, 0):
+        old = _lib.set_tuning(pair_h2=h2)
+        try:
+            out = base.clone().to(dt)
+            assert _gemm(lib, X, W, N, epi, out, True) == 0
+        finally:
+            _lib.set_tuning(**old)
+        outs.append(out)
+    assert torch.equal(outs[0], outs[1])
+    if epi == 0:
+        ref = X.double() @ W.double().t()
+        assert ((outs[0].double() - ref).abs() <= _bound(X, W) + 1e-6 * ref.abs()).all()
+
+
 # ------------------------------------------------------------------ fused MLP (gate/up + down, one kernel)
 @pytest.mark.parametrize("M,d,ff,splits", [(256, 4096, 14336, 8), (256, 4096, 14336, 4), (128, 4096, 14336, 8),
                                            (208, 4096, 14336, 8), (144, 512, 2048, 2), (256, 1024, 3072, 3)])
