@@ -91,9 +91,14 @@ static __device__ __forceinline__ float gumbel_from_bits(uint32_t x) {
 
 // pruning bound (see sample_kernel): generous against the <= 1e-5 deviation
 constexpr float kPrune = 1e-3f;
+// The inner log needs CUDA's logf (<= 1 ulp): for u -> 1, t = -log u -> 6e-8 and an
+// absolute-error log (__logf: 2^-21.4 on [0.5, 2]) would be far off exactly where the
+// largest Gumbel values (the likely winners) are.  The outer one takes __logf (MUFU):
+// |log t| <= 16.7, error <= 2^-21.4 absolute on [0.5, 2], <= 3 ulp elsewhere -- so
+// |g_fast - g| < 1e-5 still (1 ulp of t -> 1.2e-7, + <= 5.7e-6), far inside kPrune.
 static __device__ __forceinline__ float gumbel_fast(uint32_t x) {
   const float u = ((float)(x >> 9) * 2.0f + 1.0f) * 5.9604644775390625e-08f;  // exact (24-bit integer * 2^-24)
-  return -logf(-logf(u));
+  return -__logf(-logf(u));
 }
 
 static __device__ __forceinline__ bool better(float s, int j, float bs, int bj) {

@@ -40,16 +40,31 @@ __global__ void __launch_bounds__(kSampThreads) sample_kernel(SampleArgs a) {
   float bs = -INFINITY;
   int bj = 0x7fffffff;
   float mx = -INFINITY, sum = 0.f;
+  // the logits of the next group of 4 are loaded one iteration ahead (float4 when the
+  // row is 16-byte aligned): their latency overlaps this group's Philox and logs
+  // instead of stalling every iteration
+  const bool vec = (a.V & 3) == 0;
+  auto load4 = [&](int j4) -> float4 {
+    if (vec && j4 + 3 < a.V) return __ldg(reinterpret_cast<const float4*>(z + j4));
+    float t[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) t[q] = j4 + q < a.V ? __ldg(z + j4 + q) : 0.f;
+    return make_float4(t[0], t[1], t[2], t[3]);
+  };
+  float4 znext = threadIdx.x * 4 < a.V ? load4(threadIdx.x * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
   for (int j4 = threadIdx.x * 4; j4 < a.V; j4 += kSampThreads * 4) {
+    const float4 zc = znext;
+    if (j4 + kSampThreads * 4 < a.V) znext = load4(j4 + kSampThreads * 4);
+    const float zv[4] = {zc.x, zc.y, zc.z, zc.w};
     const uint4 w = philox4x32_10(make_uint4((uint32_t)(j4 >> 2), n, traj, rs), key);
     const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int j = j4 + q;
       if (j < a.V) {
-        const float zs = __fmul_rn(z[j], invT);
-        // Exact score only where it could win: g_fast (CUDA logf, <= 1 ulp each)
-        // is within 1e-5 of the RN msun value for u in [2^-24, 1 - 2^-24] (|g| <= 16.6),
+        const float zs = __fmul_rn(zv[q], invT);
+        // Exact score only where it could win: g_fast (CUDA logf inside, __logf
+        // outside: gumbel.cuh) is within 1e-5 of the RN msun value for u in [2^-24, 1 - 2^-24] (|g| <= 16.6),
         // so zs + g_fast + kPrune < bs proves exact(s) < bs.  The decision is
         // unchanged; most of the V - 1 losers skip the two RN-only logs.
         if (__fadd_rn(zs, gumbel_fast(ws[q])) + kPrune + 1e-6f * fabsf(bs) >= bs) {
