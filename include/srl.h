@@ -228,16 +228,17 @@ int32_t srl_arena_sizes(const srl_model_cfg* m, const srl_sched_cfg* s, int32_t 
  * "L<i>.wv", "L<i>.bq", "L<i>.bk", "L<i>.bv", "L<i>.wo", "L<i>.attn_norm",
  * "L<i>.mlp_norm", "L<i>.wg", "L<i>.wu", "L<i>.wd"), bf16, in the shape of a
  * linear layer's weight [out, in].  Returns -1 if unknown.  All tensors are
- * dense row-major EXCEPT wg / wu, whose rows are interleaved in 64-row blocks
+ * dense row-major EXCEPT wg / wu, whose rows are interleaved in 16-row blocks
  * (see srl_weight_layout). */
 int64_t srl_weight_offset(const srl_model_cfg* m, const char* name, int64_t* numel);
 
 /* Full placement of a named tensor: row i (of `rows`, each `cols` bf16 elements)
  * starts at byte offset + ((i / row_block) * block_stride + i % row_block) * cols * 2.
  * Dense tensors have row_block = block_stride = rows.  L<i>.wg / L<i>.wu have
- * row_block = 64, block_stride = 128: each 128-row block of the gate/up region
- * holds 64 gate rows followed by the 64 up rows of the same outputs, so one
- * 128-row tensor-core tile carries both operands of the fused SiLU-mul. */
+ * row_block = 16, block_stride = 32: each 32-row block of the gate/up region
+ * holds 16 gate rows followed by the 16 up rows of the same outputs, so one
+ * 128-row tensor-core tile carries both operands of the fused SiLU-mul and each
+ * warp's 32 accumulator lanes hold both operands of 16 outputs. */
 int32_t srl_weight_layout(const srl_model_cfg* m, const char* name, int64_t* offset, int64_t* rows, int64_t* cols,
                           int64_t* row_block, int64_t* block_stride);
 
@@ -296,7 +297,7 @@ int32_t srl_load_policy_weights(srl_engine* e, const void* flat_w, int64_t versi
  * row-major [rows, cols] bf16 (the srl_weight_layout shape; wg / wu plain, not
  * interleaved): projection matrices are packed straight into the GEMM's weight
  * stream (for wq / wk / wv into their tile range of the fused QKV matrix, for
- * wg / wu into their 64-row interleave), the others are copied.  The source is
+ * wg / wu into their 16-row interleave), the others are copied.  The source is
  * read on the engine stream; the caller keeps it alive until the next
  * synchronising call.  Then srl_load_policy_weights(e, NULL, version) makes the
  * installed tensors the new policy (and broadcasts them from rank 0).  Works

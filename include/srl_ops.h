@@ -27,9 +27,10 @@ extern "C" {
  *   order: bit-reproducible), and
  *   epi = 0: out fp32 [M, N]  = Y
  *   epi = 1: out fp32 [M, N] += Y                       (residual add)
- *   epi = 2: W has 2N rows, gate and up rows interleaved in 64-row blocks (rows
- *            [128b, 128b+64) = gate rows [64b, 64b+64), rows [128b+64, 128b+128) =
- *            the matching up rows); out bf16 [M, N] = silu(Yg) * Yu
+ *   epi = 2: W has 2N rows, gate and up rows interleaved in 16-row blocks (rows
+ *            [32b, 32b+16) = gate rows [16b, 16b+16), rows [32b+16, 32b+32) = the
+ *            matching up rows: within a warp's 32 accumulator lanes the two operands
+ *            of an output sit 16 lanes apart); out bf16 [M, N] = silu(Yg) * Yu
  * epi | SRL_GEMM_W_PACKED: W is in the packed layout written by srl_op_pack_weight
  *   (for epi 2: the packed image of the interleaved [2N, K] matrix) instead of
  *   row-major; the weight stream then moves contiguous 16 KB blocks.
@@ -51,8 +52,8 @@ int32_t srl_op_gemm_bf16(const void* X, int32_t M, const void* W, int32_t N, int
  *        `splits` equal k-ranges ks of ff               (a9: the down GEMM, k-split)
  * so that sum_s part[s] (in s order) = act Wd^T; the engine's next RMSNorm sums
  * them and adds the residual.  X [M, d] bf16 row-major; Wgu_packed = the packed
- * image (srl_op_pack_weight) of the interleaved [2ff, d] gate/up matrix (64 gate
- * rows then the matching 64 up rows per 128-row block, as epi 2 above); Wd_packed
+ * image (srl_op_pack_weight) of the interleaved [2ff, d] gate/up matrix (16 gate
+ * rows then the matching 16 up rows per 32-row block, as epi 2 above); Wd_packed
  * = the packed image of Wd [d, ff].  workspace as srl_op_gemm_workspace (zeroed
  * before first use, left zeroed).  The down k-split s starts as soon as the
  * gate/up tiles producing its act columns are stored (device-scope counters).

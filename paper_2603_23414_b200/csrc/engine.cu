@@ -72,12 +72,14 @@ struct WeightLayout {
     }
     total = al(off);
   }
-  // gate / up rows interleaved in 64-row blocks: one 128-row GEMM tile holds the
-  // gate and up rows of the same 64 outputs (fused SiLU-mul epilogue)
+  // gate / up rows interleaved in kGuBlock-row blocks: one 128-row GEMM tile holds the
+  // gate and up rows of the same 64 outputs, each warp's 32 rows those of 16 outputs
+  // (fused SiLU-mul epilogue, gemm_epi.cuh)
   void add_gate_up(const std::string& g, const std::string& u, size_t ff, size_t cols) {
     const size_t o = compact ? kNoOff : total;
-    ents.push_back({g, o, ff * cols, ff, cols, 64, 128});
-    ents.push_back({u, compact ? kNoOff : total + 64 * cols * 2, ff * cols, ff, cols, 64, 128});
+    ents.push_back({g, o, ff * cols, ff, cols, (size_t)kGuBlock, 2 * (size_t)kGuBlock});
+    ents.push_back({u, compact ? kNoOff : total + kGuBlock * cols * 2, ff * cols, ff, cols, (size_t)kGuBlock,
+                    2 * (size_t)kGuBlock});
     if (!compact) total += al(2 * ff * cols * 2);
   }
   const Ent* find(const std::string& n) const {
@@ -1434,8 +1436,8 @@ extern "C" int32_t srl_load_policy_tensor(srl_engine* e, const char* name, const
     else if (t == "wv") rc = pack_weight(s, kd, m.d, w.pqkv + (size_t)((qd + kd) / 128) * kbq * tile, e->st);
     else if (t == "wo") rc = pack_weight(s, m.d, qd, w.po, e->st);
     else if (t == "wd") rc = pack_weight(s, m.d, m.ff, w.pd, e->st);
-    else if (t == "wg") rc = pack_weight_rows(s, m.ff, m.d, w.pgu, 64, 128, 0, e->st);
-    else if (t == "wu") rc = pack_weight_rows(s, m.ff, m.d, w.pgu, 64, 128, 64, e->st);
+    else if (t == "wg") rc = pack_weight_rows(s, m.ff, m.d, w.pgu, kGuBlock, 2 * kGuBlock, 0, e->st);
+    else if (t == "wu") rc = pack_weight_rows(s, m.ff, m.d, w.pgu, kGuBlock, 2 * kGuBlock, kGuBlock, e->st);
     else return fail(SRL_E_INVALID_ARG, "srl_load_policy_tensor: not loadable: " + n);
   }
   if (is_packed_tensor(n) && !e->m.weights_compact && en->off != kNoOff) {

@@ -1,11 +1,13 @@
 // gemm_epi.cuh — fused GEMM epilogues (included by gemm_tc.cu after GemmParams).
 //
 // A 16-column chunk of the accumulator arrives one weight row per thread
-// (thread n <-> TMEM lane n, 16 batch rows in registers).  Every epilogue first
+// (thread n <-> TMEM lane n, 16 batch rows in registers).  The SiLU-mul pairs the
+// gate and up rows of an output with one warp shuffle (kGuBlock interleave: lanes l
+// and l + 16 of a warp) and needs no exchange.  Every other epilogue first
 // transposes the chunk through shared memory so that thread t then owns batch
-// row m0 + t/8 and a run of 16 consecutive weight rows (8 outputs for SiLU):
-// the global writes become 16- or 64-byte vectors along the contiguous output
-// dimension instead of 2- or 4-byte scalars strided by the row pitch.
+// row m0 + t/8 and a run of 16 consecutive weight rows: the global writes become
+// 16- or 64-byte vectors along the contiguous output dimension instead of 2- or
+// 4-byte scalars strided by the row pitch.
 #pragma once
 
 // named barrier of one epilogue group (4 warps covering the 128 TMEM lanes)
@@ -92,6 +94,26 @@ __device__ __forceinline__ void rope_prefetch(const GemmParams& p, int unit_n0, 
 __device__ __forceinline__ void apply_epilogue(const GemmParams& p, int unit_n0, int n, int m0, const float (&v)[16],
                                                float* xch, int bar, const int* rtab, const RopePre* pre = nullptr) {
   const GemmEpi& e = p.epi;
+  if (e.kind == EPI_SILU) {
+    // kGuBlock = 16 interleave: lane l < 16 holds gate row j = l of this warp's 16
+    // outputs, lane l + 16 the up row of the same output.  Lane l computes batch rows
+    // m0 .. m0+7 of output j, lane l + 16 rows m0+8 .. m0+15: each sends the partner
+    // the 8 values it needs (one xor-16 shuffle each).
+    static_assert(kGuBlock == 16, "the epilogue pairs lanes l and l + 16");
+    const int l = n & 31;
+    const bool up = l >= 16;
+    const int o = (unit_n0 >> 1) + (n >> 5) * 16 + (l & 15);  // act column (output)
+    const int mb = m0 + (up ? 8 : 0);
+    __nv_bfloat16* dst = e.act + (size_t)mb * e.ldo + o;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float mine = up ? v[8 + k] : v[k];
+      const float other = __shfl_xor_sync(0xffffffffu, up ? v[k] : v[8 + k], 16);
+      const float a = up ? silu_mul(other, mine) : silu_mul(mine, other);
+      if (mb + k < p.M) dst[(size_t)k * e.ldo] = __float2bfloat16_rn(a);
+    }
+    return;
+  }
   const int* spos = rtab;
   const int* spage = rtab + 256;
 #pragma unroll
@@ -100,25 +122,7 @@ __device__ __forceinline__ void apply_epilogue(const GemmParams& p, int unit_n0,
   const int ml = n >> 3;  // batch row within the chunk owned from here on
   const int m = m0 + ml;
   const float* row = xch + ml * kXchPitch;
-  if (e.kind == EPI_SILU) {
-    // 64-row interleave: tile rows [0,64) are gate rows, [64,128) the up rows of
-    // the same 64 outputs; thread owns outputs ob..ob+7 of this tile
-    const int ob = (n & 7) * 8;
-    if (m < p.M) {
-      float g[8], u[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        g[k] = row[ob + k];
-        u[k] = row[64 + ob + k];
-      }
-      uint4 pk;
-      pk.x = pack_bf16(silu_mul(g[0], u[0]), silu_mul(g[1], u[1]));
-      pk.y = pack_bf16(silu_mul(g[2], u[2]), silu_mul(g[3], u[3]));
-      pk.z = pack_bf16(silu_mul(g[4], u[4]), silu_mul(g[5], u[5]));
-      pk.w = pack_bf16(silu_mul(g[6], u[6]), silu_mul(g[7], u[7]));
-      *reinterpret_cast<uint4*>(e.act + (size_t)m * e.ldo + (unit_n0 >> 1) + ob) = pk;
-    }
-  } else {
+  {
     const int nb = (n & 7) * 16;  // first of the thread's 16 weight rows
     const int ng0 = unit_n0 + nb;
     float r[16];

@@ -9,7 +9,7 @@
 //   EPI_F32   out[m][n] = Y                             (LM-head logits, op tests)
 //   EPI_RESID x_res[m][n] += Y                           (O and down projections)
 //   EPI_SILU  act[m][j] = silu(Yg[m][j]) * Yu[m][j]      (gate/up rows interleaved in
-//             64-row blocks, so one 128-row tile holds both operands)
+//             16-row blocks, so one 128-row tile -- one warp's 32 lanes -- holds both operands)
 //   EPI_QKV   (+bias), RoPE on q/k at the row's position, q -> q buffer, k/v ->
 //             the paged KV cache (page_table[slot][pos/64], row pos%64)
 //

@@ -50,6 +50,11 @@ struct GemmEpi {
   void* ws;
 };
 
+// gate / up row interleave of the SiLU-mul GEMM (EPI_SILU): blocks of kGuBlock gate
+// rows then the kGuBlock up rows of the same outputs, so in every 32-row warp slice
+// of a 128-row tile lanes l and l + 16 hold the two operands of one output (the
+// epilogue pairs them with one shuffle, no shared-memory exchange)
+constexpr int kGuBlock = 16;
 constexpr size_t kSkSlotBytes = 128 * 256 * 4;  // one CTA's fp32 partial: 128 rows x <= 256 batch columns
 constexpr int kSkMaxUnits = 8192;               // stream-K counters: pair units per launch
 size_t gemm_workspace_bytes(int num_sms);
@@ -59,8 +64,8 @@ int gemm_partial_split(int M, int N, int K, int num_sms);
 
 // ---- gemm_tc.cu
 // Y = X[M,K] . W[N,K]^T with the fused epilogue `epi` (for EPI_SILU, W's
-// N rows are the interleaved gate/up rows: 64 gate rows, then the matching 64 up
-// rows, per 128-row block).  One kernel launch, no workspace: split-K partials
+// N rows are the interleaved gate/up rows: kGuBlock gate rows, then the matching
+// kGuBlock up rows, per 2 kGuBlock-row block).  One kernel launch, no workspace: split-K partials
 // are reduced over distributed shared memory inside a thread-block cluster.
 // Returns 0, -1 (bad shape) or -2/-3 (TMA encode / launch failure).
 int gemm_bf16_fused(const __nv_bfloat16* X, int M, const __nv_bfloat16* W, int N, int K, const GemmEpi& epi,

@@ -170,7 +170,7 @@ class RolloutEngine:
     # ------------------------------------------------------------------ weights
     def weight_view(self, name: str):
         """bf16 view of a named tensor in the flat weight region: [rows, cols] for dense
-        tensors, [rows/64, 64, cols] for the block-interleaved gate/up weights."""
+        tensors, [rows/16, 16, cols] for the block-interleaved gate/up weights."""
         off, rows, cols, rb, bs = (C.c_int64() for _ in range(5))
         if self.lib.srl_weight_layout(C.byref(self.m), name.encode(), C.byref(off), C.byref(rows), C.byref(cols),
                                       C.byref(rb), C.byref(bs)) != 0:

@@ -111,8 +111,8 @@ def test_gemm_silu_mul_epilogue(lib, M, N, K, packed):
     X = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
     Wg = (torch.randn(N, K, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
     Wu = (torch.randn(N, K, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
-    # 64-row block interleave of gate / up rows (srl_ops.h)
-    W = torch.stack([Wg.view(N // 64, 64, K), Wu.view(N // 64, 64, K)], dim=1).reshape(2 * N, K).contiguous()
+    # 16-row block interleave of gate / up rows (srl_ops.h)
+    W = torch.stack([Wg.view(N // 16, 16, K), Wu.view(N // 16, 16, K)], dim=1).reshape(2 * N, K).contiguous()
     out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     assert _gemm(lib, X, W, N, 2, out, packed) == 0
     gte, up = X.double() @ Wg.double().t(), X.double() @ Wu.double().t()
@@ -164,7 +164,7 @@ def test_mlp_fused_matches_unfused_and_fp64(lib, M, d, ff, splits):
     Wg = (torch.randn(ff, d, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
     Wu = (torch.randn(ff, d, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
     Wd = (torch.randn(d, ff, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
-    W = torch.stack([Wg.view(ff // 64, 64, d), Wu.view(ff // 64, 64, d)], dim=1).reshape(2 * ff, d).contiguous()
+    W = torch.stack([Wg.view(ff // 16, 16, d), Wu.view(ff // 16, 16, d)], dim=1).reshape(2 * ff, d).contiguous()
     Wgu_p, Wd_p = _pack(lib, W), _pack(lib, Wd)
     ws = torch.zeros(lib.srl_op_gemm_workspace(M, d, ff, 1), dtype=torch.uint8, device="cuda")
     outs = []
