@@ -407,6 +407,7 @@ __device__ __forceinline__ void gemm_pair_body(const CUtensorMap& tmW, const CUt
             tmem_ld16(tlh + cc, v);
             apply_epilogue(p, n0, n, m_base + cc, v, xg, 1 + eg, rtab + cc);
           }
+          if (lane == 0 && qw == 0 && eg == 0 && i == 0 && h == 0) DBG(15);  // (profiling) half 0 done
         }
       } else {
         // stream-K piece of a split unit: fp32 partial -> workspace slot (layout

@@ -1,0 +1,3 @@
+cd $GRAFT_REPO_ROOT
+timeout 300 python tools/gemm_timeline.py op 256 14336 4096 2 2>&1 | tail -20
+timeout 300 python tools/gemm_timeline.py op 256 4096 4096 1 2>&1 | tail -20
