@@ -372,7 +372,8 @@ typedef struct srl_tuning {
   int32_t fuse_mlp;        /* 1: gate/up and down GEMMs as one persistent kernel (128 <= M <= 256);
                               measured r02 equal to the two PDL-chained GEMMs, off */
   int32_t mlp_splits;      /* k-splits of the fused down GEMM (its partials go to the next RMSNorm), 1..8 */
-  int32_t attn_stages;     /* attention K/V ring depth: 4 (default) or 6 (dh = 128) */
+  int32_t attn_stages;     /* attention K/V ring depth: 4 (default) or 6 (dh = 128); 3 (dh = 128): two
+                              CTAs per SM when G = Hq / Hkv <= 4 fits both in shared memory */
   int32_t qkv_attn;        /* 1 (default): pure decode passes leave QKV split-K partials to the attention
                               kernel, whose finish warp completes q / k / v per item (bias, RoPE, KV
                               append) ahead of its TMA producer */

@@ -440,10 +440,15 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stages = smem;
-  float* mrg = reinterpret_cast<float*>(stages + kStages * C::kStageBytes);  // [4 warps][8 q][DH + 2]
+  float* mrg = reinterpret_cast<float*>(stages + kStages * C::kStageBytes);  // [4 warps][G q][DH + 2]
   pdl_trigger();
   pdl_wait();
-  uint64_t* full = reinterpret_cast<uint64_t*>(mrg + kConsumerWarps * 8 * (DH + 2));
+  const int G = a.Hq / a.Hkv;
+  // merge-buffer rows per warp: the 8-wide MMA N side, or (the 2-CTA-per-SM ring) only
+  // the G real query heads; it is also the split-KV merge's scratch (3 nch G floats,
+  // capacity checked at launch)
+  const int MR = kStages == 3 ? G : 8;
+  uint64_t* full = reinterpret_cast<uint64_t*>(mrg + kConsumerWarps * MR * (DH + 2));
   uint64_t* empty = full + kStages;
   volatile int* hdr = reinterpret_cast<volatile int*>(empty + kStages);  // [kStages] item of each staged page
   volatile int* merge_flag = hdr + kStages;
@@ -451,7 +456,6 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
   __shared__ uint64_t fq_full[kFQ], fq_empty[kFQ];
   __shared__ int fq_item[kFQ];
 
-  const int G = a.Hq / a.Hkv;
   const int w = warp_id(), lane = lane_id();
   const int n_items = *a.n_items;
   const bool fin = a.qkv_part != nullptr;
@@ -652,31 +656,41 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       if (lane == 0) mbar_arrive(&empty[s]);
     }
     // ---- merge the 4 warps' partial states (columns c0 = 2*(lane&3), c1 = c0+1)
-    float* my = mrg + w * 8 * (DH + 2);
+    // (rows >= G of the 8-wide MMA N side are padding: never stored)
+    float* my = mrg + w * MR * (DH + 2);
     const int c0 = 2 * (lane & 3);
+    const bool r0 = c0 < G, r1 = c0 + 1 < G;
     if ((lane >> 2) == 0) {
-      my[c0 * (DH + 2) + DH] = m0;
-      my[c0 * (DH + 2) + DH + 1] = l0;
-      my[(c0 + 1) * (DH + 2) + DH] = m1;
-      my[(c0 + 1) * (DH + 2) + DH + 1] = l1;
+      if (r0) {
+        my[c0 * (DH + 2) + DH] = m0;
+        my[c0 * (DH + 2) + DH + 1] = l0;
+      }
+      if (r1) {
+        my[(c0 + 1) * (DH + 2) + DH] = m1;
+        my[(c0 + 1) * (DH + 2) + DH + 1] = l1;
+      }
     }
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
       const int d = mt * 16 + (lane >> 2);
-      my[c0 * (DH + 2) + d] = o[mt][0];
-      my[(c0 + 1) * (DH + 2) + d] = o[mt][1];
-      my[c0 * (DH + 2) + d + 8] = o[mt][2];
-      my[(c0 + 1) * (DH + 2) + d + 8] = o[mt][3];
+      if (r0) {
+        my[c0 * (DH + 2) + d] = o[mt][0];
+        my[c0 * (DH + 2) + d + 8] = o[mt][2];
+      }
+      if (r1) {
+        my[(c0 + 1) * (DH + 2) + d] = o[mt][1];
+        my[(c0 + 1) * (DH + 2) + d + 8] = o[mt][3];
+      }
     }
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32));
     const bool single = a.row_nchunk[ii.m] == 1;
     for (int i = threadIdx.x; i < G * DH; i += kConsumerWarps * 32) {
       const int g = i / DH, d = i % DH;
       float mx = -INFINITY;
-      for (int ww = 0; ww < kConsumerWarps; ++ww) mx = fmaxf(mx, mrg[(ww * 8 + g) * (DH + 2) + DH]);
+      for (int ww = 0; ww < kConsumerWarps; ++ww) mx = fmaxf(mx, mrg[(ww * MR + g) * (DH + 2) + DH]);
       float acc = 0.f, l = 0.f;
       for (int ww = 0; ww < kConsumerWarps; ++ww) {
-        const float* e = mrg + (ww * 8 + g) * (DH + 2);
+        const float* e = mrg + (ww * MR + g) * (DH + 2);
         const float f = e[DH] == -INFINITY ? 0.f : exp2f(e[DH] - mx);
         acc += e[d] * f;
         l += e[DH + 1] * f;
@@ -765,7 +779,8 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
 template <int DH, int NS>
 static void launch_bf16_ns(const AttnArgs& a, const void* tk, const void* tv, cudaStream_t st, int once_slot) {
   using C = AttnCfg<DH>;
-  const size_t smem = 1024 + NS * C::kStageBytes + kConsumerWarps * 8 * (DH + 2) * 4 + 2 * NS * 8 + 64;
+  const int G = a.Hq / a.Hkv, MR = NS == 3 ? G : 8;
+  const size_t smem = 1024 + NS * C::kStageBytes + (size_t)kConsumerWarps * MR * (DH + 2) * 4 + 2 * NS * 8 + 64;
   if (once_per_device(once_slot))  // per-device attribute
     cudaFuncSetAttribute(attn_bf16_kernel<DH, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int grid = 148;
@@ -780,6 +795,11 @@ static void launch_bf16(const AttnArgs& a, const void* tk, const void* tv, cudaS
   const int slot = DH == 128 ? kOnceAttn128 : (DH == 64 ? kOnceAttn64 : kOnceAttn32);
   if (tuning().attn_stages == 6 && DH == 128)
     launch_bf16_ns<DH, 6>(a, tk, tv, st, kOnceAttn128s6);
+  else if (tuning().attn_stages == 3 && DH == 128 && a.Hq / a.Hkv <= 4 &&
+           3 * (a.max_pages / kChunkPages + 1) <= kConsumerWarps * (DH + 2))
+    // 3 x 32 KB stages and a G-row merge buffer: two CTAs per SM (the split-KV merge
+    // scratch, 3 nch G floats, fits the 4 G (DH + 2) of the buffer)
+    launch_bf16_ns<DH, 3>(a, tk, tv, st, kOnceAttn128s3);
   else
     launch_bf16_ns<DH, kStagesDefault>(a, tk, tv, st, slot);
 }

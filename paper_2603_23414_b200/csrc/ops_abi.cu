@@ -62,7 +62,7 @@ extern "C" int32_t srl_set_tuning(const srl_tuning* t) {
   if (t->gemm_split < 0 || t->gemm_split > 3 || t->gemm_pair < -1 || t->gemm_pair > 1 || t->gemm_h < 0 ||
       t->gemm_h > 2 || t->gemm_stages < 0 || t->gemm_xstages < 0 || t->attn_min_items < 0 ||
       t->attn_target_items < 0 || t->attn_l2_prefetch < 0 || t->attn_l2_prefetch > 16 || t->mlp_splits < 1 ||
-      t->mlp_splits > 8 || (t->attn_stages != 4 && t->attn_stages != 6) || t->pair_h2 < 0 || t->pair_h2 > 1) {
+      t->mlp_splits > 8 || (t->attn_stages != 3 && t->attn_stages != 4 && t->attn_stages != 6) || t->pair_h2 < 0 || t->pair_h2 > 1) {
     set_error("srl_set_tuning: %s", "field out of range", 0);
     return -1;
   }

@@ -12,5 +12,6 @@ inline const srl_tuning& tuning() { return g_tuning; }
 // returns true exactly once per (slot, current device)
 bool once_per_device(int slot);
 enum { kOnceGemmPair = 0, kOnceGemmSingle = 1, kOnceAttn32 = 2, kOnceAttn64 = 3, kOnceAttn128 = 4,
-       kOnceCtl = 5, kOnceSample = 6, kOnceGemmMlp = 7, kOnceAttn128s6 = 8, kOnceSlots = 9 };
+       kOnceCtl = 5, kOnceSample = 6, kOnceGemmMlp = 7, kOnceAttn128s6 = 8, kOnceAttn128s3 = 9,
+       kOnceSlots = 10 };
 }  // namespace srl

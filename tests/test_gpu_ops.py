@@ -453,3 +453,19 @@ def test_sampler_truncated_rejects_bad_args(lib):
     assert lib.srl_op_sample_trunc(0, 1, 16, 0, 0, 0, 1.0, 3, -1, 1.0, 0, 0, 0, _stream()) < 0
     assert lib.srl_op_sample_trunc(0, 1, 16, 0, 0, 0, 1.0, 3, 0, 0.0, 0, 0, 0, _stream()) < 0
     assert lib.srl_op_sample_trunc(0, 1, 16, 0, 0, 0, 1.0, 3, 0, 1.5, 0, 0, 0, _stream()) < 0
+
+
+def test_attention_two_ctas_per_sm_ring():
+    """srl_tuning.attn_stages = 3 (dh = 128, G <= 4): a 3-stage ring and a G-row merge
+    buffer, so two attention CTAs share each SM -- the bf16 attention parity tests
+    (per-element derived bound, split-KV long contexts, inactive rows) pass unchanged.
+    Subprocess: the harness applies the setting at session start (tests/conftest.py)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SRL_TEST_TUNING="attn_stages=3")
+    out = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "tests/test_gpu_ops.py",
+                          "-k", "attention_bf16 or inactive_rows"],
+                         cwd=root, capture_output=True, text=True, env=env, timeout=900)
+    assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
