@@ -601,13 +601,17 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const int tok0 = w * 16;
       const int tbase = p * 64 + tok0;  // absolute position of the warp's first token
       if (tbase < ii.ctx) {
-        float sacc[4] = {0.f, 0.f, 0.f, 0.f};
+        // two accumulators (even / odd 16-dim tiles): half the dependent MMA chain
+        float sacc[4] = {0.f, 0.f, 0.f, 0.f}, sodd[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int kk = 0; kk < MT; ++kk) {
           uint32_t a0, a1, a2, a3;
           ldmatrix_x4(kv_addr<DH>(kb, tok0 + (lane & 15), 2 * kk + (lane >> 4)), a0, a1, a2, a3);
-          mma_bf16_16816(sacc, a0, a1, a2, a3, bq[kk][0], bq[kk][1]);
+          if (kk & 1) mma_bf16_16816(sodd, a0, a1, a2, a3, bq[kk][0], bq[kk][1]);
+          else mma_bf16_16816(sacc, a0, a1, a2, a3, bq[kk][0], bq[kk][1]);
         }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sacc[j] += sodd[j];
         // sacc: [0]=(tok r, q c0) [1]=(tok r, q c1) [2]=(tok r+8, q c0) [3]=(tok r+8, q c1)
         const int r = lane >> 2;
         const bool v0 = tbase + r < ii.ctx, v1 = tbase + r + 8 < ii.ctx;
@@ -625,14 +629,10 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         const float al0 = m0 == -INFINITY ? 0.f : exp2f(m0 - nm0);
         const float al1 = m1 == -INFINITY ? 0.f : exp2f(m1 - nm1);
         const float p0 = exp2f(x0 - nm0), p1 = exp2f(x1 - nm1), p2 = exp2f(x2 - nm0), p3 = exp2f(x3 - nm1);
-        float s0 = p0 + p2, s1 = p1 + p3;
-#pragma unroll
-        for (int off = 4; off < 32; off <<= 1) {
-          s0 += __shfl_xor_sync(0xffffffffu, s0, off);
-          s1 += __shfl_xor_sync(0xffffffffu, s1, off);
-        }
-        l0 = l0 * al0 + s0;
-        l1 = l1 * al1 + s1;
+        // running sums stay per lane (the rescale factors are uniform over the 8 lanes
+        // of a query column); reduced across the lanes once, at the end of the item
+        l0 = l0 * al0 + (p0 + p2);
+        l1 = l1 * al1 + (p1 + p3);
         m0 = nm0;
         m1 = nm1;
 #pragma unroll
@@ -654,6 +654,11 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+    }
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, off);
     }
     // ---- merge the 4 warps' partial states (columns c0 = 2*(lane&3), c1 = c0+1)
     // (rows >= G of the 8-wide MMA N side are padding: never stored)
