@@ -287,4 +287,3 @@ def test_fullwidth_fused_kernel_paths():
                           "tests/test_gpu_fullwidth.py::test_fullwidth_teacher_forced[llama8b-L2-Q256]"],
                          cwd=root, capture_output=True, text=True, env=env, timeout=1200)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-2000:]
-
