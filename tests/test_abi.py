@@ -147,6 +147,44 @@ def test_tuning_roundtrip_and_validation(lib):
     assert _lib.get_tuning() == d
 
 
+def test_gate_up_staging_interleave_on_cpu(lib):
+    """srl.h srl_weight_layout: L<i>.wg / L<i>.wu rows interleaved in 16-row blocks
+    (row_block 16, block_stride 32, wu 16 rows after wg) -- the layout the SiLU-mul
+    epilogue pairs with one xor-16 shuffle; every other tensor dense row-major."""
+    from paper_2603_23414_b200 import _lib
+    from workload.configs import LLAMA8B
+    L = _lib.load()
+    m = _lib.ModelCfg(LLAMA8B.L, LLAMA8B.d, LLAMA8B.Hq, LLAMA8B.Hkv, LLAMA8B.dh, LLAMA8B.ff, LLAMA8B.V, 5e5, 1e-5, 0)
+    v = [ctypes.c_int64() for _ in range(5)]
+
+    def lay(name):
+        assert L.srl_weight_layout(ctypes.byref(m), name, *[ctypes.byref(x) for x in v]) == 0
+        return [x.value for x in v]
+    og, rg, cg, rbg, bsg = lay(b"L5.wg")
+    ou, ru, cu, rbu, bsu = lay(b"L5.wu")
+    assert (rg, cg, rbg, bsg) == (LLAMA8B.ff, LLAMA8B.d, 16, 32) and (ru, cu, rbu, bsu) == (rg, cg, 16, 32)
+    assert ou - og == 16 * LLAMA8B.d * 2
+    od, rd, cd, rbd, bsd = lay(b"L5.wd")
+    assert (rd, cd) == (LLAMA8B.d, LLAMA8B.ff) and rbd == bsd == rd
+    assert od >= og + 2 * LLAMA8B.ff * LLAMA8B.d * 2   # wd after the whole interleaved region
+
+
+def test_tuning_defaults_of_the_r02_kernels(lib):
+    """The production choices measured in r02: 512-row gate/up pair units
+    on, the QKV finish inside attention on, the 4-stage attention ring, the fused MLP off;
+    attn_stages accepts 3 / 4 / 6 only."""
+    from paper_2603_23414_b200 import _lib
+    d = _lib.get_tuning()
+    assert d["pair_h2"] == 1 and d["qkv_attn"] == 1 and d["attn_stages"] == 4 and d["fuse_mlp"] == 0
+    for bad in (dict(attn_stages=5), dict(pair_h2=2)):
+        with pytest.raises(_lib.SRLError):
+            _lib.set_tuning(**bad)
+        assert _lib.get_tuning() == d
+    old = _lib.set_tuning(attn_stages=3)
+    _lib.set_tuning(**old)
+    assert _lib.get_tuning() == d
+
+
 def test_library_reads_no_environment():
     """No getenv in the product library (the knobs moved to srl_tuning)."""
     import glob
